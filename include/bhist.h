@@ -1,0 +1,155 @@
+/* bhist.h — C ABI of libbhist: B200-native (sm_100a) bulk histogram filling.
+ *
+ * The operation (arXiv 2401.13310, §3.1): filling a histogram
+ * with a bulk of events is three steps per event — (1) find the bin from the
+ * coordinate(s), (2) increment that bin by one or by the event weight, (3) update
+ * the statistics sums.  The paper's GPU version keeps the histogram in device
+ * memory across bulks (RHnCUDA), "transfers bulk of events to the
+ * GPU and launches kernels ... per bulk", and copies the result back "once all
+ * bulks have been processed".  This header exposes exactly that
+ * life cycle: create from axes, fill bulks on a stream, read back bins and stats.
+ *
+ * Conventions (DESIGN.md "Readings" R1–R17 give the paper passages):
+ *  - Axis bins: 0 = underflow, 1..nbins in range, nbins+1 = overflow.
+ *    Fixed axis: b = 1 + (int)((nbins*(x-xmin))/(xmax-xmin)) in IEEE binary64
+ *    with that association (R2); x < xmin -> 0; !(x < xmax) -> nbins+1 (so
+ *    x == xmax and NaN go to overflow, R5).  Variable axis: b = number of edges
+ *    <= x (half-open [e_{i-1}, e_i), R1), with the same flow routing.
+ *  - Global bin: g = b0 + (n0+2)*(b1 + (n1+2)*b2), axis 0 fastest (R9).
+ *  - Per bin: content = sum of w, sumw2 = sum of w*w (w = 1 for unit fills).
+ *  - Stats (ROOT GetStats order, R7/R8), over events whose bin is in range on
+ *    every axis (R6):  1D [sumw, sumw2, sumwx, sumwx2]
+ *                      2D + [sumwy, sumwy2, sumwxy]
+ *                      3D + [sumwz, sumwz2, sumwxz, sumwyz]
+ *  - entries += n for every fill (all events, flow included).
+ *  - Fills accumulate into the existing state (include-initial).
+ *
+ * Ownership: the library owns all histogram storage (allocated on `device` at
+ * bh_create, freed at bh_destroy).  Input buffers are borrowed: device pointers
+ * must stay valid and unmodified until the stream has executed the fill.
+ * Streams: `bh_stream` is a cudaStream_t passed as an opaque pointer (NULL = the
+ * legacy default stream).  No call synchronizes the device; bh_read synchronizes
+ * only its stream; bh_fill_host waits only for its own host->device copies.  A
+ * histogram is single-writer: issue its fills on one stream at a time.
+ * Errors: every call returns a bh_status; no exception crosses the ABI;
+ * bh_last_error() gives a thread-local message for the last failure.  NaN/inf
+ * coordinates and any weight value are not errors.  Asynchronous kernel faults
+ * surface as BH_ECUDA at the next call that synchronizes (bh_read).
+ */
+#ifndef BHIST_H
+#define BHIST_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bh_hist bh_hist; /* opaque; owns its device storage on one device */
+typedef void *bh_stream;        /* cudaStream_t */
+typedef int32_t bh_status;
+
+#define BH_OK 0
+#define BH_EINVAL (-1)    /* invalid argument (axes, sizes, NULL pointers, ...) */
+#define BH_ENOMEM (-2)    /* device or pinned-host allocation failed */
+#define BH_ECUDA (-3)     /* CUDA runtime error (launch, copy, asynchronous fault) */
+#define BH_EDEVICE (-4)   /* bad device ordinal / no device */
+#define BH_EMISMATCH (-5) /* incompatible histograms (bh_fill_multi) */
+
+/* One axis.  Fixed: edges == NULL, xmin < xmax finite, nbins*(xmax-xmin) finite.
+ * Variable: edges = HOST pointer to nbins+1 strictly increasing finite doubles
+ * (copied at bh_create; xmin/xmax ignored).  nbins >= 1.  The product of
+ * (nbins_a + 2) over all axes must be < 2^31. */
+typedef struct {
+    int32_t nbins;
+    double xmin;
+    double xmax;
+    const double *edges;
+} bh_axis;
+
+/* Fill strategies (bh_set_strategy).  AUTO picks by bin-space size and weights:
+ * PRIV   block-private shared-memory bins, flushed once per CTA (PAPER.md:138,
+ *        "each block fills a local copy ... in shared memory");
+ * GLOBAL device-wide atomics straight into the L2-resident histogram;
+ * CACHE  per-CTA shared-memory cache of the hottest bins with global fallback
+ *        (hot-bin contention, BASELINE.json config 4). */
+#define BH_STRATEGY_AUTO 0
+#define BH_STRATEGY_PRIV 1
+#define BH_STRATEGY_GLOBAL 2
+#define BH_STRATEGY_CACHE 3
+
+/* Debug flags (bh_set_debug) — negative controls for tests only. */
+#define BH_DEBUG_SKIP_COPY_WAIT 1 /* bh_fill_host: fill without waiting for the H2D copy (PAPER.md:223 race) */
+
+/* ABI version (major*10000 + minor*100 + patch). */
+int32_t bh_version(void);
+
+/* Thread-local, NUL-terminated message describing the last failing call ("" if none). */
+const char *bh_last_error(void);
+
+/* Create a dim-D histogram (dim in {1,2,3}) from `axes[dim]` on CUDA `device`.
+ * State starts zeroed.  *out receives the handle.  Errors: BH_EINVAL, BH_EDEVICE,
+ * BH_ENOMEM, BH_ECUDA.  Synchronous (allocations + table build). */
+bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **out);
+
+/* Free all storage.  NULL is accepted.  Synchronizes the device the histogram lives on. */
+bh_status bh_destroy(bh_hist *h);
+
+/* Zero bins, sumw2, stats and entries (stream-ordered on s). */
+bh_status bh_reset(bh_hist *h, bh_stream s);
+
+/* Fill n events (PAPER.md:126 three steps).  coords: array of `dim` DEVICE
+ * pointers, coords[a][i] = coordinate of event i on axis a (float64, SoA).
+ * w: DEVICE pointer to n float64 weights, or NULL for unit weights.  Async on s.
+ * n == 0 is a no-op.  Errors: BH_EINVAL (n < 0, NULL coords), BH_ECUDA. */
+bh_status bh_fill(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s);
+
+/* Same as bh_fill but coords/w are HOST pointers (pinned: DMA straight from them;
+ * pageable: staged by the driver).  Events are copied in chunks into a device
+ * double-buffer on an internal copy stream, overlapped with the fills on s.
+ * Returns once every host byte has been consumed (the caller may overwrite its
+ * buffers — the fix of PAPER.md:223); kernels may still be in flight on s. */
+bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s);
+
+/* Per-event global bin (parity/debug): out[i] = g(event i), int32, DEVICE pointer. */
+bh_status bh_find_bins(const bh_hist *h, int64_t n, const double *const *coords, int32_t *out, bh_stream s);
+
+/* Shape: dimension, number of bins including flow bins, number of stats (4/7/11). Any may be NULL. */
+bh_status bh_info(const bh_hist *h, int32_t *dim, int64_t *nbins_total, int32_t *nstats);
+
+/* Number of doubles in the packed state: 2*nbins_total + nstats + 1. */
+bh_status bh_packed_size(const bh_hist *h, int64_t *n_doubles);
+
+/* Write the state as float64 [content(G) | sumw2(G) | stats(K) | entries(1)] to
+ * the DEVICE buffer dev_out (for an all-reduce SUM across ranks).  Async on s.
+ * Unit-weight counts are integers < 2^53, exact in any summation order. */
+bh_status bh_pack(const bh_hist *h, double *dev_out, bh_stream s);
+
+/* Replace the state with a packed buffer (DEVICE pointer), e.g. after all-reduce. Async on s. */
+bh_status bh_unpack(bh_hist *h, const double *dev_in, bh_stream s);
+
+/* Read back to HOST buffers (any may be NULL): contents[G], sumw2[G], stats[K],
+ * entries.  Synchronizes stream s.  Reports earlier asynchronous faults. */
+bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *stats, int64_t *entries,
+                  bh_stream s);
+
+/* Force a fill strategy (BH_STRATEGY_*); BH_EINVAL if it cannot hold this histogram. */
+bh_status bh_set_strategy(bh_hist *h, int32_t strategy);
+
+/* Strategy the next fill will use (resolves AUTO). */
+bh_status bh_get_strategy(const bh_hist *h, int32_t weighted, int32_t *strategy);
+
+/* Events per chunk for bh_fill_host (default 1<<22); >= 1024. */
+bh_status bh_set_chunk(bh_hist *h, int64_t events);
+
+/* Debug flags (BH_DEBUG_*), tests only. */
+bh_status bh_set_debug(bh_hist *h, int32_t flags);
+
+/* Number of kernels this histogram has launched so far (for bench/telemetry). */
+bh_status bh_launch_count(const bh_hist *h, int64_t *count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BHIST_H */

@@ -1,0 +1,12 @@
+"""paper_2401_13310_b200 — B200-native bulk histogram filling (arXiv 2401.13310).
+
+The compute path is libbhist.so (hand-written sm_100a CUDA behind the C ABI of
+include/bhist.h); this package is a thin ctypes binding with the same names.
+There is no CPU fallback: if the library is missing or no GPU is present, the
+calls raise.
+"""
+from .bhist import (BH_STRATEGY_AUTO, BH_STRATEGY_CACHE, BH_STRATEGY_GLOBAL, BH_STRATEGY_PRIV,  # noqa: F401
+                    BH_DEBUG_SKIP_COPY_WAIT, BHistError, Histogram, bh_create, bh_destroy, bh_fill,
+                    bh_fill_host, bh_find_bins, bh_get_strategy, bh_info, bh_last_error, bh_launch_count,
+                    bh_pack, bh_packed_size, bh_read, bh_reset, bh_set_chunk, bh_set_debug, bh_set_strategy,
+                    bh_unpack, bh_version, EXPORTED, lib, library_path)

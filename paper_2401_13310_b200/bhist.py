@@ -1,0 +1,278 @@
+"""ctypes binding of include/bhist.h — argument marshalling only.
+
+Every function named bh_* mirrors the C entry point of the same name (see the
+header for semantics, layouts, ownership and errors).  Pointers are passed as
+Python ints (e.g. torch ``tensor.data_ptr()``); streams as ints
+(``torch.cuda.Stream.cuda_stream``) or None for the legacy default stream.
+``Histogram`` is a convenience wrapper over torch tensors (PyTorch is used for
+device memory and streams only; every step of the fill runs in libbhist).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+BH_OK, BH_EINVAL, BH_ENOMEM, BH_ECUDA, BH_EDEVICE, BH_EMISMATCH = 0, -1, -2, -3, -4, -5
+BH_STRATEGY_AUTO, BH_STRATEGY_PRIV, BH_STRATEGY_GLOBAL, BH_STRATEGY_CACHE = 0, 1, 2, 3
+BH_DEBUG_SKIP_COPY_WAIT = 1
+
+# every symbol include/bhist.h declares (checked by tests/test_abi.py)
+EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset", "bh_fill", "bh_fill_host",
+            "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
+            "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_launch_count"]
+
+
+class BHistError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"bhist error {status}: {msg}")
+        self.status = status
+
+
+class _Axis(ctypes.Structure):
+    _fields_ = [("nbins", ctypes.c_int32), ("xmin", ctypes.c_double), ("xmax", ctypes.c_double),
+                ("edges", ctypes.c_void_p)]
+
+
+_lib = None
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+
+
+def library_path() -> str:
+    return _build.SO
+
+
+def lib(build_if_stale: bool = False):
+    """Load libbhist.so.  Raises if it is missing: there is no fallback path."""
+    global _lib
+    if _lib is None:
+        if build_if_stale:
+            _build.build()
+        if not os.path.exists(_build.SO):
+            raise ImportError(f"libbhist.so not built ({_build.SO}); run __graft_entry__.build()")
+        L = ctypes.CDLL(_build.SO)
+        sig = {
+            "bh_version": ([], _I32),
+            "bh_last_error": ([], ctypes.c_char_p),
+            "bh_create": ([_I32, _P, _I32, _P], _I32),
+            "bh_destroy": ([_P], _I32),
+            "bh_reset": ([_P, _P], _I32),
+            "bh_fill": ([_P, _I64, _P, _P, _P], _I32),
+            "bh_fill_host": ([_P, _I64, _P, _P, _P], _I32),
+            "bh_find_bins": ([_P, _I64, _P, _P, _P], _I32),
+            "bh_info": ([_P, _P, _P, _P], _I32),
+            "bh_packed_size": ([_P, _P], _I32),
+            "bh_pack": ([_P, _P, _P], _I32),
+            "bh_unpack": ([_P, _P, _P], _I32),
+            "bh_read": ([_P, _P, _P, _P, _P, _P], _I32),
+            "bh_set_strategy": ([_P, _I32], _I32),
+            "bh_get_strategy": ([_P, _I32, _P], _I32),
+            "bh_set_chunk": ([_P, _I64], _I32),
+            "bh_set_debug": ([_P, _I32], _I32),
+            "bh_launch_count": ([_P, _P], _I32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != BH_OK:
+        raise BHistError(st, bh_last_error())
+
+
+def _ptrs(ptrs):
+    arr = (ctypes.c_void_p * 3)(*(list(ptrs) + [None] * (3 - len(ptrs))))
+    return arr
+
+
+# ---------------------------------------------------------------- C-ABI mirrors
+def bh_version() -> int:
+    return lib().bh_version()
+
+
+def bh_last_error() -> str:
+    return lib().bh_last_error().decode()
+
+
+def bh_create(axes, device: int = 0):
+    """axes: list of (nbins, xmin, xmax) for fixed axes or 1-D float64 arrays of edges."""
+    dim = len(axes)
+    arr = (_Axis * 3)()
+    keep = []
+    for a, ax in enumerate(axes):
+        if isinstance(ax, np.ndarray) or (isinstance(ax, (list, tuple)) and len(ax) != 3):
+            e = np.ascontiguousarray(ax, dtype=np.float64)
+            keep.append(e)
+            arr[a] = _Axis(len(e) - 1, 0.0, 0.0, e.ctypes.data)
+        else:
+            arr[a] = _Axis(int(ax[0]), float(ax[1]), float(ax[2]), None)
+    out = ctypes.c_void_p()
+    _check(lib().bh_create(dim, ctypes.addressof(arr), device, ctypes.byref(out)))
+    return out.value
+
+
+def bh_destroy(h) -> None:
+    _check(lib().bh_destroy(h))
+
+
+def bh_reset(h, stream=None) -> None:
+    _check(lib().bh_reset(h, stream))
+
+
+def bh_fill(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
+    arr = _ptrs(coord_ptrs)      # must outlive the call
+    _check(lib().bh_fill(h, n, ctypes.addressof(arr), w_ptr, stream))
+
+
+def bh_fill_host(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
+    arr = _ptrs(coord_ptrs)
+    _check(lib().bh_fill_host(h, n, ctypes.addressof(arr), w_ptr, stream))
+
+
+def bh_find_bins(h, n: int, coord_ptrs, out_ptr, stream=None) -> None:
+    arr = _ptrs(coord_ptrs)
+    _check(lib().bh_find_bins(h, n, ctypes.addressof(arr), out_ptr, stream))
+
+
+def bh_info(h):
+    d, g, k = _I32(), _I64(), _I32()
+    _check(lib().bh_info(h, ctypes.byref(d), ctypes.byref(g), ctypes.byref(k)))
+    return d.value, g.value, k.value
+
+
+def bh_packed_size(h) -> int:
+    n = _I64()
+    _check(lib().bh_packed_size(h, ctypes.byref(n)))
+    return n.value
+
+
+def bh_pack(h, dev_out_ptr, stream=None) -> None:
+    _check(lib().bh_pack(h, dev_out_ptr, stream))
+
+
+def bh_unpack(h, dev_in_ptr, stream=None) -> None:
+    _check(lib().bh_unpack(h, dev_in_ptr, stream))
+
+
+def bh_read(h, stream=None) -> dict:
+    _, G, K = bh_info(h)
+    c = np.empty(G)
+    s2 = np.empty(G)
+    st = np.empty(K)
+    ent = _I64()
+    _check(lib().bh_read(h, c.ctypes.data, s2.ctypes.data, st.ctypes.data, ctypes.byref(ent), stream))
+    return {"content": c, "sumw2": s2, "stats": st, "entries": ent.value}
+
+
+def bh_set_strategy(h, strategy: int) -> None:
+    _check(lib().bh_set_strategy(h, strategy))
+
+
+def bh_get_strategy(h, weighted: bool) -> int:
+    s = _I32()
+    _check(lib().bh_get_strategy(h, int(bool(weighted)), ctypes.byref(s)))
+    return s.value
+
+
+def bh_set_chunk(h, events: int) -> None:
+    _check(lib().bh_set_chunk(h, events))
+
+
+def bh_set_debug(h, flags: int) -> None:
+    _check(lib().bh_set_debug(h, flags))
+
+
+def bh_launch_count(h) -> int:
+    n = _I64()
+    _check(lib().bh_launch_count(h, ctypes.byref(n)))
+    return n.value
+
+
+# ---------------------------------------------------------------- torch convenience
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Histogram:
+    """A device-resident TH1D/TH2D/TH3D-style histogram (owns a bh_hist)."""
+
+    def __init__(self, axes, device: int = 0, strategy: int = BH_STRATEGY_AUTO):
+        self.device = device
+        self.h = bh_create(axes, device)
+        self.dim, self.nbins_total, self.nstats = bh_info(self.h)
+        if strategy != BH_STRATEGY_AUTO:
+            bh_set_strategy(self.h, strategy)
+
+    def close(self):
+        if getattr(self, "h", None):
+            bh_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self, stream=None):
+        bh_reset(self.h, _stream_handle(stream))
+        return self
+
+    def fill(self, coords, w=None, stream=None):
+        """coords: list of `dim` contiguous float64 CUDA tensors; w: float64 CUDA tensor or None."""
+        import torch
+        assert len(coords) == self.dim
+        n = coords[0].numel()
+        for c in coords:
+            if not (c.is_cuda and c.dtype == torch.float64 and c.is_contiguous() and c.numel() == n):
+                raise ValueError("coords must be contiguous float64 CUDA tensors of equal length")
+        if w is not None and not (w.is_cuda and w.dtype == torch.float64 and w.is_contiguous() and w.numel() == n):
+            raise ValueError("w must be a contiguous float64 CUDA tensor of the same length")
+        bh_fill(self.h, n, [c.data_ptr() for c in coords], None if w is None else w.data_ptr(),
+                _stream_handle(stream))
+        return self
+
+    def fill_host(self, coords, w=None, stream=None):
+        """coords / w: host (preferably pinned) float64 torch tensors or numpy arrays."""
+        def ptr(a):
+            return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+        n = len(coords[0])
+        bh_fill_host(self.h, n, [ptr(c) for c in coords], None if w is None else ptr(w), _stream_handle(stream))
+        return self
+
+    def find_bins(self, coords, stream=None):
+        import torch
+        n = coords[0].numel()
+        out = torch.empty(n, dtype=torch.int32, device=coords[0].device)
+        bh_find_bins(self.h, n, [c.data_ptr() for c in coords], out.data_ptr(), _stream_handle(stream))
+        return out
+
+    def pack(self, out=None, stream=None):
+        import torch
+        n = bh_packed_size(self.h)
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
+        bh_pack(self.h, out.data_ptr(), _stream_handle(stream))
+        return out
+
+    def unpack(self, buf, stream=None):
+        bh_unpack(self.h, buf.data_ptr(), _stream_handle(stream))
+        return self
+
+    def read(self, stream=None) -> dict:
+        return bh_read(self.h, _stream_handle(stream))
+
+    def strategy(self, weighted: bool) -> int:
+        return bh_get_strategy(self.h, weighted)

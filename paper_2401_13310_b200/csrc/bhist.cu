@@ -1,0 +1,557 @@
+// bhist.cu — host side of libbhist: the C ABI of include/bhist.h.
+//
+// Owns per-histogram device state (RHnCUDA analogue: "keeps track of
+// device allocations and contains a Fill method"), validates axes, builds the
+// variable-axis guide tables, chooses the fill strategy and launch shape, and
+// runs the pinned double-buffered host->device path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bhist.h"
+#include "bhist_kernels.cuh"
+
+using namespace bh;
+
+namespace {
+
+thread_local std::string g_err;
+
+bh_status fail(bh_status st, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+bh_status fail(bh_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                             \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess) return fail(BH_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                                           __FILE__, __LINE__);                                    \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+constexpr int kStageSlots = 2;
+
+}  // namespace
+
+struct bh_hist {
+    int device = 0;
+    int dim = 0;
+    int nsm = 148;
+    int K = 0;
+    int64_t G = 0;
+    AxisP ax[kMaxDim] = {};
+    int32_t st1 = 1, st2 = 1;
+    int strategy = BH_STRATEGY_AUTO;
+    int debug = 0;
+    int64_t chunk = 1 << 22;
+    int64_t launches = 0;
+    size_t smem_optin = 0;
+    int max_grid = 0;
+    // device state
+    unsigned long long *count = nullptr;
+    double *sumw = nullptr, *sumw2 = nullptr;
+    double *stats = nullptr;
+    unsigned long long *entries = nullptr;
+    double *partials = nullptr;
+    unsigned int *counter = nullptr;
+    double *pack_buf = nullptr;       // device buffer for bh_read
+    double *pack_host = nullptr;      // pinned host buffer for bh_read
+    std::vector<void *> axis_mem;     // edges and guide tables
+    // host->device double buffer
+    cudaStream_t copy_stream = nullptr;
+    double *stage[kStageSlots] = {};  // each slot: (dim+1) columns of `chunk` doubles
+    int64_t stage_chunk = 0;
+    cudaEvent_t copied[kStageSlots] = {}, consumed[kStageSlots] = {};
+};
+
+namespace {
+
+int resolve_strategy(const bh_hist *h, bool weighted) {
+    if (h->strategy != BH_STRATEGY_AUTO) return h->strategy;
+    const size_t budget = 160 * 1024;
+    const size_t priv = weighted ? 16 * (size_t)h->G : 4 * (size_t)h->G;
+    if (priv <= budget) return BH_STRATEGY_PRIV;
+    return BH_STRATEGY_GLOBAL;
+}
+
+int cache_slots_for(bool weighted) { return weighted ? 4096 : 16384; }
+
+size_t smem_bytes(const bh_hist *h, int strategy, bool weighted) {
+    if (strategy == BH_STRATEGY_PRIV) return weighted ? 16 * (size_t)h->G : 4 * (size_t)h->G;
+    if (strategy == BH_STRATEGY_CACHE) {
+        const size_t S = cache_slots_for(weighted);
+        return S * 4 + (weighted ? 16 * S : 4 * S);
+    }
+    return 0;
+}
+
+FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, const double *w) {
+    FillP p{};
+    p.n = n;
+    for (int a = 0; a < h->dim; ++a) { p.x[a] = coords[a]; p.ax[a] = h->ax[a]; }
+    p.w = w;
+    p.st1 = h->st1;
+    p.st2 = h->st2;
+    p.G = (int32_t)h->G;
+    p.K = h->K;
+    p.count = h->count;
+    p.sumw = h->sumw;
+    p.sumw2 = h->sumw2;
+    p.partials = h->partials;
+    p.counter = h->counter;
+    p.stats = h->stats;
+    p.entries = h->entries;
+    p.entries_add = n;
+    return p;
+}
+
+template <int DIM, bool W, int SINK, bool VEC>
+cudaError_t launch_t(const bh_hist *h, const FillP &p, int grid, size_t smem, cudaStream_t s) {
+    auto kern = k_fill<DIM, W, SINK, VEC>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, kThreads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <int DIM, bool W, int SINK>
+cudaError_t launch_v(const bh_hist *h, const FillP &p, bool vec, int grid, size_t smem, cudaStream_t s) {
+    return vec ? launch_t<DIM, W, SINK, true>(h, p, grid, smem, s) : launch_t<DIM, W, SINK, false>(h, p, grid, smem, s);
+}
+
+template <int DIM, bool W>
+cudaError_t launch_s(const bh_hist *h, const FillP &p, int strategy, bool vec, int grid, size_t smem, cudaStream_t s) {
+    switch (strategy) {
+    case BH_STRATEGY_PRIV: return launch_v<DIM, W, SINK_PRIV>(h, p, vec, grid, smem, s);
+    case BH_STRATEGY_CACHE: return launch_v<DIM, W, SINK_CACHE>(h, p, vec, grid, smem, s);
+    default: return launch_v<DIM, W, SINK_GLOBAL>(h, p, vec, grid, smem, s);
+    }
+}
+
+template <int DIM>
+cudaError_t launch_d(const bh_hist *h, const FillP &p, bool weighted, int strategy, bool vec, int grid, size_t smem,
+                     cudaStream_t s) {
+    return weighted ? launch_s<DIM, true>(h, p, strategy, vec, grid, smem, s)
+                    : launch_s<DIM, false>(h, p, strategy, vec, grid, smem, s);
+}
+
+// Blocks resident per SM for a strategy (occupancy-limited by shared memory and by
+// __launch_bounds__(kThreads, 2)).
+int resident_blocks(const bh_hist *h, size_t smem) {
+    int by_smem = smem ? (int)std::min<size_t>(2, (228 * 1024) / (smem + 1024)) : 2;
+    return std::max(1, by_smem);
+}
+
+// One fill over device-resident columns, split into launches of <= 2^31 events.
+bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
+    const bool weighted = w != nullptr;
+    const int strategy = resolve_strategy(h, weighted);
+    const size_t smem = smem_bytes(h, strategy, weighted);
+    if (smem > h->smem_optin)
+        return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", strategy, smem, h->smem_optin);
+    const int64_t kMaxLaunch = int64_t(1) << 31;
+    for (int64_t off = 0; off < n; off += kMaxLaunch) {
+        const int64_t m = std::min(kMaxLaunch, n - off);
+        const double *cs[kMaxDim] = {};
+        for (int a = 0; a < h->dim; ++a) cs[a] = coords[a] + off;
+        const double *ws = weighted ? w + off : nullptr;
+        FillP p = make_params(h, m, cs, ws);
+        // vector path: every column must share the same 16-byte phase
+        const uintptr_t ph = reinterpret_cast<uintptr_t>(cs[0]) & 15;
+        bool vec = (ph % 8) == 0;
+        for (int a = 1; a < h->dim; ++a) vec &= (reinterpret_cast<uintptr_t>(cs[a]) & 15) == ph;
+        if (weighted) vec &= (reinterpret_cast<uintptr_t>(ws) & 15) == ph;
+        p.peel = vec && ph ? 1 : 0;
+        if (p.peel > m) p.peel = (int32_t)m;
+        p.cache_slots = cache_slots_for(weighted);
+        // launch shape: persistent grid, but each block should see enough events to
+        // amortize zeroing + flushing its private bins
+        const int per_sm = resident_blocks(h, smem);
+        int64_t want_per_block = kThreads * 8;
+        if (strategy == BH_STRATEGY_PRIV) want_per_block = std::max<int64_t>(want_per_block, 4 * h->G);
+        int64_t grid = (m + want_per_block - 1) / want_per_block;
+        grid = std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)h->nsm * per_sm));
+        cudaError_t e;
+        switch (h->dim) {
+        case 1: e = launch_d<1>(h, p, weighted, strategy, vec, (int)grid, smem, s); break;
+        case 2: e = launch_d<2>(h, p, weighted, strategy, vec, (int)grid, smem, s); break;
+        default: e = launch_d<3>(h, p, weighted, strategy, vec, (int)grid, smem, s); break;
+        }
+        if (e != cudaSuccess) return fail(BH_ECUDA, "fill launch: %s", cudaGetErrorString(e));
+        ++h->launches;
+    }
+    return BH_OK;
+}
+
+bh_status check_hist(const bh_hist *h) {
+    if (!h) return fail(BH_EINVAL, "NULL histogram");
+    return BH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t bh_version(void) { return 10000; }
+
+const char *bh_last_error(void) { return g_err.c_str(); }
+
+bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **out) {
+    if (!out) return fail(BH_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (dim < 1 || dim > 3) return fail(BH_EINVAL, "dim must be 1, 2 or 3 (got %d)", dim);
+    if (!axes) return fail(BH_EINVAL, "axes is NULL");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(BH_EDEVICE, "no CUDA device");
+    }
+    if (device < 0 || device >= ndev) return fail(BH_EDEVICE, "device %d out of range [0,%d)", device, ndev);
+    // validate axes (all on the host, before any allocation)
+    int64_t G = 1;
+    for (int a = 0; a < dim; ++a) {
+        const bh_axis &A = axes[a];
+        if (A.nbins < 1) return fail(BH_EINVAL, "axis %d: nbins must be >= 1", a);
+        if (A.edges) {
+            for (int i = 0; i <= A.nbins; ++i)
+                if (!std::isfinite(A.edges[i])) return fail(BH_EINVAL, "axis %d: edge %d not finite", a, i);
+            for (int i = 0; i < A.nbins; ++i)
+                if (!(A.edges[i] < A.edges[i + 1])) return fail(BH_EINVAL, "axis %d: edges not strictly increasing at %d", a, i);
+            if (!std::isfinite(A.edges[A.nbins] - A.edges[0])) return fail(BH_EINVAL, "axis %d: edge range overflows", a);
+        } else {
+            if (!std::isfinite(A.xmin) || !std::isfinite(A.xmax) || !(A.xmin < A.xmax))
+                return fail(BH_EINVAL, "axis %d: need finite xmin < xmax", a);
+            const double D = A.xmax - A.xmin;
+            if (!std::isfinite(D) || !std::isfinite((double)A.nbins * D) || !std::isfinite((double)A.nbins / D))
+                return fail(BH_EINVAL, "axis %d: nbins*(xmax-xmin) not finite", a);
+        }
+        G *= (int64_t)A.nbins + 2;
+        if (G >= (int64_t(1) << 31)) return fail(BH_EINVAL, "total bins (with flow) must be < 2^31");
+    }
+    DeviceGuard dg(device);
+    if (!dg.ok) return fail(BH_EDEVICE, "cudaSetDevice(%d) failed", device);
+    bh_hist *h = new bh_hist();
+    h->device = device;
+    h->dim = dim;
+    h->G = G;
+    h->K = dim == 1 ? 4 : dim == 2 ? 7 : 11;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) { delete h; return fail(BH_ECUDA, "cudaGetDeviceProperties"); }
+    h->nsm = prop.multiProcessorCount;
+    h->smem_optin = prop.sharedMemPerBlockOptin;
+    h->max_grid = h->nsm * 4;
+    h->st1 = axes[0].nbins + 2;
+    h->st2 = dim > 2 ? (axes[0].nbins + 2) * (axes[1].nbins + 2) : 1;
+    auto cleanup = [&](bh_status st) { bh_destroy(h); return st; };
+#define ALLOC(ptr, bytes)                                                                          \
+    do {                                                                                           \
+        if (cudaMalloc(reinterpret_cast<void **>(&(ptr)), (bytes)) != cudaSuccess) {               \
+            cudaGetLastError();                                                                    \
+            return cleanup(fail(BH_ENOMEM, "cudaMalloc(%zu) failed", (size_t)(bytes)));            \
+        }                                                                                          \
+    } while (0)
+    ALLOC(h->count, sizeof(unsigned long long) * G);
+    ALLOC(h->sumw, sizeof(double) * G);
+    ALLOC(h->sumw2, sizeof(double) * G);
+    ALLOC(h->stats, sizeof(double) * 16);
+    ALLOC(h->entries, sizeof(unsigned long long));
+    ALLOC(h->partials, sizeof(double) * 16 * h->max_grid);
+    ALLOC(h->counter, sizeof(unsigned int));
+    ALLOC(h->pack_buf, sizeof(double) * (2 * G + h->K + 1));
+    if (cudaMallocHost(reinterpret_cast<void **>(&h->pack_host), sizeof(double) * (2 * G + h->K + 1)) != cudaSuccess) {
+        cudaGetLastError();
+        return cleanup(fail(BH_ENOMEM, "cudaMallocHost failed"));
+    }
+    for (int a = 0; a < dim; ++a) {
+        const bh_axis &A = axes[a];
+        AxisP &P = h->ax[a];
+        P.n = A.nbins;
+        if (!A.edges) {
+            P.var = 0;
+            P.xmin = A.xmin;
+            P.xmax = A.xmax;
+            P.D = A.xmax - A.xmin;            // RN, as the definition rounds it
+            P.inv = (double)A.nbins / P.D;    // RN(n/D): fast-path multiplier
+        } else {
+            P.var = 1;
+            P.xmin = A.edges[0];
+            P.xmax = A.edges[A.nbins];
+            int gc = 1;
+            while (gc < A.nbins && gc < (1 << 22)) gc <<= 1;
+            P.gcells = gc;
+            P.gscale = (double)gc / (P.xmax - P.xmin);
+            if (!std::isfinite(P.gscale) || !(P.gscale > 0)) return cleanup(fail(BH_EINVAL, "axis %d: edge range too small", a));
+            double *de = nullptr;
+            uint32_t *dg2 = nullptr;
+            ALLOC(de, sizeof(double) * (A.nbins + 1));
+            h->axis_mem.push_back(de);
+            ALLOC(dg2, sizeof(uint32_t) * (gc + 1));
+            h->axis_mem.push_back(dg2);
+            if (cudaMemcpy(de, A.edges, sizeof(double) * (A.nbins + 1), cudaMemcpyHostToDevice) != cudaSuccess)
+                return cleanup(fail(BH_ECUDA, "edge upload failed"));
+            P.e = de;
+            P.guide = dg2;
+            k_build_guide<<<(gc + 1 + 255) / 256, 256>>>(P, dg2);
+            if (cudaGetLastError() != cudaSuccess) return cleanup(fail(BH_ECUDA, "guide build launch failed"));
+        }
+    }
+#undef ALLOC
+    if (cudaMemset(h->count, 0, sizeof(unsigned long long) * G) != cudaSuccess ||
+        cudaMemset(h->sumw, 0, sizeof(double) * G) != cudaSuccess ||
+        cudaMemset(h->sumw2, 0, sizeof(double) * G) != cudaSuccess ||
+        cudaMemset(h->stats, 0, sizeof(double) * 16) != cudaSuccess ||
+        cudaMemset(h->entries, 0, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(h->counter, 0, sizeof(unsigned int)) != cudaSuccess)
+        return cleanup(fail(BH_ECUDA, "initial memset failed"));
+    if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(BH_ECUDA, "create: %s", cudaGetErrorString(cudaGetLastError())));
+    *out = h;
+    return BH_OK;
+}
+
+bh_status bh_destroy(bh_hist *h) {
+    if (!h) return BH_OK;
+    DeviceGuard dg(h->device);
+    cudaDeviceSynchronize();
+    cudaFree(h->count);
+    cudaFree(h->sumw);
+    cudaFree(h->sumw2);
+    cudaFree(h->stats);
+    cudaFree(h->entries);
+    cudaFree(h->partials);
+    cudaFree(h->counter);
+    cudaFree(h->pack_buf);
+    if (h->pack_host) cudaFreeHost(h->pack_host);
+    for (void *p : h->axis_mem) cudaFree(p);
+    for (int i = 0; i < kStageSlots; ++i) {
+        if (h->stage[i]) cudaFree(h->stage[i]);
+        if (h->copied[i]) cudaEventDestroy(h->copied[i]);
+        if (h->consumed[i]) cudaEventDestroy(h->consumed[i]);
+    }
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    delete h;
+    return BH_OK;
+}
+
+bh_status bh_reset(bh_hist *h, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    CUDA_TRY(cudaMemsetAsync(h->count, 0, sizeof(unsigned long long) * h->G, st));
+    CUDA_TRY(cudaMemsetAsync(h->sumw, 0, sizeof(double) * h->G, st));
+    CUDA_TRY(cudaMemsetAsync(h->sumw2, 0, sizeof(double) * h->G, st));
+    CUDA_TRY(cudaMemsetAsync(h->stats, 0, sizeof(double) * 16, st));
+    CUDA_TRY(cudaMemsetAsync(h->entries, 0, sizeof(unsigned long long), st));
+    return BH_OK;
+}
+
+bh_status bh_fill(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (n < 0) return fail(BH_EINVAL, "n < 0");
+    if (n == 0) return BH_OK;
+    if (!coords) return fail(BH_EINVAL, "coords is NULL");
+    for (int a = 0; a < h->dim; ++a)
+        if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
+    DeviceGuard dg(h->device);
+    return fill_device(h, n, coords, w, static_cast<cudaStream_t>(s));
+}
+
+bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (n < 0) return fail(BH_EINVAL, "n < 0");
+    if (n == 0) return BH_OK;
+    if (!coords) return fail(BH_EINVAL, "coords is NULL");
+    for (int a = 0; a < h->dim; ++a)
+        if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    const int ncol = h->dim + (w ? 1 : 0);
+    // lazily create the copy stream, events and the device double buffer
+    if (!h->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    if (h->stage_chunk != h->chunk) {
+        CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
+        for (int i = 0; i < kStageSlots; ++i) {
+            if (h->consumed[i]) CUDA_TRY(cudaEventSynchronize(h->consumed[i]));
+            if (h->stage[i]) cudaFree(h->stage[i]);
+            h->stage[i] = nullptr;
+            if (cudaMalloc(reinterpret_cast<void **>(&h->stage[i]), sizeof(double) * (kMaxDim + 1) * h->chunk) != cudaSuccess) {
+                cudaGetLastError();
+                h->stage_chunk = 0;
+                return fail(BH_ENOMEM, "staging allocation failed");
+            }
+            if (!h->copied[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->copied[i], cudaEventDisableTiming));
+            if (!h->consumed[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->consumed[i], cudaEventDisableTiming));
+        }
+        h->stage_chunk = h->chunk;
+    }
+    const int64_t C = h->stage_chunk;
+    int k = 0;
+    for (int64_t off = 0; off < n; off += C, ++k) {
+        const int slot = k % kStageSlots;
+        const int64_t m = std::min(C, n - off);
+        double *buf = h->stage[slot];
+        // the slot may be overwritten only after the fill that read it has run
+        if (k >= kStageSlots) CUDA_TRY(cudaStreamWaitEvent(h->copy_stream, h->consumed[slot], 0));
+        const double *dcols[kMaxDim] = {};
+        for (int a = 0; a < h->dim; ++a) {
+            CUDA_TRY(cudaMemcpyAsync(buf + a * C, coords[a] + off, sizeof(double) * m, cudaMemcpyHostToDevice, h->copy_stream));
+            dcols[a] = buf + a * C;
+        }
+        const double *dw = nullptr;
+        if (w) {
+            CUDA_TRY(cudaMemcpyAsync(buf + h->dim * C, w + off, sizeof(double) * m, cudaMemcpyHostToDevice, h->copy_stream));
+            dw = buf + h->dim * C;
+        }
+        CUDA_TRY(cudaEventRecord(h->copied[slot], h->copy_stream));
+        if (!(h->debug & BH_DEBUG_SKIP_COPY_WAIT)) CUDA_TRY(cudaStreamWaitEvent(st, h->copied[slot], 0));
+        bh_status r = fill_device(h, m, dcols, dw, st);
+        if (r != BH_OK) return r;
+        CUDA_TRY(cudaEventRecord(h->consumed[slot], st));
+    }
+    (void)ncol;
+    // every host byte has been read once the last copy has completed
+    CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
+    return BH_OK;
+}
+
+bh_status bh_find_bins(const bh_hist *h, int64_t n, const double *const *coords, int32_t *out, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (n < 0) return fail(BH_EINVAL, "n < 0");
+    if (n == 0) return BH_OK;
+    if (!coords || !out) return fail(BH_EINVAL, "NULL pointer");
+    for (int a = 0; a < h->dim; ++a)
+        if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
+    DeviceGuard dg(h->device);
+    FillP p = make_params(h, n, coords, nullptr);
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)h->nsm * 16);
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    switch (h->dim) {
+    case 1: k_find_bins<1><<<grid, 256, 0, st>>>(p, out); break;
+    case 2: k_find_bins<2><<<grid, 256, 0, st>>>(p, out); break;
+    default: k_find_bins<3><<<grid, 256, 0, st>>>(p, out); break;
+    }
+    CUDA_TRY(cudaGetLastError());
+    const_cast<bh_hist *>(h)->launches++;
+    return BH_OK;
+}
+
+bh_status bh_info(const bh_hist *h, int32_t *dim, int64_t *nbins_total, int32_t *nstats) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (dim) *dim = h->dim;
+    if (nbins_total) *nbins_total = h->G;
+    if (nstats) *nstats = h->K;
+    return BH_OK;
+}
+
+bh_status bh_packed_size(const bh_hist *h, int64_t *n_doubles) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (!n_doubles) return fail(BH_EINVAL, "NULL output");
+    *n_doubles = 2 * h->G + h->K + 1;
+    return BH_OK;
+}
+
+bh_status bh_pack(const bh_hist *h, double *dev_out, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (!dev_out) return fail(BH_EINVAL, "NULL output");
+    DeviceGuard dg(h->device);
+    const int64_t tot = 2 * h->G + h->K + 1;
+    const int grid = (int)std::min<int64_t>((tot + 255) / 256, (int64_t)h->nsm * 8);
+    k_pack<<<grid, 256, 0, static_cast<cudaStream_t>(s)>>>((int)h->G, h->K, h->count, h->sumw, h->sumw2, h->stats,
+                                                            h->entries, dev_out);
+    CUDA_TRY(cudaGetLastError());
+    const_cast<bh_hist *>(h)->launches++;
+    return BH_OK;
+}
+
+bh_status bh_unpack(bh_hist *h, const double *dev_in, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (!dev_in) return fail(BH_EINVAL, "NULL input");
+    DeviceGuard dg(h->device);
+    const int64_t tot = 2 * h->G + h->K + 1;
+    const int grid = (int)std::min<int64_t>((tot + 255) / 256, (int64_t)h->nsm * 8);
+    k_unpack<<<grid, 256, 0, static_cast<cudaStream_t>(s)>>>((int)h->G, h->K, h->count, h->sumw, h->sumw2, h->stats,
+                                                              h->entries, dev_in);
+    CUDA_TRY(cudaGetLastError());
+    h->launches++;
+    return BH_OK;
+}
+
+bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *stats, int64_t *entries, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    bh_status r = bh_pack(h, h->pack_buf, s);
+    if (r != BH_OK) return r;
+    const int64_t tot = 2 * h->G + h->K + 1;
+    CUDA_TRY(cudaMemcpyAsync(h->pack_host, h->pack_buf, sizeof(double) * tot, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (contents) memcpy(contents, h->pack_host, sizeof(double) * h->G);
+    if (sumw2) memcpy(sumw2, h->pack_host + h->G, sizeof(double) * h->G);
+    if (stats) memcpy(stats, h->pack_host + 2 * h->G, sizeof(double) * h->K);
+    if (entries) *entries = (int64_t)h->pack_host[2 * h->G + h->K];
+    return BH_OK;
+}
+
+bh_status bh_set_strategy(bh_hist *h, int32_t strategy) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (strategy < BH_STRATEGY_AUTO || strategy > BH_STRATEGY_CACHE) return fail(BH_EINVAL, "unknown strategy %d", strategy);
+    if (strategy == BH_STRATEGY_PRIV && 4 * (size_t)h->G > h->smem_optin)
+        return fail(BH_EINVAL, "PRIV cannot hold %lld bins in shared memory", (long long)h->G);
+    h->strategy = strategy;
+    return BH_OK;
+}
+
+bh_status bh_get_strategy(const bh_hist *h, int32_t weighted, int32_t *strategy) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (!strategy) return fail(BH_EINVAL, "NULL output");
+    *strategy = resolve_strategy(h, weighted != 0);
+    return BH_OK;
+}
+
+bh_status bh_set_chunk(bh_hist *h, int64_t events) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (events < 1024) return fail(BH_EINVAL, "chunk must be >= 1024 events");
+    h->chunk = events;
+    return BH_OK;
+}
+
+bh_status bh_set_debug(bh_hist *h, int32_t flags) {
+    if (check_hist(h)) return BH_EINVAL;
+    h->debug = flags;
+    return BH_OK;
+}
+
+bh_status bh_launch_count(const bh_hist *h, int64_t *count) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (!count) return fail(BH_EINVAL, "NULL output");
+    *count = h->launches;
+    return BH_OK;
+}
+
+}  // extern "C"

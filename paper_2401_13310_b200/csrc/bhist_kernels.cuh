@@ -1,0 +1,475 @@
+// bhist_kernels.cuh — sm_100a device code for bulk histogram filling.
+//
+// One fused kernel per fill: it streams the coordinate (and weight) columns
+// once, runs FindBin per axis, composes the global bin, adds into the bins and
+// accumulates the GetStats sums in registers — the three steps of PAPER.md:126
+// in a single pass (the paper's CUDA path used one histogram kernel plus one
+// reduction kernel per statistic, re-reading the inputs each
+// time; the SYCL study found fusing the reductions 1.4-1.9x faster).
+// The statistics end in per-CTA partials reduced in a fixed order by the last CTA
+// to finish, so they are run-to-run deterministic for a given launch shape.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bh {
+
+constexpr int kMaxDim = 3;
+constexpr int kThreads = 512;
+
+// Axis as the kernels see it.  Fixed axes use (xmin, xmax, D = xmax-xmin,
+// inv = n/D), all rounded once on the host exactly as the definition rounds them.
+// Variable axes use the edges plus a monotone "guide" table.
+struct AxisP {
+    int32_t n;       // in-range bins
+    int32_t var;     // 0 fixed, 1 variable
+    double xmin;     // fixed: xmin; variable: e[0]
+    double xmax;     // fixed: xmax; variable: e[n]
+    double D;        // fixed: RN(xmax - xmin)
+    double inv;      // fixed: RN(n / D)
+    const double *e;         // variable: n+1 edges (device)
+    const uint32_t *guide;   // variable: gcells+1 entries, guide[c] = #{interior i : cell(e_i) < c}
+    int32_t gcells;          // variable: number of cells (power of two)
+    double gscale;           // variable: gcells / (e[n] - e[0])
+};
+
+struct FillP {
+    int64_t n;               // events in this launch
+    const double *x[kMaxDim];
+    const double *w;         // nullptr: unit weights
+    AxisP ax[kMaxDim];
+    int32_t st1, st2;        // strides of axes 1 and 2 in the flat bin index
+    int32_t G;               // total bins (flow included)
+    int32_t K;               // number of stats
+    int32_t peel;            // vector path: leading events handled one by one (alignment)
+    int32_t cache_slots;     // CACHE strategy: shared-memory slots (power of two)
+    unsigned long long *count;   // unit-weight counts [G]
+    double *sumw;                // weighted sums [G]
+    double *sumw2;               // weighted sums of squares [G]
+    double *partials;            // [gridDim.x * K]
+    unsigned int *counter;       // last-CTA ticket
+    double *stats;               // [K], running totals
+    unsigned long long *entries; // running entries
+    int64_t entries_add;         // added to *entries by the last CTA
+};
+
+// ------------------------------------------------------------------ FindBin
+// Fixed axis: b = 1 + floor(n*(x-xmin)/(xmax-xmin)), evaluated as
+// the IEEE binary64 expression (n*(x-xmin))/(xmax-xmin) (reading R2).  Fast path:
+// q' = (x-xmin)*inv with inv = RN(n/D).  |q' - q| <= ~4u*q (u = 2^-53), so when the
+// fractional part of q' is farther than 2^-40*max(q',1) from an integer, floor(q')
+// == floor(q) and the division is skipped; otherwise the exact expression runs.
+// All operations are explicit _rn intrinsics: nvcc may not contract or reorder them.
+__device__ __forceinline__ int find_bin_fixed(const AxisP &a, double x) {
+    if (x < a.xmin) return 0;
+    if (!(x < a.xmax)) return a.n + 1;   // x == xmax and NaN -> overflow (R5)
+    const double d = __dsub_rn(x, a.xmin);
+    double q = __dmul_rn(d, a.inv);
+    const double fl = floor(q);
+    const double fr = __dsub_rn(q, fl);
+    const double tol = 0x1p-40 * fmax(q, 1.0);
+    if (fr < tol || __dsub_rn(1.0, fr) < tol) q = __ddiv_rn(__dmul_rn((double)a.n, d), a.D);
+    return 1 + (int)q;                   // q >= 0: truncation == floor; q <= n
+}
+
+// Guide cell of a coordinate x >= e[0]: monotone non-decreasing in x (RN is
+// monotone, gscale > 0, truncation and min are monotone).  The same function
+// builds the table, so the table is exact for it.
+__device__ __forceinline__ int guide_cell(const AxisP &a, double x) {
+    const double t = __dmul_rn(__dsub_rn(x, a.xmin), a.gscale);
+    const int c = (int)t;               // cvt.rzi saturates; t >= 0
+    return c < a.gcells - 1 ? c : a.gcells - 1;
+}
+
+// Variable axis, PAPER.md:126,138 ("binary search"): b = #{edges <= x} (R1).
+// Interior edges 1..lo of the cell are < x, lo+1..hi share x's cell, hi+1.. are > x
+// (monotonicity of guide_cell), so b = 1 + lo + #{i in (lo, hi] : e_i <= x}; the
+// remaining count is a binary search over the (usually 0-3) edges of the cell.
+template <typename EdgeLoad>
+__device__ __forceinline__ int find_bin_var_impl(const AxisP &a, double x, const uint32_t *guide, EdgeLoad edge) {
+    if (x < a.xmin) return 0;
+    if (!(x < a.xmax)) return a.n + 1;
+    const int c = guide_cell(a, x);
+    int lo = (int)guide[c], hi = (int)guide[c + 1];
+    while (lo < hi) {                    // largest l in [lo, hi] with l == lo or e[l] <= x
+        const int m = (lo + hi + 1) >> 1;
+        if (edge(m) <= x) lo = m; else hi = m - 1;
+    }
+    return 1 + lo;
+}
+
+__device__ __forceinline__ int find_bin_var_global(const AxisP &a, double x) {
+    return find_bin_var_impl(a, x, a.guide, [&](int i) { return __ldg(a.e + i); });
+}
+
+__device__ __forceinline__ int find_bin(const AxisP &a, double x) {
+    return a.var ? find_bin_var_global(a, x) : find_bin_fixed(a, x);
+}
+
+// ------------------------------------------------------------------ stats
+template <int DIM>
+struct NStats { static constexpr int K = DIM == 1 ? 4 : DIM == 2 ? 7 : 11; };
+
+// Register accumulator of the GetStats sums (ROOT order, reading R7/R8).
+template <int DIM, bool W>
+struct Acc {
+    static constexpr int K = NStats<DIM>::K;
+    double s[K];
+    unsigned long long cnt;   // unit weights: in-range count (= sumw = sumw2, exact)
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int k = 0; k < K; ++k) s[k] = 0.0;
+        cnt = 0;
+    }
+    __device__ __forceinline__ void add(const double (&x)[DIM], double w) {
+        double wx = W ? w * x[0] : x[0];
+        if (W) { s[0] += w; s[1] = fma(w, w, s[1]); } else { ++cnt; }
+        s[2] += wx;
+        s[3] = fma(wx, x[0], s[3]);
+        if (DIM >= 2) {
+            const double wy = W ? w * x[1] : x[1];
+            s[4] += wy;
+            s[5] = fma(wy, x[1], s[5]);
+            s[6] = fma(wx, x[1], s[6]);
+            if (DIM == 3) {
+                const double wz = W ? w * x[2] : x[2];
+                s[7] += wz;
+                s[8] = fma(wz, x[2], s[8]);
+                s[9] = fma(wx, x[2], s[9]);
+                s[10] = fma(wy, x[2], s[10]);
+            }
+        }
+    }
+    __device__ __forceinline__ void finalize_unit() {
+        if (!W) { s[0] = (double)cnt; s[1] = (double)cnt; }
+    }
+};
+
+// Block reduction of the K sums -> partials[blockIdx.x]; the last CTA to arrive
+// sums the partials in block order and adds them to the running stats
+// (include-initial) and adds the event count to entries.
+template <int K>
+__device__ __forceinline__ void block_stats_finish(const FillP &p, double (&s)[K]) {
+    __shared__ double red[kThreads / 32][K];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double v = s[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double t = 0.0;
+        const int nw = blockDim.x >> 5;
+        for (int i = 0; i < nw; ++i) t += red[i][threadIdx.x];
+        p.partials[(size_t)blockIdx.x * K + threadIdx.x] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(p.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x < K) {
+        double t = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(p.partials + (size_t)b * K + threadIdx.x);
+        p.stats[threadIdx.x] += t;
+    }
+    if (threadIdx.x == 0) {
+        *p.entries += (unsigned long long)p.entries_add;
+        *p.counter = 0u;
+    }
+}
+
+// ------------------------------------------------------------------ bin sinks
+enum Sink { SINK_PRIV = 0, SINK_GLOBAL = 1, SINK_CACHE = 2 };
+
+// Shared-memory layout of the PRIV sink: unit -> uint32 count[G];
+// weighted -> double sumw[G] then double sumw2[G].
+template <bool W>
+struct PrivSink {
+    unsigned char *sm;
+    int G;
+    __device__ __forceinline__ void init(unsigned char *s, int g) {
+        sm = s; G = g;
+        if (W) {
+            double *d = reinterpret_cast<double *>(sm);
+            for (int i = threadIdx.x; i < 2 * G; i += blockDim.x) d[i] = 0.0;
+        } else {
+            uint32_t *c = reinterpret_cast<uint32_t *>(sm);
+            for (int i = threadIdx.x; i < G; i += blockDim.x) c[i] = 0u;
+        }
+    }
+    __device__ __forceinline__ void add(int g, double w) {
+        if (W) {
+            double *d = reinterpret_cast<double *>(sm);
+            atomicAdd(d + g, w);
+            atomicAdd(d + G + g, w * w);
+        } else {
+            atomicAdd(reinterpret_cast<uint32_t *>(sm) + g, 1u);
+        }
+    }
+    // Merge stage of PAPER.md:162-165: each block adds its local bins to the global ones.
+    __device__ __forceinline__ void flush(const FillP &p) {
+        if (W) {
+            const double *d = reinterpret_cast<const double *>(sm);
+            for (int i = threadIdx.x; i < G; i += blockDim.x) {
+                const double a = d[i], b = d[G + i];
+                if (a != 0.0) atomicAdd(p.sumw + i, a);
+                if (b != 0.0) atomicAdd(p.sumw2 + i, b);
+            }
+        } else {
+            const uint32_t *c = reinterpret_cast<const uint32_t *>(sm);
+            for (int i = threadIdx.x; i < G; i += blockDim.x) {
+                const uint32_t v = c[i];
+                if (v) atomicAdd(p.count + i, (unsigned long long)v);
+            }
+        }
+    }
+};
+
+template <bool W>
+struct GlobalSink {
+    const FillP *pp;
+    __device__ __forceinline__ void init(unsigned char *, int) {}
+    __device__ __forceinline__ void add(int g, double w) {
+        if (W) {
+            atomicAdd(pp->sumw + g, w);
+            atomicAdd(pp->sumw2 + g, w * w);
+        } else {
+            atomicAdd(pp->count + g, 1ull);
+        }
+    }
+    __device__ __forceinline__ void flush(const FillP &) {}
+};
+
+// CACHE sink: direct-mapped shared-memory cache of global bins.  A slot is
+// claimed by the first bin that hashes to it (32-bit CAS, native); hits add in
+// shared memory, misses go to global atomics.  Unit weights first aggregate equal
+// bins across the warp (match.any) so the hottest bin costs one shared atomic per
+// warp instead of up to 32 serialized ones.
+template <bool W>
+struct CacheSink {
+    uint32_t *keys;
+    unsigned char *vals;
+    int S;
+    const FillP *pp;
+    static constexpr uint32_t kEmpty = 0xffffffffu;
+    __device__ __forceinline__ void init(unsigned char *s, int slots) {
+        S = slots;
+        keys = reinterpret_cast<uint32_t *>(s);
+        vals = s + (size_t)S * 4;
+        for (int i = threadIdx.x; i < S; i += blockDim.x) keys[i] = kEmpty;
+        if (W) {
+            double *d = reinterpret_cast<double *>(vals);
+            for (int i = threadIdx.x; i < 2 * S; i += blockDim.x) d[i] = 0.0;
+        } else {
+            uint32_t *c = reinterpret_cast<uint32_t *>(vals);
+            for (int i = threadIdx.x; i < S; i += blockDim.x) c[i] = 0u;
+        }
+    }
+    __device__ __forceinline__ int slot_of(uint32_t g) const { return (int)((g * 2654435761u) >> 7) & (S - 1); }
+    __device__ __forceinline__ int lookup(uint32_t g) {
+        const int sl = slot_of(g);
+        uint32_t k = keys[sl];
+        if (k == kEmpty) {
+            k = atomicCAS(keys + sl, kEmpty, g);
+            if (k == kEmpty) k = g;
+        }
+        return k == g ? sl : -1;
+    }
+    __device__ __forceinline__ void add(int g, double w) {
+        if (W) {
+            const int sl = lookup((uint32_t)g);
+            if (sl >= 0) {
+                double *d = reinterpret_cast<double *>(vals);
+                atomicAdd(d + sl, w);
+                atomicAdd(d + S + sl, w * w);
+            } else {
+                atomicAdd(pp->sumw + g, w);
+                atomicAdd(pp->sumw2 + g, w * w);
+            }
+        } else {
+            const unsigned act = __activemask();
+            const unsigned peers = __match_any_sync(act, g);
+            const int leader = __ffs(peers) - 1;
+            if ((int)(threadIdx.x & 31) == leader) {
+                const uint32_t c = (uint32_t)__popc(peers);
+                const int sl = lookup((uint32_t)g);
+                if (sl >= 0) atomicAdd(reinterpret_cast<uint32_t *>(vals) + sl, c);
+                else atomicAdd(pp->count + g, (unsigned long long)c);
+            }
+        }
+    }
+    __device__ __forceinline__ void flush(const FillP &p) {
+        for (int i = threadIdx.x; i < S; i += blockDim.x) {
+            const uint32_t k = keys[i];
+            if (k == kEmpty) continue;
+            if (W) {
+                const double *d = reinterpret_cast<const double *>(vals);
+                if (d[i] != 0.0) atomicAdd(p.sumw + k, d[i]);
+                if (d[S + i] != 0.0) atomicAdd(p.sumw2 + k, d[S + i]);
+            } else {
+                const uint32_t v = reinterpret_cast<const uint32_t *>(vals)[i];
+                if (v) atomicAdd(p.count + k, (unsigned long long)v);
+            }
+        }
+    }
+};
+
+template <int SINK, bool W> struct SinkOf;
+template <bool W> struct SinkOf<SINK_PRIV, W> { using T = PrivSink<W>; };
+template <bool W> struct SinkOf<SINK_GLOBAL, W> { using T = GlobalSink<W>; };
+template <bool W> struct SinkOf<SINK_CACHE, W> { using T = CacheSink<W>; };
+
+// ------------------------------------------------------------------ the fill kernel
+template <int DIM, bool W, typename S>
+__device__ __forceinline__ void do_event(const FillP &p, const double (&x)[DIM], double w, S &sink,
+                                         Acc<DIM, W> &acc) {
+    int g = 0, mul = 1;
+    bool inr = true;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const int b = find_bin(p.ax[a], x[a]);          // step (1), per axis
+        inr &= (b >= 1) & (b <= p.ax[a].n);
+        g += b * mul;
+        if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
+    }
+    sink.add(g, w);                                      // step (2): bin += w, sumw2 += w*w
+    if (inr) acc.add(x, w);                              // step (3): stats, in-range only (R6)
+}
+
+__device__ __forceinline__ double2 ld_stream2(const double *p, int64_t pair) {
+    return __ldcs(reinterpret_cast<const double2 *>(p) + pair);
+}
+
+// VEC: columns are read as double2 (LDG.E.128) after `peel` leading events.
+template <int DIM, bool W, int SINK, bool VEC>
+__global__ void __launch_bounds__(kThreads, 2) k_fill(FillP p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    using Sink_t = typename SinkOf<SINK, W>::T;
+    Sink_t sink;
+    if constexpr (SINK == SINK_GLOBAL) sink.pp = &p;
+    if constexpr (SINK == SINK_CACHE) sink.pp = &p;
+    if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots); else sink.init(smem, p.G);
+    if constexpr (SINK != SINK_GLOBAL) __syncthreads();
+
+    Acc<DIM, W> acc;
+    acc.zero();
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+
+    if constexpr (VEC) {
+        constexpr int U = 2;
+        const int64_t base = p.peel;
+        const int64_t npair = (p.n - base) >> 1;
+        const double *xs[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) xs[a] = p.x[a] + base;
+        const double *ws = W ? p.w + base : nullptr;
+        for (int64_t q0 = tid; q0 < npair; q0 += U * nth) {
+            double2 xv[U][DIM], wv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = q0 + u * nth;
+                if (q < npair) {
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) xv[u][a] = ld_stream2(xs[a], q);
+                    if (W) wv[u] = ld_stream2(ws, q);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = q0 + u * nth;
+                if (q < npair) {
+                    double x0[DIM], x1[DIM];
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) { x0[a] = xv[u][a].x; x1[a] = xv[u][a].y; }
+                    do_event<DIM, W>(p, x0, W ? wv[u].x : 1.0, sink, acc);
+                    do_event<DIM, W>(p, x1, W ? wv[u].y : 1.0, sink, acc);
+                }
+            }
+        }
+        // leading peeled events and the odd tail
+        const int64_t tail0 = base + 2 * npair;
+        const int64_t nscalar = base + (p.n - tail0);
+        if (tid < nscalar) {
+            const int64_t i = tid < base ? tid : tail0 + (tid - base);
+            double x[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) x[a] = p.x[a][i];
+            do_event<DIM, W>(p, x, W ? p.w[i] : 1.0, sink, acc);
+        }
+    } else {
+        for (int64_t i = tid; i < p.n; i += nth) {
+            double x[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) x[a] = __ldcs(p.x[a] + i);
+            do_event<DIM, W>(p, x, W ? __ldcs(p.w + i) : 1.0, sink, acc);
+        }
+    }
+
+    if constexpr (SINK != SINK_GLOBAL) {
+        __syncthreads();
+        sink.flush(p);
+    }
+    acc.finalize_unit();
+    block_stats_finish<Acc<DIM, W>::K>(p, acc.s);
+}
+
+// ------------------------------------------------------------------ auxiliary kernels
+// guide[c] = #{interior i in [1, n-1] : cell(e_i) < c}, c = 0..gcells (cell is monotone in i).
+__global__ void k_build_guide(AxisP a, uint32_t *guide) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > a.gcells) return;
+    int lo = 1, hi = a.n;            // first interior i with cell(e_i) >= c, in [1, n]
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (guide_cell(a, a.e[m]) < c) lo = m + 1; else hi = m;
+    }
+    guide[c] = (uint32_t)(lo - 1);
+}
+
+template <int DIM>
+__global__ void k_find_bins(FillP p, int32_t *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
+        int g = 0, mul = 1;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            g += find_bin(p.ax[a], p.x[a][i]) * mul;
+            if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
+        }
+        out[i] = g;
+    }
+}
+
+// packed = [content | sumw2 | stats | entries], content = count + sumw.
+__global__ void k_pack(int G, int K, const unsigned long long *count, const double *sumw, const double *sumw2,
+                       const double *stats, const unsigned long long *entries, double *out) {
+    const int64_t tot = 2 * (int64_t)G + K + 1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        double v;
+        if (i < G) v = (double)count[i] + sumw[i];
+        else if (i < 2 * (int64_t)G) v = (double)count[i - G] + sumw2[i - G];
+        else if (i < 2 * (int64_t)G + K) v = stats[i - 2 * G];
+        else v = (double)*entries;
+        out[i] = v;
+    }
+}
+
+__global__ void k_unpack(int G, int K, unsigned long long *count, double *sumw, double *sumw2, double *stats,
+                         unsigned long long *entries, const double *in) {
+    const int64_t tot = 2 * (int64_t)G + K + 1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = in[i];
+        if (i < G) { count[i] = 0ull; sumw[i] = v; }
+        else if (i < 2 * (int64_t)G) sumw2[i - G] = v;
+        else if (i < 2 * (int64_t)G + K) stats[i - 2 * G] = v;
+        else *entries = (unsigned long long)v;
+    }
+}
+
+}  // namespace bh

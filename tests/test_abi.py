@@ -1,0 +1,65 @@
+"""CPU-side checks of the C-ABI boundary: the library loads, exports every symbol the
+header declares, and fails loudly (status codes, no crash, no fallback) without a GPU."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2401_13310_b200 as pkg
+from paper_2401_13310_b200 import _build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "bhist.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bh_[a-z_]+)\s*\(", src)))
+
+
+def test_library_builds_and_loads():
+    _build.build()
+    assert os.path.exists(_build.SO)
+    assert pkg.bh_version() >= 10000
+
+
+def test_every_declared_symbol_exported():
+    declared = _declared()
+    assert declared == sorted(pkg.EXPORTED)
+    L = ctypes.CDLL(_build.SO)
+    for name in declared:
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _build.SO], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\sT\s(bh_\w+)", out))
+    assert set(declared) <= exported
+
+
+def test_kernels_are_sm100a_sass():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", _build.SO], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(pkg.BHistError) as ei:
+        pkg.bh_create([(10, 0.0, 1.0)], 0)
+    assert ei.value.status in (-4, -3)   # BH_EDEVICE / BH_ECUDA, never a silent success
+
+
+def test_null_handle_rejected():
+    L = pkg.lib()
+    assert L.bh_reset(None, None) == -1
+    assert L.bh_fill(None, 1, None, None, None) == -1
+    assert "NULL" in pkg.bh_last_error()
+
+
+def test_product_does_not_import_oracle():
+    for dirpath, _, files in os.walk(os.path.join(ROOT, "paper_2401_13310_b200")):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower(), f

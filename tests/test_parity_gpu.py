@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical
+seeded inputs.  Bin indices and unit-weight counts bit-exact; weighted sums within
+1e-12 of sum|term| (BASELINE.json north star)."""
+import math
+
+import numpy as np
+import pytest
+
+import bhgen
+import oracle
+import paper_2401_13310_b200 as pkg
+from _helpers import compare, gen_columns, oracle_parallel
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+STRATS = {"priv": pkg.BH_STRATEGY_PRIV, "global": pkg.BH_STRATEGY_GLOBAL, "cache": pkg.BH_STRATEGY_CACHE}
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _gpu_fill(axes, cols, w, strategy=pkg.BH_STRATEGY_AUTO, splits=1):
+    h = pkg.Histogram(axes, strategy=strategy)
+    n = len(cols[0])
+    tc = [_t(c) for c in cols]
+    tw = None if w is None else _t(w)
+    cuts = np.linspace(0, n, splits + 1).astype(int)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        h.fill([c[a:b] for c in tc], None if tw is None else tw[a:b])
+    r = h.read()
+    h.close()
+    return r
+
+
+def _adversarial(axis, rng, m=4000):
+    """Coordinates at and around every edge (+-3 ulps), flow values, NaN/inf, -0.0."""
+    if isinstance(axis, np.ndarray):
+        edges = axis
+    else:
+        n, lo, hi = axis
+        edges = np.array([lo + i * (hi - lo) / n for i in range(n + 1)])
+    pick = edges[rng.integers(0, len(edges), size=m)]
+    xs = [pick]
+    up = dn = pick
+    for _ in range(3):
+        up, dn = np.nextafter(up, np.inf), np.nextafter(dn, -np.inf)
+        xs += [up, dn]
+    xs.append(np.array([np.nan, np.inf, -np.inf, -0.0, 0.0, edges[0], edges[-1],
+                        np.nextafter(edges[-1], -np.inf), np.nextafter(edges[0], -np.inf), 1e308, -1e308]))
+    return np.concatenate(xs)
+
+
+# ------------------------------------------------------------------ FindBin bit-exact
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_find_bins_bit_exact(name):
+    wl = bhgen.workload(name, 1_000_003)
+    rng = np.random.default_rng(hash(name) % 2 ** 32)
+    for hist in wl.hists:
+        axes = oracle.oracle_axes(hist)
+        cols, _ = gen_columns(wl, hist, 0, wl.n_events)
+        adv = [_adversarial(ax, rng) for ax in axes]
+        m = min(len(a) for a in adv)
+        cols = [np.concatenate([c, rng.permutation(a)[:m]]) for c, a in zip(cols, adv)]
+        ref = oracle.OracleHist(axes).find_bins(cols)
+        h = pkg.Histogram(axes)
+        got = h.find_bins([_t(c) for c in cols]).cpu().numpy()
+        h.close()
+        assert np.array_equal(got, ref), (name, np.flatnonzero(got != ref)[:10])
+
+
+def test_find_bins_random_axes():
+    rng = np.random.default_rng(2024)
+    for trial in range(40):
+        if trial % 2:
+            n = int(rng.integers(1, 3000))
+            edges = np.cumsum(rng.uniform(1e-3, 1.0, n + 1) ** 3) + rng.uniform(-5, 5)
+            if trial % 4 == 1:   # log-spaced, very non-uniform cells
+                edges = np.geomspace(1e-4, 10.0, n + 1)
+            ax = edges
+        else:
+            n = int(rng.choice([1, 3, 100, 1000, 12345, 2 ** 20]))
+            lo = float(rng.uniform(-100, 100))
+            ax = (n, lo, lo + float(10 ** rng.uniform(-5, 5)))
+        lo_, hi_ = (ax[0], ax[-1]) if isinstance(ax, np.ndarray) else (ax[1], ax[2])
+        xs = np.concatenate([rng.uniform(lo_ - (hi_ - lo_) * 0.1, hi_ + (hi_ - lo_) * 0.1, 20000), _adversarial(ax, rng, 2000)])
+        ref = oracle.OracleHist([ax]).find_bins([xs])
+        h = pkg.Histogram([ax])
+        got = h.find_bins([_t(xs)]).cpu().numpy()
+        h.close()
+        assert np.array_equal(got, ref), (trial, np.flatnonzero(got != ref)[:5])
+
+
+# ------------------------------------------------------------------ fills vs oracle
+CASES = [("C1", 1_000_000), ("C2", 2_000_003), ("C3", 2_000_001), ("C3W", 1_000_001), ("C4", 2_000_000),
+         ("C4W", 1_000_003)]
+
+
+@pytest.mark.parametrize("name,n", CASES)
+@pytest.mark.parametrize("strat", ["auto", "priv", "global", "cache"])
+def test_fill_parity(name, n, strat):
+    wl = bhgen.workload(name, n)
+    hist = wl.hists[0]
+    axes = oracle.oracle_axes(hist)
+    if strat == "priv" and (16 if hist.weighted else 4) * np.prod([a.nbins + 2 for a in hist.axes]) > 200 * 1024:
+        pytest.skip("bin space does not fit shared memory")
+    cols, w = gen_columns(wl, hist, 0, n)
+    ref = oracle.OracleHist(axes).fill(cols, w).read()
+    got = _gpu_fill(axes, cols, w, pkg.BH_STRATEGY_AUTO if strat == "auto" else STRATS[strat])
+    compare(got, ref, hist.weighted, f"{name}/{strat}")
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 5, 31, 33, 1023, 4097])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_tiny_and_ragged(n, weighted):
+    rng = np.random.default_rng(n)
+    axes = [(7, 0.0, 1.0), np.array([-0.5, 0.0, 0.2, 0.9, 1.5])]
+    cols = [rng.uniform(-0.2, 1.2, n), rng.uniform(-1, 2, n)]
+    w = rng.uniform(-1, 2, n) if weighted else None
+    ref = oracle.OracleHist(axes).fill(cols, w).read()
+    for s in STRATS.values():
+        compare(_gpu_fill(axes, cols, w, s), ref, weighted, f"n={n}")
+
+
+@pytest.mark.parametrize("offset", [1, 3])
+def test_unaligned_and_mixed_phase_columns(offset):
+    wl = bhgen.workload("C3W", 300_001)
+    hist = wl.hists[0]
+    axes = oracle.oracle_axes(hist)
+    cols, w = gen_columns(wl, hist, 0, wl.n_events)
+    ref = oracle.OracleHist(axes).fill([c[offset:] for c in cols], w[offset:]).read()
+    tc = [_t(c) for c in cols]
+    tw = _t(w)
+    for s in STRATS.values():
+        if s == pkg.BH_STRATEGY_PRIV:
+            continue
+        h = pkg.Histogram(axes, strategy=s)
+        h.fill([c[offset:] for c in tc], tw[offset:])            # same phase: peeled vector path
+        compare(h.read(), ref, True, f"same-phase {offset}")
+        h.close()
+    # mixed phases: x shifted by `offset`, y and w copied so their phase differs -> scalar path
+    y2 = torch.empty(len(cols[1]) + 1, dtype=torch.float64, device=DEV)
+    y2[1 + offset:] = tc[1][offset:]
+    w2 = torch.empty(len(w) + 1, dtype=torch.float64, device=DEV)
+    w2[1 + offset:] = tw[offset:]
+    h = pkg.Histogram(axes, strategy=pkg.BH_STRATEGY_GLOBAL)
+    h.fill([tc[0][offset:], y2[1 + offset:]], w2[1 + offset:])
+    compare(h.read(), ref, True, "mixed-phase")
+    h.close()
+
+
+def test_accumulation_across_fills_and_reset():
+    # include-initial semantics: B fills == 1 fill; reset zeroes
+    wl = bhgen.workload("C2", 1_000_000)
+    hist = wl.hists[0]
+    axes = oracle.oracle_axes(hist)
+    cols, w = gen_columns(wl, hist, 0, wl.n_events)
+    ref = oracle.OracleHist(axes).fill(cols, w).read()
+    for splits in (2, 7, 32):
+        compare(_gpu_fill(axes, cols, w, splits=splits), ref, True, f"splits={splits}")
+    wl1 = bhgen.workload("C1", 1_000_000)
+    x = wl1.column(0, 0, wl1.n_events)
+    ref1 = oracle.OracleHist([(100, 0.0, 1.0)]).fill([x]).read()
+    for splits in (2, 7, 32):
+        got = _gpu_fill([(100, 0.0, 1.0)], [x], None, splits=splits)
+        compare(got, ref1, False)
+    h = pkg.Histogram([(100, 0.0, 1.0)])
+    h.fill([_t(x)]).reset()
+    r = h.read()
+    assert r["entries"] == 0 and not r["content"].any() and not r["stats"].any()
+    h.fill([_t(x)])
+    compare(h.read(), ref1, False, "after reset")
+    h.close()
+
+
+def test_mixed_unit_and_weighted_fills():
+    rng = np.random.default_rng(3)
+    axes = [(50, 0.0, 1.0)]
+    x1, x2 = rng.uniform(0, 1, 100_000), rng.uniform(-0.1, 1.1, 100_000)
+    w2 = rng.uniform(0.5, 1.5, 100_000)
+    ref = oracle.OracleHist(axes).fill([x1]).fill([x2], w2).read()
+    h = pkg.Histogram(axes)
+    h.fill([_t(x1)]).fill([_t(x2)], _t(w2))
+    compare(h.read(), ref, True)
+    h.close()
+
+
+def test_pack_unpack_merge():
+    # multi-GPU exchange step emulated on one device: the SUM of packed
+    # partial states, unpacked, equals the oracle over all events.
+    wl = bhgen.workload("C3W", 400_000)
+    hist = wl.hists[0]
+    axes = oracle.oracle_axes(hist)
+    ref = oracle.OracleHist(axes)
+    bufs = []
+    for r in range(4):
+        a, b = bhgen.shard(wl.n_events, r, 4)
+        cols, w = gen_columns(wl, hist, a, b - a)
+        ref.fill(cols, w)
+        h = pkg.Histogram(axes)
+        h.fill([_t(c) for c in cols], _t(w))
+        bufs.append(h.pack())
+        h.close()
+    total = torch.stack(bufs).sum(0)
+    h = pkg.Histogram(axes)
+    h.unpack(total)
+    compare(h.read(), ref.read(), True, "pack/unpack")
+    # unpacked state keeps accumulating
+    cols, w = gen_columns(wl, hist, 0, 1000)
+    ref.fill(cols, w)
+    h.fill([_t(c) for c in cols], _t(w))
+    compare(h.read(), ref.read(), True, "unpack+fill")
+    h.close()
+
+
+# ------------------------------------------------------------------ host -> device path
+@pytest.mark.parametrize("pinned", [True, False])
+def test_fill_host_double_buffered(pinned):
+    wl = bhgen.workload("C2", 3_000_017)
+    hist = wl.hists[0]
+    axes = oracle.oracle_axes(hist)
+    cols, w = gen_columns(wl, hist, 0, wl.n_events)
+    ref = oracle.OracleHist(axes).fill(cols, w).read()
+    hc = [torch.from_numpy(c) for c in cols]
+    hw = torch.from_numpy(w)
+    if pinned:
+        hc = [c.pin_memory() for c in hc]
+        hw = hw.pin_memory()
+    h = pkg.Histogram(axes)
+    pkg.bh_set_chunk(h.h, 100_000)          # 31 chunks through a 2-slot ring
+    h.fill_host(hc, hw)
+    compare(h.read(), ref, True, f"fill_host pinned={pinned}")
+    h.close()
+
+
+def test_fill_host_returns_after_host_bytes_consumed():
+    # the host bulk buffer may be overwritten as soon as fill_host returns
+    rng = np.random.default_rng(8)
+    axes = [(1000, 0.0, 1.0)]
+    h = pkg.Histogram(axes)
+    ref = oracle.OracleHist(axes)
+    buf = torch.empty(1 << 20, dtype=torch.float64).pin_memory()
+    for it in range(8):
+        x = rng.uniform(0, 1, 1 << 20)
+        buf.numpy()[:] = x           # refill the same host buffer every bulk
+        h.fill_host([buf])
+        ref.fill([x])
+    compare(h.read(), ref.read(), False, "buffer reuse")
+    h.close()
+
+
+def test_negative_control_skip_copy_wait():
+    # fault injection: filling without waiting for the H2D copy must break parity
+    wl = bhgen.workload("C1", 4_000_000)
+    x = wl.column(0, 0, wl.n_events)
+    ref = oracle.OracleHist([(100, 0.0, 1.0)]).fill([x]).read()
+    hx = torch.from_numpy(x).pin_memory()
+    h = pkg.Histogram([(100, 0.0, 1.0)])
+    pkg.bh_set_chunk(h.h, 1 << 20)
+    pkg.bh_set_debug(h.h, pkg.BH_DEBUG_SKIP_COPY_WAIT)
+    h.fill_host([hx])
+    got = h.read()
+    h.close()
+    assert not np.array_equal(got["content"], ref["content"])
+
+
+# ------------------------------------------------------------------ full size (bench shapes)
+def _gpu_full(name, strategy=pkg.BH_STRATEGY_AUTO, chunk=1 << 25):
+    wl = bhgen.workload(name)
+    hist = wl.hists[0]
+    h = pkg.Histogram(oracle.oracle_axes(hist), strategy=strategy)
+    ncol = len(hist.cols) + (1 if hist.weighted else 0)
+    host = [torch.empty(chunk, dtype=torch.float64).pin_memory() for _ in range(ncol)]
+    for off in range(0, wl.n_events, chunk):
+        m = min(chunk, wl.n_events - off)
+        for j, c in enumerate(hist.cols):
+            wl.column_ptr(c, off, m, host[j].data_ptr())
+        if hist.weighted:
+            wl.column_ptr(wl.wcol, off, m, host[-1].data_ptr())
+        h.fill_host([t[:m] for t in host[:len(hist.cols)]], host[-1][:m] if hist.weighted else None)
+    r = h.read()
+    h.close()
+    return wl, r
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_full_size_against_sharded_oracle(name):
+    wl, got = _gpu_full(name)
+    ref = oracle_parallel(name, wl.n_events)
+    compare(got, ref, wl.hists[0].weighted, f"full {name}")

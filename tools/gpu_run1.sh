@@ -1,0 +1,3 @@
+set -x
+python __graft_entry__.py smoke 2>&1 | tail -5
+timeout 900 python -m pytest tests/test_parity_gpu.py -x -q -m "gpu and not slow" 2>&1 | tail -30

@@ -117,6 +117,10 @@ class Hist:
     cols: list          # column index per axis
     weighted: bool
 
+    def axes_spec(self) -> list:
+        """[(nbins, xmin, xmax) | edges ndarray] per axis, the form both bindings accept."""
+        return [ax.edges if ax.edges is not None else (ax.nbins, ax.xmin, ax.xmax) for ax in self.axes]
+
 
 @dataclass
 class Workload:

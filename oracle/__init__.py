@@ -149,7 +149,7 @@ class OracleHist:
 
 def oracle_axes(hist) -> list:
     """bhgen.Hist -> OracleHist axes spec."""
-    return [ax.edges if ax.edges is not None else (ax.nbins, ax.xmin, ax.xmax) for ax in hist.axes]
+    return hist.axes_spec()
 
 
 def finalize_stats(stats, dim: int):

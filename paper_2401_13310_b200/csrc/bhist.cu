@@ -96,19 +96,31 @@ int resolve_strategy(const bh_hist *h, bool weighted) {
     const size_t budget = 160 * 1024;
     const size_t priv = weighted ? 16 * (size_t)h->G : 4 * (size_t)h->G;
     if (priv <= budget) return BH_STRATEGY_PRIV;
-    return BH_STRATEGY_GLOBAL;
+    // large bin spaces: shared-memory cache of the hottest bins in front of L2 atomics
+    // (as fast as plain GLOBAL on uniform data, 30x faster on the peaked C4 shape)
+    return BH_STRATEGY_CACHE;
 }
 
 int cache_slots_for(bool weighted) { return weighted ? 4096 : 16384; }
 
-size_t smem_bytes(const bh_hist *h, int strategy, bool weighted) {
-    if (strategy == BH_STRATEGY_PRIV) return weighted ? 16 * (size_t)h->G : 4 * (size_t)h->G;
+size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+
+size_t sink_bytes(const bh_hist *h, int strategy, bool weighted) {
+    if (strategy == BH_STRATEGY_PRIV) return align16(weighted ? 16 * (size_t)h->G : 4 * (size_t)h->G);
     if (strategy == BH_STRATEGY_CACHE) {
         const size_t S = cache_slots_for(weighted);
         return S * 4 + (weighted ? 16 * S : 4 * S);
     }
     return 0;
 }
+
+// Bytes of shared memory the variable-axis tables take (float32 edges + guide).
+size_t axis_table_bytes(const AxisP &a) {
+    if (!a.var) return 0;
+    return align16(4 * (size_t)(a.n + 1)) + align16((a.g16 ? 2 : 4) * (size_t)(a.gcells + 1));
+}
+
+constexpr size_t kStaticSmemReserve = 4096;   // block_stats_finish scratch + driver reserve
 
 FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, const double *w) {
     FillP p{};
@@ -130,79 +142,100 @@ FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, cons
     return p;
 }
 
-template <int DIM, bool W, int SINK, bool VEC>
-cudaError_t launch_t(const bh_hist *h, const FillP &p, int grid, size_t smem, cudaStream_t s) {
-    auto kern = k_fill<DIM, W, SINK, VEC>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+struct LaunchCfg {
+    int strategy;
+    bool weighted, vec, vsm;
+    int grid;
+    size_t smem;
+};
+
+template <int DIM, bool W, int SINK, bool VEC, bool VSM>
+cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    auto kern = k_fill<DIM, W, SINK, VEC, VSM>;
+    if (c.smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
         if (e != cudaSuccess) return e;
     }
-    kern<<<grid, kThreads, smem, s>>>(p);
+    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
     return cudaGetLastError();
 }
 
+template <int DIM, bool W, int SINK, bool VEC>
+cudaError_t launch_m(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    return c.vsm ? launch_t<DIM, W, SINK, VEC, true>(p, c, s) : launch_t<DIM, W, SINK, VEC, false>(p, c, s);
+}
+
 template <int DIM, bool W, int SINK>
-cudaError_t launch_v(const bh_hist *h, const FillP &p, bool vec, int grid, size_t smem, cudaStream_t s) {
-    return vec ? launch_t<DIM, W, SINK, true>(h, p, grid, smem, s) : launch_t<DIM, W, SINK, false>(h, p, grid, smem, s);
+cudaError_t launch_v(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    return c.vec ? launch_m<DIM, W, SINK, true>(p, c, s) : launch_m<DIM, W, SINK, false>(p, c, s);
 }
 
 template <int DIM, bool W>
-cudaError_t launch_s(const bh_hist *h, const FillP &p, int strategy, bool vec, int grid, size_t smem, cudaStream_t s) {
-    switch (strategy) {
-    case BH_STRATEGY_PRIV: return launch_v<DIM, W, SINK_PRIV>(h, p, vec, grid, smem, s);
-    case BH_STRATEGY_CACHE: return launch_v<DIM, W, SINK_CACHE>(h, p, vec, grid, smem, s);
-    default: return launch_v<DIM, W, SINK_GLOBAL>(h, p, vec, grid, smem, s);
+cudaError_t launch_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    switch (c.strategy) {
+    case BH_STRATEGY_PRIV: return launch_v<DIM, W, SINK_PRIV>(p, c, s);
+    case BH_STRATEGY_CACHE: return launch_v<DIM, W, SINK_CACHE>(p, c, s);
+    default: return launch_v<DIM, W, SINK_GLOBAL>(p, c, s);
     }
 }
 
 template <int DIM>
-cudaError_t launch_d(const bh_hist *h, const FillP &p, bool weighted, int strategy, bool vec, int grid, size_t smem,
-                     cudaStream_t s) {
-    return weighted ? launch_s<DIM, true>(h, p, strategy, vec, grid, smem, s)
-                    : launch_s<DIM, false>(h, p, strategy, vec, grid, smem, s);
+cudaError_t launch_d(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    return c.weighted ? launch_s<DIM, true>(p, c, s) : launch_s<DIM, false>(p, c, s);
 }
 
-// Blocks resident per SM for a strategy (occupancy-limited by shared memory and by
-// __launch_bounds__(kThreads, 2)).
-int resident_blocks(const bh_hist *h, size_t smem) {
-    int by_smem = smem ? (int)std::min<size_t>(2, (228 * 1024) / (smem + 1024)) : 2;
-    return std::max(1, by_smem);
-}
+int threads_of(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? kThreadsGlobal : kThreadsSmem; }
+int resident_blocks(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? 2 : 1; }
 
 // One fill over device-resident columns, split into launches of <= 2^31 events.
 bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
-    const bool weighted = w != nullptr;
-    const int strategy = resolve_strategy(h, weighted);
-    const size_t smem = smem_bytes(h, strategy, weighted);
-    if (smem > h->smem_optin)
-        return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", strategy, smem, h->smem_optin);
+    LaunchCfg c{};
+    c.weighted = w != nullptr;
+    c.strategy = resolve_strategy(h, c.weighted);
+    const size_t sink = sink_bytes(h, c.strategy, c.weighted);
+    // variable-axis tables go to shared memory behind the sink when they fit
+    size_t tabs = 0;
+    AxisP ax[kMaxDim];
+    for (int a = 0; a < h->dim; ++a) {
+        ax[a] = h->ax[a];
+        if (ax[a].var) {
+            ax[a].tab_off = (int32_t)(sink + tabs);
+            tabs += axis_table_bytes(ax[a]);
+        }
+    }
+    c.vsm = tabs > 0 && sink + tabs + kStaticSmemReserve <= h->smem_optin;
+    c.smem = sink + (c.vsm ? tabs : 0);
+    if (c.smem + kStaticSmemReserve > h->smem_optin)
+        return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", c.strategy, c.smem, h->smem_optin);
     const int64_t kMaxLaunch = int64_t(1) << 31;
     for (int64_t off = 0; off < n; off += kMaxLaunch) {
         const int64_t m = std::min(kMaxLaunch, n - off);
         const double *cs[kMaxDim] = {};
         for (int a = 0; a < h->dim; ++a) cs[a] = coords[a] + off;
-        const double *ws = weighted ? w + off : nullptr;
+        const double *ws = c.weighted ? w + off : nullptr;
         FillP p = make_params(h, m, cs, ws);
+        for (int a = 0; a < h->dim; ++a) p.ax[a] = ax[a];
         // vector path: every column must share the same 16-byte phase
         const uintptr_t ph = reinterpret_cast<uintptr_t>(cs[0]) & 15;
-        bool vec = (ph % 8) == 0;
-        for (int a = 1; a < h->dim; ++a) vec &= (reinterpret_cast<uintptr_t>(cs[a]) & 15) == ph;
-        if (weighted) vec &= (reinterpret_cast<uintptr_t>(ws) & 15) == ph;
-        p.peel = vec && ph ? 1 : 0;
+        c.vec = (ph % 8) == 0;
+        for (int a = 1; a < h->dim; ++a) c.vec &= (reinterpret_cast<uintptr_t>(cs[a]) & 15) == ph;
+        if (c.weighted) c.vec &= (reinterpret_cast<uintptr_t>(ws) & 15) == ph;
+        p.peel = c.vec && ph ? 1 : 0;
         if (p.peel > m) p.peel = (int32_t)m;
-        p.cache_slots = cache_slots_for(weighted);
-        // launch shape: persistent grid, but each block should see enough events to
-        // amortize zeroing + flushing its private bins
-        const int per_sm = resident_blocks(h, smem);
-        int64_t want_per_block = kThreads * 8;
-        if (strategy == BH_STRATEGY_PRIV) want_per_block = std::max<int64_t>(want_per_block, 4 * h->G);
+        p.cache_slots = cache_slots_for(c.weighted);
+        // launch shape: persistent grid (resident CTAs on every SM), but each block
+        // should see enough events to amortize zeroing + flushing its private bins
+        const int nt = threads_of(c.strategy);
+        int64_t want_per_block = (int64_t)nt * 8;
+        if (c.strategy == BH_STRATEGY_PRIV) want_per_block = std::max<int64_t>(want_per_block, 4 * h->G);
         int64_t grid = (m + want_per_block - 1) / want_per_block;
-        grid = std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)h->nsm * per_sm));
+        grid = std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)h->nsm * resident_blocks(c.strategy)));
+        c.grid = (int)grid;
         cudaError_t e;
         switch (h->dim) {
-        case 1: e = launch_d<1>(h, p, weighted, strategy, vec, (int)grid, smem, s); break;
-        case 2: e = launch_d<2>(h, p, weighted, strategy, vec, (int)grid, smem, s); break;
-        default: e = launch_d<3>(h, p, weighted, strategy, vec, (int)grid, smem, s); break;
+        case 1: e = launch_d<1>(p, c, s); break;
+        case 2: e = launch_d<2>(p, c, s); break;
+        default: e = launch_d<3>(p, c, s); break;
         }
         if (e != cudaSuccess) return fail(BH_ECUDA, "fill launch: %s", cudaGetErrorString(e));
         ++h->launches;
@@ -303,8 +336,8 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
             P.var = 1;
             P.xmin = A.edges[0];
             P.xmax = A.edges[A.nbins];
-            int gc = 1;
-            while (gc < A.nbins && gc < (1 << 22)) gc <<= 1;
+            int gc = 1;                       // about one interior edge per cell, power of two
+            while (2 * gc < A.nbins && gc < (1 << 22)) gc <<= 1;
             P.gcells = gc;
             P.gscale = (double)gc / (P.xmax - P.xmin);
             if (!std::isfinite(P.gscale) || !(P.gscale > 0)) return cleanup(fail(BH_EINVAL, "axis %d: edge range too small", a));
@@ -316,9 +349,15 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
             h->axis_mem.push_back(dg2);
             if (cudaMemcpy(de, A.edges, sizeof(double) * (A.nbins + 1), cudaMemcpyHostToDevice) != cudaSuccess)
                 return cleanup(fail(BH_ECUDA, "edge upload failed"));
+            float *de32 = nullptr;
+            ALLOC(de32, sizeof(float) * (A.nbins + 1));
+            h->axis_mem.push_back(de32);
             P.e = de;
             P.guide = dg2;
+            P.e32 = de32;
+            P.g16 = (A.nbins - 1) < 65536 ? 1 : 0;
             k_build_guide<<<(gc + 1 + 255) / 256, 256>>>(P, dg2);
+            k_edges_f32<<<(A.nbins + 1 + 255) / 256, 256>>>(de, A.nbins + 1, de32);
             if (cudaGetLastError() != cudaSuccess) return cleanup(fail(BH_ECUDA, "guide build launch failed"));
         }
     }
@@ -521,7 +560,7 @@ bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *sta
 bh_status bh_set_strategy(bh_hist *h, int32_t strategy) {
     if (check_hist(h)) return BH_EINVAL;
     if (strategy < BH_STRATEGY_AUTO || strategy > BH_STRATEGY_CACHE) return fail(BH_EINVAL, "unknown strategy %d", strategy);
-    if (strategy == BH_STRATEGY_PRIV && 4 * (size_t)h->G > h->smem_optin)
+    if (strategy == BH_STRATEGY_PRIV && 4 * (size_t)h->G + kStaticSmemReserve > h->smem_optin)
         return fail(BH_EINVAL, "PRIV cannot hold %lld bins in shared memory", (long long)h->G);
     h->strategy = strategy;
     return BH_OK;

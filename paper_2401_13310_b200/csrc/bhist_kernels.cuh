@@ -15,7 +15,9 @@
 namespace bh {
 
 constexpr int kMaxDim = 3;
-constexpr int kThreads = 512;
+constexpr int kThreadsGlobal = 512;   // GLOBAL sink: 2 CTAs/SM
+constexpr int kThreadsSmem = 1024;    // PRIV / CACHE sinks: 1 CTA/SM owns the SM's shared memory
+template <int SINK> struct ThreadsOf { static constexpr int v = SINK == 1 ? kThreadsGlobal : kThreadsSmem; };
 
 // Axis as the kernels see it.  Fixed axes use (xmin, xmax, D = xmax-xmin,
 // inv = n/D), all rounded once on the host exactly as the definition rounds them.
@@ -31,6 +33,9 @@ struct AxisP {
     const uint32_t *guide;   // variable: gcells+1 entries, guide[c] = #{interior i : cell(e_i) < c}
     int32_t gcells;          // variable: number of cells (power of two)
     double gscale;           // variable: gcells / (e[n] - e[0])
+    const float *e32;        // variable: RN-to-float32 copy of the edges (device), staged in smem
+    int32_t tab_off;         // variable + VSM: byte offset of [e32 | guide] in dynamic smem
+    int32_t g16;             // variable + VSM: guide staged as uint16 (n-1 < 65536)
 };
 
 struct FillP {
@@ -102,8 +107,63 @@ __device__ __forceinline__ int find_bin_var_global(const AxisP &a, double x) {
     return find_bin_var_impl(a, x, a.guide, [&](int i) { return __ldg(a.e + i); });
 }
 
-__device__ __forceinline__ int find_bin(const AxisP &a, double x) {
-    return a.var ? find_bin_var_global(a, x) : find_bin_fixed(a, x);
+// Shared-memory variant: the guide and a float32 copy of the edges live in smem.
+// RN-to-float is monotone, so e32_i < x32 implies e_i < x and e32_i > x32 implies
+// e_i > x; only a float tie needs the exact float64 edge (global, ~1e-3 of events
+// on the C2 axis).  The result is therefore identical to the float64 search.
+template <bool G16>
+__device__ __forceinline__ int find_bin_var_smem(const AxisP &a, double x, const unsigned char *tab) {
+    if (x < a.xmin) return 0;
+    if (!(x < a.xmax)) return a.n + 1;
+    const float *e32 = reinterpret_cast<const float *>(tab);
+    const unsigned char *gt = tab + ((4 * (a.n + 1) + 15) & ~15);
+    const int c = guide_cell(a, x);
+    int lo, hi;
+    if (G16) {
+        lo = reinterpret_cast<const uint16_t *>(gt)[c];
+        hi = reinterpret_cast<const uint16_t *>(gt)[c + 1];
+    } else {
+        lo = (int)reinterpret_cast<const uint32_t *>(gt)[c];
+        hi = (int)reinterpret_cast<const uint32_t *>(gt)[c + 1];
+    }
+    const float x32 = __double2float_rn(x);
+    while (lo < hi) {
+        const int m = (lo + hi + 1) >> 1;
+        const float em = e32[m];
+        const bool le = em < x32 ? true : (em > x32 ? false : (__ldg(a.e + m) <= x));
+        if (le) lo = m; else hi = m - 1;
+    }
+    return 1 + lo;
+}
+
+template <bool VSM>
+__device__ __forceinline__ int find_bin(const AxisP &a, double x, const unsigned char *smem) {
+    if (!a.var) return find_bin_fixed(a, x);
+    if (VSM) {
+        return a.g16 ? find_bin_var_smem<true>(a, x, smem + a.tab_off) : find_bin_var_smem<false>(a, x, smem + a.tab_off);
+    }
+    return find_bin_var_global(a, x);
+}
+
+__device__ __forceinline__ int find_bin(const AxisP &a, double x) { return find_bin<false>(a, x, nullptr); }
+
+// Copy each variable axis' float32 edges and guide table into shared memory.
+template <int DIM>
+__device__ __forceinline__ void stage_axes(const AxisP *ax, unsigned char *smem) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        if (!ax[a].var) continue;
+        float *e32 = reinterpret_cast<float *>(smem + ax[a].tab_off);
+        for (int i = threadIdx.x; i <= ax[a].n; i += blockDim.x) e32[i] = ax[a].e32[i];
+        unsigned char *gt = smem + ax[a].tab_off + ((4 * (ax[a].n + 1) + 15) & ~15);
+        if (ax[a].g16) {
+            for (int i = threadIdx.x; i <= ax[a].gcells; i += blockDim.x)
+                reinterpret_cast<uint16_t *>(gt)[i] = (uint16_t)ax[a].guide[i];
+        } else {
+            for (int i = threadIdx.x; i <= ax[a].gcells; i += blockDim.x)
+                reinterpret_cast<uint32_t *>(gt)[i] = ax[a].guide[i];
+        }
+    }
 }
 
 // ------------------------------------------------------------------ stats
@@ -150,7 +210,7 @@ struct Acc {
 // (include-initial) and adds the event count to entries.
 template <int K>
 __device__ __forceinline__ void block_stats_finish(const FillP &p, double (&s)[K]) {
-    __shared__ double red[kThreads / 32][K];
+    __shared__ double red[1024 / 32][K];
     __shared__ bool last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -248,9 +308,10 @@ struct GlobalSink {
 
 // CACHE sink: direct-mapped shared-memory cache of global bins.  A slot is
 // claimed by the first bin that hashes to it (32-bit CAS, native); hits add in
-// shared memory, misses go to global atomics.  Unit weights first aggregate equal
-// bins across the warp (match.any) so the hottest bin costs one shared atomic per
-// warp instead of up to 32 serialized ones.
+// shared memory, misses go to global atomics.  Equal bins are first aggregated
+// across the warp (match.any; counts by popc, weights by a shuffle walk over the
+// peer mask) so the hottest bin costs one atomic per warp instead of up to 32
+// serialized ones (hot-bin contention, BASELINE.json config 4).
 template <bool W>
 struct CacheSink {
     uint32_t *keys;
@@ -282,21 +343,34 @@ struct CacheSink {
         return k == g ? sl : -1;
     }
     __device__ __forceinline__ void add(int g, double w) {
+        const unsigned act = __activemask();
+        const unsigned peers = __match_any_sync(act, g);
+        const int lane = (int)(threadIdx.x & 31);
+        const int leader = __ffs(peers) - 1;
         if (W) {
-            const int sl = lookup((uint32_t)g);
-            if (sl >= 0) {
-                double *d = reinterpret_cast<double *>(vals);
-                atomicAdd(d + sl, w);
-                atomicAdd(d + S + sl, w * w);
-            } else {
-                atomicAdd(pp->sumw + g, w);
-                atomicAdd(pp->sumw2 + g, w * w);
+            // each lane sums w and w*w over its peer group (lane order), walking its own
+            // peer mask; every lane runs the same number of shuffles (the largest group)
+            const int rounds = __reduce_max_sync(act, (unsigned)__popc(peers));
+            double s1 = 0.0, s2 = 0.0;
+            unsigned m = peers;
+            for (int k = 0; k < rounds; ++k) {
+                const int src = m ? __ffs(m) - 1 : lane;
+                const double v = __shfl_sync(act, w, src);
+                if (m) { s1 += v; s2 = fma(v, v, s2); m &= m - 1; }
+            }
+            if (lane == leader) {
+                const int sl = lookup((uint32_t)g);
+                if (sl >= 0) {
+                    double *d = reinterpret_cast<double *>(vals);
+                    atomicAdd(d + sl, s1);
+                    atomicAdd(d + S + sl, s2);
+                } else {
+                    atomicAdd(pp->sumw + g, s1);
+                    atomicAdd(pp->sumw2 + g, s2);
+                }
             }
         } else {
-            const unsigned act = __activemask();
-            const unsigned peers = __match_any_sync(act, g);
-            const int leader = __ffs(peers) - 1;
-            if ((int)(threadIdx.x & 31) == leader) {
+            if (lane == leader) {
                 const uint32_t c = (uint32_t)__popc(peers);
                 const int sl = lookup((uint32_t)g);
                 if (sl >= 0) atomicAdd(reinterpret_cast<uint32_t *>(vals) + sl, c);
@@ -326,14 +400,14 @@ template <bool W> struct SinkOf<SINK_GLOBAL, W> { using T = GlobalSink<W>; };
 template <bool W> struct SinkOf<SINK_CACHE, W> { using T = CacheSink<W>; };
 
 // ------------------------------------------------------------------ the fill kernel
-template <int DIM, bool W, typename S>
+template <int DIM, bool W, bool VSM, typename S>
 __device__ __forceinline__ void do_event(const FillP &p, const double (&x)[DIM], double w, S &sink,
-                                         Acc<DIM, W> &acc) {
+                                         Acc<DIM, W> &acc, const unsigned char *smem) {
     int g = 0, mul = 1;
     bool inr = true;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
-        const int b = find_bin(p.ax[a], x[a]);          // step (1), per axis
+        const int b = find_bin<VSM>(p.ax[a], x[a], smem);   // step (1), per axis
         inr &= (b >= 1) & (b <= p.ax[a].n);
         g += b * mul;
         if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
@@ -346,16 +420,27 @@ __device__ __forceinline__ double2 ld_stream2(const double *p, int64_t pair) {
     return __ldcs(reinterpret_cast<const double2 *>(p) + pair);
 }
 
-// VEC: columns are read as double2 (LDG.E.128) after `peel` leading events.
-template <int DIM, bool W, int SINK, bool VEC>
-__global__ void __launch_bounds__(kThreads, 2) k_fill(FillP p) {
+template <int DIM, bool W>
+struct Batch {            // U event pairs of every column, held in registers
+    static constexpr int U = 2;
+    double2 x[U][DIM];
+    double2 w[U];
+};
+
+// Shared-memory layout: [sink | variable-axis tables (VSM)]; the tables start at
+// each axis' tab_off.  VEC: columns are read as double2 (LDG.E.128) after `peel`
+// leading events; the next batch is loaded before the current one is processed
+// (register double-buffering) so each thread keeps 2*U*ncol 16-byte loads in flight.
+template <int DIM, bool W, int SINK, bool VEC, bool VSM>
+__global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Sink_t = typename SinkOf<SINK, W>::T;
     Sink_t sink;
     if constexpr (SINK == SINK_GLOBAL) sink.pp = &p;
     if constexpr (SINK == SINK_CACHE) sink.pp = &p;
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots); else sink.init(smem, p.G);
-    if constexpr (SINK != SINK_GLOBAL) __syncthreads();
+    if constexpr (VSM) stage_axes<DIM>(p.ax, smem);
+    if constexpr (SINK != SINK_GLOBAL || VSM) __syncthreads();
 
     Acc<DIM, W> acc;
     acc.zero();
@@ -363,35 +448,42 @@ __global__ void __launch_bounds__(kThreads, 2) k_fill(FillP p) {
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
 
     if constexpr (VEC) {
-        constexpr int U = 2;
+        using B = Batch<DIM, W>;
+        constexpr int U = B::U;
         const int64_t base = p.peel;
         const int64_t npair = (p.n - base) >> 1;
         const double *xs[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) xs[a] = p.x[a] + base;
         const double *ws = W ? p.w + base : nullptr;
-        for (int64_t q0 = tid; q0 < npair; q0 += U * nth) {
-            double2 xv[U][DIM], wv[U];
+        auto load = [&](B &bt, int64_t q0) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t q = q0 + u * nth;
                 if (q < npair) {
 #pragma unroll
-                    for (int a = 0; a < DIM; ++a) xv[u][a] = ld_stream2(xs[a], q);
-                    if (W) wv[u] = ld_stream2(ws, q);
+                    for (int a = 0; a < DIM; ++a) bt.x[u][a] = ld_stream2(xs[a], q);
+                    if (W) bt.w[u] = ld_stream2(ws, q);
                 }
             }
+        };
+        B cur, nxt;
+        int64_t q0 = tid;
+        if (q0 < npair) load(cur, q0);
+        for (; q0 < npair; q0 += U * nth) {
+            if (q0 + U * nth < npair) load(nxt, q0 + U * nth);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t q = q0 + u * nth;
                 if (q < npair) {
                     double x0[DIM], x1[DIM];
 #pragma unroll
-                    for (int a = 0; a < DIM; ++a) { x0[a] = xv[u][a].x; x1[a] = xv[u][a].y; }
-                    do_event<DIM, W>(p, x0, W ? wv[u].x : 1.0, sink, acc);
-                    do_event<DIM, W>(p, x1, W ? wv[u].y : 1.0, sink, acc);
+                    for (int a = 0; a < DIM; ++a) { x0[a] = cur.x[u][a].x; x1[a] = cur.x[u][a].y; }
+                    do_event<DIM, W, VSM>(p, x0, W ? cur.w[u].x : 1.0, sink, acc, smem);
+                    do_event<DIM, W, VSM>(p, x1, W ? cur.w[u].y : 1.0, sink, acc, smem);
                 }
             }
+            cur = nxt;
         }
         // leading peeled events and the odd tail
         const int64_t tail0 = base + 2 * npair;
@@ -401,14 +493,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_fill(FillP p) {
             double x[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) x[a] = p.x[a][i];
-            do_event<DIM, W>(p, x, W ? p.w[i] : 1.0, sink, acc);
+            do_event<DIM, W, VSM>(p, x, W ? p.w[i] : 1.0, sink, acc, smem);
         }
     } else {
         for (int64_t i = tid; i < p.n; i += nth) {
             double x[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) x[a] = __ldcs(p.x[a] + i);
-            do_event<DIM, W>(p, x, W ? __ldcs(p.w + i) : 1.0, sink, acc);
+            do_event<DIM, W, VSM>(p, x, W ? __ldcs(p.w + i) : 1.0, sink, acc, smem);
         }
     }
 
@@ -431,6 +523,11 @@ __global__ void k_build_guide(AxisP a, uint32_t *guide) {
         if (guide_cell(a, a.e[m]) < c) lo = m + 1; else hi = m;
     }
     guide[c] = (uint32_t)(lo - 1);
+}
+
+__global__ void k_edges_f32(const double *e, int n, float *e32) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) e32[i] = __double2float_rn(e[i]);
 }
 
 template <int DIM>

@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -223,6 +224,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         p.peel = c.vec && ph ? 1 : 0;
         if (p.peel > m) p.peel = (int32_t)m;
         p.cache_slots = cache_slots_for(c.weighted);
+
         // launch shape: persistent grid (resident CTAs on every SM), but each block
         // should see enough events to amortize zeroing + flushing its private bins
         const int nt = threads_of(c.strategy);

@@ -60,21 +60,21 @@ struct FillP {
 
 // ------------------------------------------------------------------ FindBin
 // Fixed axis: b = 1 + floor(n*(x-xmin)/(xmax-xmin)), evaluated as
-// the IEEE binary64 expression (n*(x-xmin))/(xmax-xmin) (reading R2).  Fast path:
-// q' = (x-xmin)*inv with inv = RN(n/D).  |q' - q| <= ~4u*q (u = 2^-53), so when the
-// fractional part of q' is farther than 2^-40*max(q',1) from an integer, floor(q')
-// == floor(q) and the division is skipped; otherwise the exact expression runs.
-// All operations are explicit _rn intrinsics: nvcc may not contract or reorder them.
+// the IEEE binary64 expression q = RN(RN(n*RN(x-xmin))/D) (reading R2).  Fast path:
+// q' = RN(RN(x-xmin)*inv) with inv = RN(n/D); |q' - q| <= ~4u*q (u = 2^-53).  If
+// trunc(q'(1-2^-40)) == trunc(q'(1+2^-40)) (both products rounded, so the computed
+// interval still contains q), every value in it -- q included -- truncates to the
+// same integer, and the division is skipped; otherwise (~1e-6 of uniform events)
+// the exact expression runs.  q >= 0, so truncation == floor.  All operations are
+// explicit _rn intrinsics: nvcc may not contract or reorder them.
 __device__ __forceinline__ int find_bin_fixed(const AxisP &a, double x) {
     if (x < a.xmin) return 0;
     if (!(x < a.xmax)) return a.n + 1;   // x == xmax and NaN -> overflow (R5)
     const double d = __dsub_rn(x, a.xmin);
-    double q = __dmul_rn(d, a.inv);
-    const double fl = floor(q);
-    const double fr = __dsub_rn(q, fl);
-    const double tol = 0x1p-40 * fmax(q, 1.0);
-    if (fr < tol || __dsub_rn(1.0, fr) < tol) q = __ddiv_rn(__dmul_rn((double)a.n, d), a.D);
-    return 1 + (int)q;                   // q >= 0: truncation == floor; q <= n
+    const double q = __dmul_rn(d, a.inv);
+    int b = (int)__dmul_rn(q, 1.0 - 0x1p-40);
+    if (b != (int)__dmul_rn(q, 1.0 + 0x1p-40)) b = (int)__ddiv_rn(__dmul_rn((double)a.n, d), a.D);
+    return 1 + b;                        // q <= n: bin n+1 is overflow (R4)
 }
 
 // Guide cell of a coordinate x >= e[0]: monotone non-decreasing in x (RN is
@@ -249,6 +249,36 @@ enum Sink { SINK_PRIV = 0, SINK_GLOBAL = 1, SINK_CACHE = 2 };
 
 // Shared-memory layout of the PRIV sink: unit -> uint32 count[G];
 // weighted -> double sumw[G] then double sumw2[G].
+__device__ __forceinline__ bool cas128_shared(uint32_t addr, unsigned long long cl, unsigned long long ch,
+                                              unsigned long long nl, unsigned long long nh,
+                                              unsigned long long &ol, unsigned long long &oh) {
+    asm volatile(
+        "{\n .reg .b128 c, n, o;\n mov.b128 c, {%2, %3};\n mov.b128 n, {%4, %5};\n"
+        " atom.shared.cas.b128 o, [%6], c, n;\n mov.b128 {%0, %1}, o;\n}"
+        : "=l"(ol), "=l"(oh)
+        : "l"(cl), "l"(ch), "l"(nl), "l"(nh), "r"(addr)
+        : "memory");
+    return ol == cl && oh == ch;
+}
+
+// (sumw, sumw2) += (w, w*w) on one 16-byte shared-memory cell with a single 128-bit
+// CAS (ATOMS.CAS.128): one load + one CAS per event instead of two of each (smem
+// float64 add has no native atomic on sm_100a; nvcc's atomicAdd(double*) is a CAS loop).
+__device__ __forceinline__ void add2_shared(double2 *cell, double w, double w2) {
+    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(cell);
+    double2 cur = *cell;
+    while (true) {
+        unsigned long long ol, oh;
+        const double nx = cur.x + w, ny = cur.y + w2;
+        if (cas128_shared(addr, __double_as_longlong(cur.x), __double_as_longlong(cur.y), __double_as_longlong(nx),
+                          __double_as_longlong(ny), ol, oh))
+            break;
+        cur = make_double2(__longlong_as_double(ol), __longlong_as_double(oh));
+    }
+}
+
+// Shared-memory layout of the PRIV sink: unit -> uint32 count[G];
+// weighted -> double2 (sumw, sumw2)[G].
 template <bool W>
 struct PrivSink {
     unsigned char *sm;
@@ -256,8 +286,8 @@ struct PrivSink {
     __device__ __forceinline__ void init(unsigned char *s, int g) {
         sm = s; G = g;
         if (W) {
-            double *d = reinterpret_cast<double *>(sm);
-            for (int i = threadIdx.x; i < 2 * G; i += blockDim.x) d[i] = 0.0;
+            double2 *d = reinterpret_cast<double2 *>(sm);
+            for (int i = threadIdx.x; i < G; i += blockDim.x) d[i] = make_double2(0.0, 0.0);
         } else {
             uint32_t *c = reinterpret_cast<uint32_t *>(sm);
             for (int i = threadIdx.x; i < G; i += blockDim.x) c[i] = 0u;
@@ -265,9 +295,7 @@ struct PrivSink {
     }
     __device__ __forceinline__ void add(int g, double w) {
         if (W) {
-            double *d = reinterpret_cast<double *>(sm);
-            atomicAdd(d + g, w);
-            atomicAdd(d + G + g, w * w);
+            add2_shared(reinterpret_cast<double2 *>(sm) + g, w, w * w);
         } else {
             atomicAdd(reinterpret_cast<uint32_t *>(sm) + g, 1u);
         }
@@ -275,11 +303,11 @@ struct PrivSink {
     // Merge stage of PAPER.md:162-165: each block adds its local bins to the global ones.
     __device__ __forceinline__ void flush(const FillP &p) {
         if (W) {
-            const double *d = reinterpret_cast<const double *>(sm);
+            const double2 *d = reinterpret_cast<const double2 *>(sm);
             for (int i = threadIdx.x; i < G; i += blockDim.x) {
-                const double a = d[i], b = d[G + i];
-                if (a != 0.0) atomicAdd(p.sumw + i, a);
-                if (b != 0.0) atomicAdd(p.sumw2 + i, b);
+                const double2 v = d[i];
+                if (v.x != 0.0) atomicAdd(p.sumw + i, v.x);
+                if (v.y != 0.0) atomicAdd(p.sumw2 + i, v.y);
             }
         } else {
             const uint32_t *c = reinterpret_cast<const uint32_t *>(sm);
@@ -416,10 +444,6 @@ __device__ __forceinline__ void do_event(const FillP &p, const double (&x)[DIM],
     if (inr) acc.add(x, w);                              // step (3): stats, in-range only (R6)
 }
 
-__device__ __forceinline__ double2 ld_stream2(const double *p, int64_t pair) {
-    return __ldcs(reinterpret_cast<const double2 *>(p) + pair);
-}
-
 template <int DIM, bool W>
 struct Batch {            // U event pairs of every column, held in registers
     static constexpr int U = 2;
@@ -444,38 +468,39 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
 
     Acc<DIM, W> acc;
     acc.zero();
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    // one launch covers <= 2^31 events, so pair and event indices fit in int32
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nth = gridDim.x * blockDim.x;
 
     if constexpr (VEC) {
         using B = Batch<DIM, W>;
         constexpr int U = B::U;
-        const int64_t base = p.peel;
-        const int64_t npair = (p.n - base) >> 1;
-        const double *xs[DIM];
+        const int base = p.peel;
+        const int n = (int)p.n;
+        const int npair = (n - base) >> 1;
+        const double2 *xs[DIM];
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) xs[a] = p.x[a] + base;
-        const double *ws = W ? p.w + base : nullptr;
-        auto load = [&](B &bt, int64_t q0) {
+        for (int a = 0; a < DIM; ++a) xs[a] = reinterpret_cast<const double2 *>(p.x[a] + base);
+        const double2 *ws = W ? reinterpret_cast<const double2 *>(p.w + base) : nullptr;
+        auto load = [&](B &bt, int q0) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int64_t q = q0 + u * nth;
+                const int q = q0 + u * nth;
                 if (q < npair) {
 #pragma unroll
-                    for (int a = 0; a < DIM; ++a) bt.x[u][a] = ld_stream2(xs[a], q);
-                    if (W) bt.w[u] = ld_stream2(ws, q);
+                    for (int a = 0; a < DIM; ++a) bt.x[u][a] = __ldcs(xs[a] + q);
+                    if (W) bt.w[u] = __ldcs(ws + q);
                 }
             }
         };
         B cur, nxt;
-        int64_t q0 = tid;
+        int q0 = tid;
         if (q0 < npair) load(cur, q0);
         for (; q0 < npair; q0 += U * nth) {
             if (q0 + U * nth < npair) load(nxt, q0 + U * nth);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int64_t q = q0 + u * nth;
-                if (q < npair) {
+                if (q0 + u * nth < npair) {
                     double x0[DIM], x1[DIM];
 #pragma unroll
                     for (int a = 0; a < DIM; ++a) { x0[a] = cur.x[u][a].x; x1[a] = cur.x[u][a].y; }
@@ -486,17 +511,17 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
             cur = nxt;
         }
         // leading peeled events and the odd tail
-        const int64_t tail0 = base + 2 * npair;
-        const int64_t nscalar = base + (p.n - tail0);
+        const int tail0 = base + 2 * npair;
+        const int nscalar = base + (n - tail0);
         if (tid < nscalar) {
-            const int64_t i = tid < base ? tid : tail0 + (tid - base);
+            const int i = tid < base ? tid : tail0 + (tid - base);
             double x[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) x[a] = p.x[a][i];
             do_event<DIM, W, VSM>(p, x, W ? p.w[i] : 1.0, sink, acc, smem);
         }
     } else {
-        for (int64_t i = tid; i < p.n; i += nth) {
+        for (int i = tid; i < (int)p.n; i += nth) {
             double x[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) x[a] = __ldcs(p.x[a] + i);

@@ -67,7 +67,9 @@ def workload_desc(wl) -> str:
             "C3": "C3: TH2D 1000x1000 fixed bins, 2e8 uniform events, unit weights",
             "C3W": "C3w: TH2D 1000x1000 fixed bins, 2e8 uniform events, random weights",
             "C4": "C4: TH3D 100^3 with flow, 2e8 Cauchy-peaked events, unit weights",
-            "C4W": "C4w: TH3D 100^3 with flow, 2e8 Cauchy-peaked events, random weights"}.get(wl.name, wl.name)
+            "C4W": "C4w: TH3D 100^3 with flow, 2e8 Cauchy-peaked events, random weights",
+            "C5": "C5: 8 histograms (1D/2D mix) from 7 columns, 1.25e8 events/GPU (1e9 over 8 GPUs), "
+                  "fused one-pass fill"}.get(wl.name, wl.name)
 
 
 def get_workload(name: str):
@@ -76,6 +78,8 @@ def get_workload(name: str):
         wl = bhgen.workload("C1", 1 << 30)
         wl.name = "C1S"
         return wl
+    if name == "C5":             # 1e9 events over 8 GPUs: 1.25e8 per GPU
+        return bhgen.workload("C5", 125_000_000)
     return bhgen.workload(name)
 
 
@@ -132,16 +136,17 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ CPU oracle timing (reference arm / cpu_baseline)
 def time_oracle(wl, sample_events: int, repeats: int = 1):
-    """Time the CPU oracle (as it stands, single thread) on events [0, sample) of the workload."""
+    """Time the CPU oracle (as it stands, single thread) on events [0, sample) of the workload:
+    every histogram of the workload is filled from its columns, one after the other."""
     import oracle
-    hist = wl.hists[0]
-    cols = [wl.column(c, 0, sample_events) for c in hist.cols]
-    w = wl.column(wl.wcol, 0, sample_events) if hist.weighted else None
+    need = sorted({c for h in wl.hists for c in h.cols} | ({wl.wcol} if wl.wcol is not None else set()))
+    cols = {c: wl.column(c, 0, sample_events) for c in need}
     times = []
     for _ in range(repeats):
-        h = oracle.OracleHist(oracle.oracle_axes(hist))
+        hs = [oracle.OracleHist(oracle.oracle_axes(h)) for h in wl.hists]
         t0 = time.perf_counter()
-        h.fill(cols, w)
+        for o, h in zip(hs, wl.hists):
+            o.fill([cols[c] for c in h.cols], cols[wl.wcol] if h.weighted else None)
         times.append(time.perf_counter() - t0)
     return times
 
@@ -190,40 +195,47 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=dev)
 
     wl = get_workload(args.config)
-    hist = wl.hists[0]
     N = wl.n_events
     start = rank * N           # weak scaling: this rank's shard of the seeded stream
-    ncol = len(hist.cols) + (1 if hist.weighted else 0)
+    hists = wl.hists
+    used = sorted({c for h in hists for c in h.cols} | ({wl.wcol} if any(h.weighted for h in hists) else set()))
+    slot = {c: j for j, c in enumerate(used)}
 
     # ---- inputs: generated on the host into pinned memory (also the e2e source), copied to HBM once
-    host = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in range(ncol)]
-    for j, c in enumerate(hist.cols):
-        wl.column_ptr(c, start, N, host[j].data_ptr())
-    if hist.weighted:
-        wl.column_ptr(wl.wcol, start, N, host[-1].data_ptr())
+    host = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in used]
+    for c in used:
+        wl.column_ptr(c, start, N, host[slot[c]].data_ptr())
     devc = [t.to(dev, non_blocking=True) for t in host]
     torch.cuda.synchronize()
-    coords = devc[:len(hist.cols)]
-    w = devc[-1] if hist.weighted else None
 
-    axes = hist.axes_spec()
-    H = pkg.Histogram(axes, device=local, strategy={"auto": 0, "priv": 1, "global": 2, "cache": 3}[args.strategy])
+    strat_code = {"auto": 0, "priv": 1, "global": 2, "cache": 3}[args.strategy]
+    Hs = [pkg.Histogram(h.axes_spec(), device=local, strategy=strat_code) for h in hists]
+    multi = len(Hs) > 1
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
-    packed = torch.empty(pkg.bh_packed_size(H.h), dtype=torch.float64, device=dev)
-    cptrs = [c.data_ptr() for c in coords]
-    wptr = None if w is None else w.data_ptr()
+    packed = [torch.empty(pkg.bh_packed_size(H.h), dtype=torch.float64, device=dev) for H in Hs]
     fill_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
 
+    def do_fill(cols):
+        if multi:
+            pkg.fill_multi(Hs, [[slot[c] for c in h.cols] for h in hists], [h.weighted for h in hists], cols,
+                           cols[slot[wl.wcol]] if wl.wcol is not None else None, stream)
+        else:
+            h = hists[0]
+            pkg.bh_fill(Hs[0].h, N, [cols[slot[c]].data_ptr() for c in h.cols],
+                        cols[slot[wl.wcol]].data_ptr() if h.weighted else None, sh)
+
     def step(i=None):
-        pkg.bh_reset(H.h, sh)
+        for H in Hs:
+            pkg.bh_reset(H.h, sh)
         if i is not None:
             fill_ev[i][0].record(stream)
-        pkg.bh_fill(H.h, N, cptrs, wptr, sh)
+        do_fill(devc)
         if i is not None:
             fill_ev[i][1].record(stream)
         if world > 1:
-            allreduce_state(H, packed)
+            for H, buf in zip(Hs, packed):
+                allreduce_state(H, buf)
 
     for _ in range(args.warmup):
         step()
@@ -232,7 +244,7 @@ def run_gpu(args):
         dist.barrier()
     clk = ClockSampler(local)
     clk.start()
-    l0 = pkg.bh_launch_count(H.h)
+    l0 = [pkg.bh_launch_count(H.h) for H in Hs]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     t0.record(stream)
@@ -241,7 +253,11 @@ def run_gpu(args):
     t1.record(stream)
     torch.cuda.synchronize()
     clk.stop()
-    launches = pkg.bh_launch_count(H.h) - l0
+    dl = [pkg.bh_launch_count(H.h) - a for H, a in zip(Hs, l0)]
+    # a fused multi-histogram launch is counted once per histogram it fills
+    launches = dl[0] if multi else sum(dl)
+    if world > 1:
+        launches += len(Hs) * 2 * args.steps     # pack + unpack kernels per histogram per step
     ms = t0.elapsed_time(t1)
     fill_ms = [a.elapsed_time(b) for a, b in fill_ev]
     if world > 1:
@@ -254,15 +270,20 @@ def run_gpu(args):
 
     # ---- end to end through the public API: pinned host columns -> H2D (in the timed region) -> fill -> D2H read
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    host_c = host[:len(hist.cols)]
-    host_w = host[-1] if hist.weighted else None
 
     def e2e_step():
-        H.reset()
-        H.fill_host(host_c, host_w)
+        for H in Hs:
+            H.reset()
+        if multi:
+            cols = [t.to(dev, non_blocking=True) for t in host]
+            do_fill(cols)
+        else:
+            h = hists[0]
+            Hs[0].fill_host([host[slot[c]] for c in h.cols], host[slot[wl.wcol]] if h.weighted else None)
         if world > 1:
-            allreduce_state(H, packed)
-        return H.read()
+            for H, buf in zip(Hs, packed):
+                allreduce_state(H, buf)
+        return [H.read() for H in Hs]
 
     e2e_step()   # warm-up (staging buffers, copy stream)
     torch.cuda.synchronize()
@@ -279,10 +300,10 @@ def run_gpu(args):
         m = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         e2e_s = float(m.item())
-    assert res["entries"] == N * world, res["entries"]
+    assert all(r["entries"] == N * world for r in res), [r["entries"] for r in res]
     e2e_value = N * world * e2e_steps / e2e_s
-    h2d = 8 * N * ncol
-    d2h = 8 * pkg.bh_packed_size(H.h)
+    h2d = 8 * N * len(used)
+    d2h = 8 * sum(pkg.bh_packed_size(H.h) for H in Hs)
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
@@ -298,20 +319,24 @@ def run_gpu(args):
         fill_avg = float(np.mean(fill_ms))
         achieved = bpe * N / (fill_avg * 1e-3) / 1e9
         traffic = ncu_traffic(wl.name)
-        strat = {0: "auto", 1: "priv", 2: "global", 3: "cache"}[H.strategy(hist.weighted)]
+        names = {0: "auto", 1: "priv", 2: "global", 3: "cache"}
+        strat = "fused multi-histogram (per-histogram smem/global plan)" if multi else \
+            names[Hs[0].strategy(hists[0].weighted)]
         clocks = clk.summary()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (bhgen seeded generator, host-generated)",
-            "config": {"workload": workload_desc(wl), "events_per_gpu": N, "total_bins": H.nbins_total,
-                       "weighted": hist.weighted, "fill_strategy": strat,
+            "config": {"workload": workload_desc(wl), "events_per_gpu": N,
+                       "total_bins": sum(H.nbins_total for H in Hs), "histograms": len(Hs),
+                       "weighted": any(h.weighted for h in hists), "fill_strategy": strat,
                        "l2": f"inputs {bpe * N / 2**30:.1f} GiB/GPU >> 126 MB L2 (no flush needed)",
                        "parallelism": f"dp{world}: events sharded, NCCL all-reduce of packed bins+stats"
                        if world > 1 else "single GPU"},
             "pct_hbm_peak": 100.0 * bpe * value / world / 1e9 / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": f"k_fill ({strat})", "launch_ms": fill_avg,
+                         "traffic": traffic, "kernel": "k_fill_multi" if multi else f"k_fill ({strat})",
+                         "launch_ms": fill_avg,
                          "algorithmic_bytes_per_launch": bpe * N, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps, "pcie_gbs": h2d * world * e2e_steps / e2e_s / 1e9 / world,
@@ -321,7 +346,8 @@ def run_gpu(args):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    H.close()
+    for H in Hs:
+        H.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -332,7 +358,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", help="C1, C1S, C2 (default), C3, C3W, C4, C4W")
+    ap.add_argument("--config", default="C2", help="C1, C1S, C2 (default), C3, C3W, C4, C4W, C5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--strategy", default="auto", choices=["auto", "priv", "global", "cache"])

@@ -111,6 +111,17 @@ bh_status bh_fill(bh_hist *h, int64_t n, const double *const *coords, const doub
  * buffers — the fix of PAPER.md:223); kernels may still be in flight on s. */
 bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s);
 
+/* Fused multi-histogram fill (one pass over the columns; PAPER.md:470 future work,
+ * BASELINE.json config 5).  hs[nh] (1 <= nh <= 8, distinct, same device);
+ * col_of_axis[3*i + a] = index into cols[] of the column feeding axis a of
+ * histogram i (unused entries ignored); weighted[i] != 0 -> histogram i adds w
+ * (then w must be a DEVICE pointer to n weights), else unit weights.  cols:
+ * ncols (1..8) DEVICE pointers to float64 columns of n events.  Each histogram
+ * gets exactly the result of bh_fill with its own columns.  Async on s.  Errors:
+ * BH_EINVAL, BH_EMISMATCH (different devices), BH_ECUDA. */
+bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_axis, const uint8_t *weighted,
+                        int64_t n, const double *const *cols, int32_t ncols, const double *w, bh_stream s);
+
 /* Per-event global bin (parity/debug): out[i] = g(event i), int32, DEVICE pointer. */
 bh_status bh_find_bins(const bh_hist *h, int64_t n, const double *const *coords, int32_t *out, bh_stream s);
 

@@ -22,7 +22,7 @@ BH_DEBUG_SKIP_COPY_WAIT = 1
 
 # every symbol include/bhist.h declares (checked by tests/test_abi.py)
 EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset", "bh_fill", "bh_fill_host",
-            "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
+            "bh_fill_multi", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
             "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_launch_count"]
 
 
@@ -65,6 +65,7 @@ def lib(build_if_stale: bool = False):
             "bh_fill": ([_P, _I64, _P, _P, _P], _I32),
             "bh_fill_host": ([_P, _I64, _P, _P, _P], _I32),
             "bh_find_bins": ([_P, _I64, _P, _P, _P], _I32),
+            "bh_fill_multi": ([_P, _I32, _P, _P, _I64, _P, _I32, _P, _P], _I32),
             "bh_info": ([_P, _P, _P, _P], _I32),
             "bh_packed_size": ([_P, _P], _I32),
             "bh_pack": ([_P, _P, _P], _I32),
@@ -136,6 +137,27 @@ def bh_fill(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
 def bh_fill_host(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
     arr = _ptrs(coord_ptrs)
     _check(lib().bh_fill_host(h, n, ctypes.addressof(arr), w_ptr, stream))
+
+
+def bh_fill_multi(handles, col_of_axis, weighted, n: int, col_ptrs, w_ptr=None, stream=None) -> None:
+    """handles: list of bh_hist handles; col_of_axis: per histogram a list of column indices."""
+    nh = len(handles)
+    hs = (ctypes.c_void_p * nh)(*handles)
+    coa = (ctypes.c_int32 * (3 * nh))()
+    for i, cs in enumerate(col_of_axis):
+        for a, c in enumerate(cs):
+            coa[3 * i + a] = c
+    wt = (ctypes.c_uint8 * nh)(*[1 if x else 0 for x in weighted])
+    cp = (ctypes.c_void_p * len(col_ptrs))(*col_ptrs)
+    _check(lib().bh_fill_multi(ctypes.addressof(hs), nh, ctypes.addressof(coa), ctypes.addressof(wt), n,
+                               ctypes.addressof(cp), len(col_ptrs), w_ptr, stream))
+
+
+def fill_multi(hists, col_of_axis, weighted, cols, w=None, stream=None) -> None:
+    """Histogram-level wrapper: cols are contiguous float64 CUDA tensors of equal length."""
+    n = cols[0].numel()
+    bh_fill_multi([h.h for h in hists], col_of_axis, weighted, n, [c.data_ptr() for c in cols],
+                  None if w is None else w.data_ptr(), _stream_handle(stream))
 
 
 def bh_find_bins(h, n: int, coord_ptrs, out_ptr, stream=None) -> None:

@@ -481,6 +481,95 @@ bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const
     return BH_OK;
 }
 
+bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_axis, const uint8_t *weighted,
+                        int64_t n, const double *const *cols, int32_t ncols, const double *w, bh_stream s) {
+    if (!hs || nh < 1 || nh > kMaxHist) return fail(BH_EINVAL, "need 1..%d histograms", kMaxHist);
+    if (!col_of_axis || !weighted || !cols) return fail(BH_EINVAL, "NULL argument");
+    if (ncols < 1 || ncols > kMaxCols) return fail(BH_EINVAL, "need 1..%d columns", kMaxCols);
+    if (n < 0) return fail(BH_EINVAL, "n < 0");
+    for (int c = 0; c < ncols; ++c)
+        if (!cols[c]) return fail(BH_EINVAL, "cols[%d] is NULL", c);
+    int nstats = 0;
+    for (int i = 0; i < nh; ++i) {
+        if (!hs[i]) return fail(BH_EINVAL, "histogram %d is NULL", i);
+        if (hs[i]->device != hs[0]->device) return fail(BH_EMISMATCH, "histograms live on different devices");
+        for (int j = 0; j < i; ++j)
+            if (hs[j] == hs[i]) return fail(BH_EINVAL, "histogram %d appears twice", i);
+        if (weighted[i] && !w) return fail(BH_EINVAL, "histogram %d is weighted but w is NULL", i);
+        for (int a = 0; a < hs[i]->dim; ++a) {
+            const int c = col_of_axis[3 * i + a];
+            if (c < 0 || c >= ncols) return fail(BH_EINVAL, "histogram %d axis %d: column %d out of range", i, a, c);
+        }
+        nstats += hs[i]->K;
+    }
+    if (n == 0) return BH_OK;
+    bh_hist *h0 = hs[0];
+    DeviceGuard dg(h0->device);
+    MultiP p{};
+    p.nh = nh;
+    p.ncols = ncols;
+    p.nstats = nstats;
+    p.w = w;
+    p.counter = h0->counter;
+    // shared-memory plan: cheapest items first (bins of a histogram, tables of a variable axis)
+    struct Item { size_t bytes; int h, a; };   // a < 0: bins of h; a >= 0: tables of axis a of h
+    std::vector<Item> items;
+    for (int i = 0; i < nh; ++i) {
+        const bh_hist *H = hs[i];
+        items.push_back({align16((weighted[i] ? 16 : 4) * (size_t)H->G), i, -1});
+        for (int a = 0; a < H->dim; ++a)
+            if (H->ax[a].var) items.push_back({axis_table_bytes(H->ax[a]), i, a});
+    }
+    std::sort(items.begin(), items.end(), [](const Item &x, const Item &y) { return x.bytes < y.bytes; });
+    const size_t static_smem = sizeof(double) * (kMultiThreads / 32) * kMultiStats + 64;
+    const size_t budget = h0->smem_optin > static_smem + 2048 ? h0->smem_optin - static_smem - 2048 : 0;
+    size_t used = 0;
+    int stat_off = 0;
+    for (int i = 0; i < nh; ++i) {
+        const bh_hist *H = hs[i];
+        MultiH &M = p.h[i];
+        M.dim = H->dim;
+        M.weighted = weighted[i] ? 1 : 0;
+        for (int a = 0; a < 3; ++a) M.col[a] = a < H->dim ? col_of_axis[3 * i + a] : 0;
+        for (int a = 0; a < H->dim; ++a) { M.ax[a] = H->ax[a]; M.ax[a].tab_off = -1; }
+        M.st1 = H->st1;
+        M.st2 = H->st2;
+        M.G = (int32_t)H->G;
+        M.K = H->K;
+        M.stat_off = stat_off;
+        stat_off += H->K;
+        M.smem_off = -1;
+        M.count = H->count;
+        M.sumw = H->sumw;
+        M.sumw2 = H->sumw2;
+        M.stats = H->stats;
+        M.partials = H->partials;
+        M.entries = H->entries;
+    }
+    for (const Item &it : items) {
+        if (used + it.bytes > budget) continue;
+        if (it.a < 0) p.h[it.h].smem_off = (int32_t)used;
+        else p.h[it.h].ax[it.a].tab_off = (int32_t)used;
+        used += it.bytes;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    auto kern = k_fill_multi;
+    if (used > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)used));
+    const int64_t kMaxLaunch = int64_t(1) << 31;
+    for (int64_t off = 0; off < n; off += kMaxLaunch) {
+        const int64_t m = std::min(kMaxLaunch, n - off);
+        p.n = m;
+        for (int c = 0; c < ncols; ++c) p.cols[c] = cols[c] + off;
+        p.w = w ? w + off : nullptr;
+        int64_t grid = (m + kMultiThreads * 4 - 1) / (kMultiThreads * 4);
+        grid = std::max<int64_t>(1, std::min<int64_t>(grid, h0->nsm));
+        kern<<<(int)grid, kMultiThreads, used, st>>>(p);
+        CUDA_TRY(cudaGetLastError());
+        for (int i = 0; i < nh; ++i) hs[i]->launches++;
+    }
+    return BH_OK;
+}
+
 bh_status bh_find_bins(const bh_hist *h, int64_t n, const double *const *coords, int32_t *out, bh_stream s) {
     if (check_hist(h)) return BH_EINVAL;
     if (n < 0) return fail(BH_EINVAL, "n < 0");

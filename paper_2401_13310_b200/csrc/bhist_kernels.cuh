@@ -537,6 +537,179 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
     block_stats_finish<Acc<DIM, W>::K>(p, acc.s);
 }
 
+// ------------------------------------------------------------------ fused multi-histogram fill (C5)
+// One pass over a set of columns feeding up to kMaxHist histograms (the paper's
+// future work "multiple histograms from different columns in one pass", P:470;
+// RDataFrame runs all actions in one event loop).  Each column byte is read
+// once; each histogram runs the same three steps as k_fill.  Small bin spaces are
+// privatized in shared memory (u32 counts / double2 (sumw, sumw2) with 128-bit CAS),
+// the rest use global atomics.  The statistics (up to 8 x 11 sums) do not fit in
+// registers, so each warp reduces its 32 events' terms with shuffles and lane k
+// keeps the warp's running sum of statistic k (and k+32, k+64).
+constexpr int kMaxHist = 8;
+constexpr int kMaxCols = 8;
+constexpr int kMultiStats = 96;          // >= sum of K over the histograms (<= 8 * 11 = 88)
+constexpr int kMultiThreads = 512;
+
+struct MultiH {
+    int32_t dim;
+    int32_t weighted;
+    int32_t col[kMaxDim];
+    AxisP ax[kMaxDim];
+    int32_t st1, st2;
+    int32_t G, K;
+    int32_t stat_off;                    // first index of this histogram's stats in the flat list
+    int32_t smem_off;                    // >= 0: privatized at this byte offset; -1: global atomics
+    unsigned long long *count;
+    double *sumw, *sumw2, *stats, *partials;
+    unsigned long long *entries;
+};
+
+struct MultiP {
+    int64_t n;
+    int32_t nh, ncols, nstats;
+    const double *cols[kMaxCols];
+    const double *w;
+    unsigned int *counter;               // ticket of histogram 0
+    MultiH h[kMaxHist];
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(kMultiThreads, 1) k_fill_multi(const __grid_constant__ MultiP p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double red[kMultiThreads / 32][kMultiStats];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // zero the privatized bins; stage variable-axis tables that were given smem room
+    for (int hh = 0; hh < p.nh; ++hh) {
+        const MultiH &H = p.h[hh];
+        if (H.smem_off >= 0) {
+            if (H.weighted) {
+                double2 *d = reinterpret_cast<double2 *>(smem + H.smem_off);
+                for (int i = threadIdx.x; i < H.G; i += blockDim.x) d[i] = make_double2(0.0, 0.0);
+            } else {
+                uint32_t *c = reinterpret_cast<uint32_t *>(smem + H.smem_off);
+                for (int i = threadIdx.x; i < H.G; i += blockDim.x) c[i] = 0u;
+            }
+        }
+        for (int a = 0; a < H.dim; ++a)
+            if (H.ax[a].var && H.ax[a].tab_off >= 0) stage_axes<1>(&H.ax[a], smem);
+    }
+    __syncthreads();
+
+    double acc[3] = {0.0, 0.0, 0.0};     // lane k: warp totals of statistics k, k+32, k+64
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = ((p.n + nth - 1) / nth) * nth;     // every lane runs every iteration
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += nth) {
+        const bool valid = i < p.n;
+        double x[kMaxCols];
+#pragma unroll
+        for (int c = 0; c < kMaxCols; ++c)
+            if (c < p.ncols) x[c] = valid ? __ldcs(p.cols[c] + i) : 0.0;
+        const double wv = (valid && p.w) ? __ldcs(p.w + i) : 1.0;
+        for (int hh = 0; hh < p.nh; ++hh) {
+            const MultiH &H = p.h[hh];
+            const double w = H.weighted ? wv : 1.0;
+            double xa[kMaxDim] = {0.0, 0.0, 0.0};
+            int g = 0, mul = 1;
+            bool inr = valid;
+            for (int a = 0; a < H.dim; ++a) {
+                xa[a] = x[H.col[a]];
+                const AxisP &A = H.ax[a];
+                int b;
+                if (!A.var) b = find_bin_fixed(A, xa[a]);
+                else if (A.tab_off >= 0)
+                    b = A.g16 ? find_bin_var_smem<true>(A, xa[a], smem + A.tab_off)
+                              : find_bin_var_smem<false>(A, xa[a], smem + A.tab_off);
+                else b = find_bin_var_global(A, xa[a]);
+                inr &= (b >= 1) & (b <= A.n);
+                g += b * mul;
+                mul = (a == 0) ? H.st1 : H.st2;
+            }
+            if (valid) {                                    // step (2)
+                if (H.smem_off >= 0) {
+                    if (H.weighted) add2_shared(reinterpret_cast<double2 *>(smem + H.smem_off) + g, w, w * w);
+                    else atomicAdd(reinterpret_cast<uint32_t *>(smem + H.smem_off) + g, 1u);
+                } else if (H.weighted) {
+                    atomicAdd(H.sumw + g, w);
+                    atomicAdd(H.sumw2 + g, w * w);
+                } else {
+                    atomicAdd(H.count + g, 1ull);
+                }
+            }
+            // step (3): terms of this event (zero when out of range), reduced over the warp
+            const double ww = inr ? w : 0.0;
+            const double wx = ww * xa[0], wy = ww * xa[1], wz = ww * xa[2];
+            double t[11];
+            t[0] = ww; t[1] = ww * ww; t[2] = wx; t[3] = wx * xa[0];
+            t[4] = wy; t[5] = wy * xa[1]; t[6] = wx * xa[1];
+            t[7] = wz; t[8] = wz * xa[2]; t[9] = wx * xa[2]; t[10] = wy * xa[2];
+#pragma unroll
+            for (int k = 0; k < 11; ++k) {
+                if (k < H.K) {
+                    const double v = warp_sum(t[k]);
+                    const int j = H.stat_off + k;
+                    if ((j & 31) == lane) acc[j >> 5] += v;
+                }
+            }
+        }
+    }
+
+    // merge stage: privatized bins -> global
+    __syncthreads();
+    for (int hh = 0; hh < p.nh; ++hh) {
+        const MultiH &H = p.h[hh];
+        if (H.smem_off < 0) continue;
+        if (H.weighted) {
+            const double2 *d = reinterpret_cast<const double2 *>(smem + H.smem_off);
+            for (int i = threadIdx.x; i < H.G; i += blockDim.x) {
+                const double2 v = d[i];
+                if (v.x != 0.0) atomicAdd(H.sumw + i, v.x);
+                if (v.y != 0.0) atomicAdd(H.sumw2 + i, v.y);
+            }
+        } else {
+            const uint32_t *c = reinterpret_cast<const uint32_t *>(smem + H.smem_off);
+            for (int i = threadIdx.x; i < H.G; i += blockDim.x)
+                if (c[i]) atomicAdd(H.count + i, (unsigned long long)c[i]);
+        }
+    }
+    // stats: warp totals -> block partials (per histogram) -> last CTA, fixed order
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+        if (r * 32 + lane < kMultiStats) red[warp][r * 32 + lane] = acc[r];
+    __syncthreads();
+    if (threadIdx.x < p.nstats) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i][threadIdx.x];
+        int hh = 0;
+        while (hh + 1 < p.nh && p.h[hh + 1].stat_off <= (int)threadIdx.x) ++hh;
+        const MultiH &H = p.h[hh];
+        H.partials[(size_t)blockIdx.x * H.K + (threadIdx.x - H.stat_off)] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(p.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x < p.nstats) {
+        int hh = 0;
+        while (hh + 1 < p.nh && p.h[hh + 1].stat_off <= (int)threadIdx.x) ++hh;
+        const MultiH &H = p.h[hh];
+        const int k = threadIdx.x - H.stat_off;
+        double t = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(H.partials + (size_t)b * H.K + k);
+        H.stats[k] += t;
+    }
+    if (threadIdx.x < p.nh) *p.h[threadIdx.x].entries += (unsigned long long)p.n;
+    if (threadIdx.x == 0) *p.counter = 0u;
+}
+
 // ------------------------------------------------------------------ auxiliary kernels
 // guide[c] = #{interior i in [1, n-1] : cell(e_i) < c}, c = 0..gcells (cell is monotone in i).
 __global__ void k_build_guide(AxisP a, uint32_t *guide) {

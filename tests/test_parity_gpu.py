@@ -291,3 +291,51 @@ def test_full_size_against_sharded_oracle(name):
     wl, got = _gpu_full(name)
     ref = oracle_parallel(name, wl.n_events)
     compare(got, ref, wl.hists[0].weighted, f"full {name}")
+
+
+# ------------------------------------------------------------------ fused multi-histogram fill (C5)
+@pytest.mark.parametrize("n", [1_000_003, 7])
+def test_fill_multi_c5(n):
+    wl = bhgen.workload("C5", n)
+    cols = [wl.column(c, 0, n) for c in range(len(wl.columns))]
+    w = cols[wl.wcol]
+    tcols = [_t(c) for c in cols]
+    hs = [pkg.Histogram(oracle.oracle_axes(h)) for h in wl.hists]
+    for rep in range(2):   # accumulates across calls
+        pkg.fill_multi(hs, [h.cols for h in wl.hists], [h.weighted for h in wl.hists], tcols, tcols[wl.wcol])
+    for i, hist in enumerate(wl.hists):
+        ref = oracle.OracleHist(oracle.oracle_axes(hist))
+        for rep in range(2):
+            ref.fill([cols[c] for c in hist.cols], w if hist.weighted else None)
+        compare(hs[i].read(), ref.read(), hist.weighted, f"C5 H{i}")
+        hs[i].close()
+
+
+def test_fill_multi_matches_single_fills():
+    wl = bhgen.workload("C5", 300_001)
+    cols = [_t(wl.column(c, 0, wl.n_events)) for c in range(len(wl.columns))]
+    multi = [pkg.Histogram(oracle.oracle_axes(h)) for h in wl.hists]
+    pkg.fill_multi(multi, [h.cols for h in wl.hists], [h.weighted for h in wl.hists], cols, cols[wl.wcol])
+    for i, hist in enumerate(wl.hists):
+        single = pkg.Histogram(oracle.oracle_axes(hist))
+        single.fill([cols[c] for c in hist.cols], cols[wl.wcol] if hist.weighted else None)
+        a, b = multi[i].read(), single.read()
+        assert a["entries"] == b["entries"]
+        if not hist.weighted:
+            assert np.array_equal(a["content"], b["content"])
+        else:
+            np.testing.assert_allclose(a["content"], b["content"], rtol=1e-12, atol=0)
+        single.close()
+        multi[i].close()
+
+
+def test_fill_multi_rejects_bad_arguments():
+    h = pkg.Histogram([(10, 0.0, 1.0)])
+    x = _t(np.zeros(10))
+    with pytest.raises(pkg.BHistError):
+        pkg.bh_fill_multi([h.h], [[3]], [False], 10, [x.data_ptr()])        # column out of range
+    with pytest.raises(pkg.BHistError):
+        pkg.bh_fill_multi([h.h], [[0]], [True], 10, [x.data_ptr()], None)   # weighted without w
+    with pytest.raises(pkg.BHistError):
+        pkg.bh_fill_multi([h.h, h.h], [[0], [0]], [False, False], 10, [x.data_ptr()])   # duplicate
+    h.close()

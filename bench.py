@@ -254,8 +254,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     clk.stop()
     dl = [pkg.bh_launch_count(H.h) - a for H, a in zip(Hs, l0)]
-    # a fused multi-histogram launch is counted once per histogram it fills
-    launches = dl[0] if multi else sum(dl)
+    launches = sum(dl)        # the library counts each kernel launch once (fused passes on their first histogram)
     if world > 1:
         launches += len(Hs) * 2 * args.steps     # pack + unpack kernels per histogram per step
     ms = t0.elapsed_time(t1)

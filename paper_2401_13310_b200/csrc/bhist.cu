@@ -503,69 +503,108 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
         nstats += hs[i]->K;
     }
     if (n == 0) return BH_OK;
-    bh_hist *h0 = hs[0];
-    DeviceGuard dg(h0->device);
-    MultiP p{};
-    p.nh = nh;
-    p.ncols = ncols;
-    p.nstats = nstats;
-    p.w = w;
-    p.counter = h0->counter;
-    // shared-memory plan: cheapest items first (bins of a histogram, tables of a variable axis)
-    struct Item { size_t bytes; int h, a; };   // a < 0: bins of h; a >= 0: tables of axis a of h
-    std::vector<Item> items;
-    for (int i = 0; i < nh; ++i) {
-        const bh_hist *H = hs[i];
-        items.push_back({align16((weighted[i] ? 16 : 4) * (size_t)H->G), i, -1});
-        for (int a = 0; a < H->dim; ++a)
-            if (H->ax[a].var) items.push_back({axis_table_bytes(H->ax[a]), i, a});
-    }
-    std::sort(items.begin(), items.end(), [](const Item &x, const Item &y) { return x.bytes < y.bytes; });
-    const size_t static_smem = sizeof(double) * (kMultiThreads / 32) * kMultiStats + 64;
-    const size_t budget = h0->smem_optin > static_smem + 2048 ? h0->smem_optin - static_smem - 2048 : 0;
-    size_t used = 0;
-    int stat_off = 0;
-    for (int i = 0; i < nh; ++i) {
-        const bh_hist *H = hs[i];
-        MultiH &M = p.h[i];
-        M.dim = H->dim;
-        M.weighted = weighted[i] ? 1 : 0;
-        for (int a = 0; a < 3; ++a) M.col[a] = a < H->dim ? col_of_axis[3 * i + a] : 0;
-        for (int a = 0; a < H->dim; ++a) { M.ax[a] = H->ax[a]; M.ax[a].tab_off = -1; }
-        M.st1 = H->st1;
-        M.st2 = H->st2;
-        M.G = (int32_t)H->G;
-        M.K = H->K;
-        M.stat_off = stat_off;
-        stat_off += H->K;
-        M.smem_off = -1;
-        M.count = H->count;
-        M.sumw = H->sumw;
-        M.sumw2 = H->sumw2;
-        M.stats = H->stats;
-        M.partials = H->partials;
-        M.entries = H->entries;
-    }
-    for (const Item &it : items) {
-        if (used + it.bytes > budget) continue;
-        if (it.a < 0) p.h[it.h].smem_off = (int32_t)used;
-        else p.h[it.h].ax[it.a].tab_off = (int32_t)used;
-        used += it.bytes;
-    }
+    DeviceGuard dg(hs[0]->device);
     cudaStream_t st = static_cast<cudaStream_t>(s);
-    auto kern = k_fill_multi;
-    if (used > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)used));
-    const int64_t kMaxLaunch = int64_t(1) << 31;
-    for (int64_t off = 0; off < n; off += kMaxLaunch) {
-        const int64_t m = std::min(kMaxLaunch, n - off);
-        p.n = m;
-        for (int c = 0; c < ncols; ++c) p.cols[c] = cols[c] + off;
-        p.w = w ? w + off : nullptr;
-        int64_t grid = (m + kMultiThreads * 4 - 1) / (kMultiThreads * 4);
-        grid = std::max<int64_t>(1, std::min<int64_t>(grid, h0->nsm));
-        kern<<<(int)grid, kMultiThreads, used, st>>>(p);
-        CUDA_TRY(cudaGetLastError());
-        for (int i = 0; i < nh; ++i) hs[i]->launches++;
+    // ---- plan: histograms with a large private state get a pass of their own (k_fill,
+    // AUTO strategy); the small ones are packed into fused passes (k_fill_multi) whose
+    // privatized bins + search tables + per-thread stats fit in shared memory.
+    const size_t kFuseLimit = 64 * 1024;
+    const size_t budget = hs[0]->smem_optin - kStaticSmemReserve;
+    struct Cand { int i; size_t bytes; };
+    std::vector<int> solo;
+    std::vector<Cand> small;
+    for (int i = 0; i < nh; ++i) {
+        const bh_hist *H = hs[i];
+        size_t b = align16((weighted[i] ? 16 : 4) * (size_t)H->G);
+        for (int a = 0; a < H->dim; ++a) b += axis_table_bytes(H->ax[a]);
+        if (b > kFuseLimit) solo.push_back(i); else small.push_back({i, b});
+    }
+    std::sort(small.begin(), small.end(), [](const Cand &x, const Cand &y) { return x.bytes < y.bytes; });
+    std::vector<std::vector<int>> fused;
+    {
+        std::vector<int> cur;
+        size_t used = 0;
+        int stats = 0;
+        for (const Cand &c : small) {
+            const int k = hs[c.i]->K;
+            if (!cur.empty() && used + c.bytes + (size_t)(stats + k) * kMultiThreads * 8 > budget) {
+                fused.push_back(cur);
+                cur.clear();
+                used = 0;
+                stats = 0;
+            }
+            cur.push_back(c.i);
+            used += c.bytes;
+            stats += k;
+        }
+        if (!cur.empty()) fused.push_back(cur);
+    }
+    for (auto it = fused.begin(); it != fused.end();) {
+        if (it->size() == 1) { solo.push_back((*it)[0]); it = fused.erase(it); } else ++it;
+    }
+    // ---- solo passes: the single-histogram kernel on this histogram's own columns
+    for (int i : solo) {
+        const double *cs[kMaxDim] = {};
+        for (int a = 0; a < hs[i]->dim; ++a) cs[a] = cols[col_of_axis[3 * i + a]];
+        bh_status r = fill_device(hs[i], n, cs, weighted[i] ? w : nullptr, st);
+        if (r != BH_OK) return r;
+    }
+    // ---- fused passes
+    for (const std::vector<int> &pass : fused) {
+        MultiP p{};
+        p.nh = (int32_t)pass.size();
+        p.ncols = ncols;
+        p.counter = hs[pass[0]]->counter;
+        size_t used = 0;
+        int stat_off = 0;
+        for (int j = 0; j < p.nh; ++j) {
+            const int i = pass[j];
+            const bh_hist *H = hs[i];
+            MultiH &M = p.h[j];
+            M.dim = H->dim;
+            M.weighted = weighted[i] ? 1 : 0;
+            for (int a = 0; a < 3; ++a) M.col[a] = a < H->dim ? col_of_axis[3 * i + a] : 0;
+            M.st1 = H->st1;
+            M.st2 = H->st2;
+            M.G = (int32_t)H->G;
+            M.K = H->K;
+            M.stat_off = stat_off;
+            stat_off += H->K;
+            M.smem_off = (int32_t)used;
+            used += align16((weighted[i] ? 16 : 4) * (size_t)H->G);
+            for (int a = 0; a < H->dim; ++a) {
+                M.ax[a] = H->ax[a];
+                M.ax[a].tab_off = -1;
+                if (M.ax[a].var) {
+                    M.ax[a].tab_off = (int32_t)used;
+                    used += axis_table_bytes(M.ax[a]);
+                }
+            }
+            M.count = H->count;
+            M.sumw = H->sumw;
+            M.sumw2 = H->sumw2;
+            M.stats = H->stats;
+            M.partials = H->partials;
+            M.entries = H->entries;
+        }
+        p.nstats = stat_off;
+        p.acc_off = (int32_t)used;
+        used += (size_t)stat_off * kMultiThreads * sizeof(double);
+        if (used > budget) return fail(BH_EINVAL, "fused pass needs %zu B of shared memory", used);
+        auto kern = k_fill_multi;
+        if (used > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)used));
+        const int64_t kMaxLaunch = int64_t(1) << 31;
+        for (int64_t off = 0; off < n; off += kMaxLaunch) {
+            const int64_t m = std::min(kMaxLaunch, n - off);
+            p.n = m;
+            for (int c = 0; c < ncols; ++c) p.cols[c] = cols[c] + off;
+            p.w = w ? w + off : nullptr;
+            int64_t grid = (m + kMultiThreads * 4 - 1) / (kMultiThreads * 4);
+            grid = std::max<int64_t>(1, std::min<int64_t>(grid, hs[0]->nsm));
+            kern<<<(int)grid, kMultiThreads, used, st>>>(p);
+            CUDA_TRY(cudaGetLastError());
+            hs[pass[0]]->launches++;      // one launch, counted once
+        }
     }
     return BH_OK;
 }

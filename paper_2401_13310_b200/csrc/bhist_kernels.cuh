@@ -205,6 +205,12 @@ struct Acc {
     }
 };
 
+__device__ __forceinline__ double warp_sum_fixed(double v) {   // butterfly: same order on every run
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 // Block reduction of the K sums -> partials[blockIdx.x]; the last CTA to arrive
 // sums the partials in block order and adds them to the running stats
 // (include-initial) and adds the event count to entries.
@@ -538,14 +544,16 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
 }
 
 // ------------------------------------------------------------------ fused multi-histogram fill (C5)
-// One pass over a set of columns feeding up to kMaxHist histograms (the paper's
-// future work "multiple histograms from different columns in one pass", P:470;
-// RDataFrame runs all actions in one event loop).  Each column byte is read
-// once; each histogram runs the same three steps as k_fill.  Small bin spaces are
-// privatized in shared memory (u32 counts / double2 (sumw, sumw2) with 128-bit CAS),
-// the rest use global atomics.  The statistics (up to 8 x 11 sums) do not fit in
-// registers, so each warp reduces its 32 events' terms with shuffles and lane k
-// keeps the warp's running sum of statistic k (and k+32, k+64).
+// One pass over a set of columns feeding several histograms (the paper's future
+// work "multiple histograms from different columns in one pass"; RDataFrame
+// runs all actions of a dataframe in one event loop).  Each column byte is
+// read once per pass; each histogram runs the same three steps as k_fill.  The host
+// planner (bh_fill_multi) puts histograms whose private state is large in passes of
+// their own (k_fill) and fuses the small ones here: all their bins are privatized in
+// shared memory (u32 counts / double2 (sumw, sumw2) with 128-bit CAS), equal bins
+// are aggregated across the warp first (hot bins, e.g. a Cauchy-peaked column), and
+// each thread keeps its statistics in a private shared-memory column
+// (acc[stat][thread], conflict-free), since up to 8 x 11 sums do not fit in registers.
 constexpr int kMaxHist = 8;
 constexpr int kMaxCols = 8;
 constexpr int kMultiStats = 96;          // >= sum of K over the histograms (<= 8 * 11 = 88)
@@ -559,7 +567,7 @@ struct MultiH {
     int32_t st1, st2;
     int32_t G, K;
     int32_t stat_off;                    // first index of this histogram's stats in the flat list
-    int32_t smem_off;                    // >= 0: privatized at this byte offset; -1: global atomics
+    int32_t smem_off;                    // byte offset of the privatized bins
     unsigned long long *count;
     double *sumw, *sumw2, *stats, *partials;
     unsigned long long *entries;
@@ -568,58 +576,79 @@ struct MultiH {
 struct MultiP {
     int64_t n;
     int32_t nh, ncols, nstats;
+    int32_t acc_off;                     // byte offset of acc[nstats][blockDim.x]
     const double *cols[kMaxCols];
     const double *w;
     unsigned int *counter;               // ticket of histogram 0
     MultiH h[kMaxHist];
 };
 
-__device__ __forceinline__ double warp_sum(double v) {
+__device__ __forceinline__ double pick(const double (&x)[kMaxCols], int c) {
+    double v = x[0];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int k = 1; k < kMaxCols; ++k) v = (c == k) ? x[k] : v;   // selects, no local memory
     return v;
+}
+
+// Bin add for one event of histogram H with warp aggregation: lanes with equal bins
+// elect a leader that adds the group's count (popc) or (sum w, sum w*w) once.
+__device__ __forceinline__ void multi_add(const MultiH &H, unsigned char *smem, bool valid, int g, double w) {
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const unsigned peers = __match_any_sync(act, g);
+    const int lane = (int)(threadIdx.x & 31);
+    const int leader = __ffs(peers) - 1;
+    if (H.weighted) {
+        const int rounds = __reduce_max_sync(act, (unsigned)__popc(peers));
+        double s1 = 0.0, s2 = 0.0;
+        unsigned m = peers;
+        for (int k = 0; k < rounds; ++k) {
+            const int src = m ? __ffs(m) - 1 : lane;
+            const double v = __shfl_sync(act, w, src);
+            if (m) { s1 += v; s2 = fma(v, v, s2); m &= m - 1; }
+        }
+        if (lane == leader) add2_shared(reinterpret_cast<double2 *>(smem + H.smem_off) + g, s1, s2);
+    } else if (lane == leader) {
+        atomicAdd(reinterpret_cast<uint32_t *>(smem + H.smem_off) + g, (uint32_t)__popc(peers));
+    }
 }
 
 __global__ void __launch_bounds__(kMultiThreads, 1) k_fill_multi(const __grid_constant__ MultiP p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ double red[kMultiThreads / 32][kMultiStats];
     __shared__ bool last;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // zero the privatized bins; stage variable-axis tables that were given smem room
+    double *acc = reinterpret_cast<double *>(smem + p.acc_off);     // acc[k * blockDim.x + tid]
+    const int T = blockDim.x;
     for (int hh = 0; hh < p.nh; ++hh) {
         const MultiH &H = p.h[hh];
-        if (H.smem_off >= 0) {
-            if (H.weighted) {
-                double2 *d = reinterpret_cast<double2 *>(smem + H.smem_off);
-                for (int i = threadIdx.x; i < H.G; i += blockDim.x) d[i] = make_double2(0.0, 0.0);
-            } else {
-                uint32_t *c = reinterpret_cast<uint32_t *>(smem + H.smem_off);
-                for (int i = threadIdx.x; i < H.G; i += blockDim.x) c[i] = 0u;
-            }
+        if (H.weighted) {
+            double2 *d = reinterpret_cast<double2 *>(smem + H.smem_off);
+            for (int i = threadIdx.x; i < H.G; i += T) d[i] = make_double2(0.0, 0.0);
+        } else {
+            uint32_t *c = reinterpret_cast<uint32_t *>(smem + H.smem_off);
+            for (int i = threadIdx.x; i < H.G; i += T) c[i] = 0u;
         }
         for (int a = 0; a < H.dim; ++a)
             if (H.ax[a].var && H.ax[a].tab_off >= 0) stage_axes<1>(&H.ax[a], smem);
     }
+    for (int k = 0; k < p.nstats; ++k) acc[k * T + threadIdx.x] = 0.0;
     __syncthreads();
 
-    double acc[3] = {0.0, 0.0, 0.0};     // lane k: warp totals of statistics k, k+32, k+64
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nth = (int64_t)gridDim.x * T;
     const int64_t n_round = ((p.n + nth - 1) / nth) * nth;     // every lane runs every iteration
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += nth) {
+    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n_round; i += nth) {
         const bool valid = i < p.n;
         double x[kMaxCols];
 #pragma unroll
-        for (int c = 0; c < kMaxCols; ++c)
-            if (c < p.ncols) x[c] = valid ? __ldcs(p.cols[c] + i) : 0.0;
+        for (int c = 0; c < kMaxCols; ++c) x[c] = (c < p.ncols && valid) ? __ldcs(p.cols[c] + i) : 0.0;
         const double wv = (valid && p.w) ? __ldcs(p.w + i) : 1.0;
         for (int hh = 0; hh < p.nh; ++hh) {
             const MultiH &H = p.h[hh];
             const double w = H.weighted ? wv : 1.0;
             double xa[kMaxDim] = {0.0, 0.0, 0.0};
             int g = 0, mul = 1;
-            bool inr = valid;
+            bool inr = true;
             for (int a = 0; a < H.dim; ++a) {
-                xa[a] = x[H.col[a]];
+                xa[a] = pick(x, H.col[a]);
                 const AxisP &A = H.ax[a];
                 int b;
                 if (!A.var) b = find_bin_fixed(A, xa[a]);
@@ -631,30 +660,26 @@ __global__ void __launch_bounds__(kMultiThreads, 1) k_fill_multi(const __grid_co
                 g += b * mul;
                 mul = (a == 0) ? H.st1 : H.st2;
             }
-            if (valid) {                                    // step (2)
-                if (H.smem_off >= 0) {
-                    if (H.weighted) add2_shared(reinterpret_cast<double2 *>(smem + H.smem_off) + g, w, w * w);
-                    else atomicAdd(reinterpret_cast<uint32_t *>(smem + H.smem_off) + g, 1u);
-                } else if (H.weighted) {
-                    atomicAdd(H.sumw + g, w);
-                    atomicAdd(H.sumw2 + g, w * w);
-                } else {
-                    atomicAdd(H.count + g, 1ull);
-                }
-            }
-            // step (3): terms of this event (zero when out of range), reduced over the warp
-            const double ww = inr ? w : 0.0;
-            const double wx = ww * xa[0], wy = ww * xa[1], wz = ww * xa[2];
-            double t[11];
-            t[0] = ww; t[1] = ww * ww; t[2] = wx; t[3] = wx * xa[0];
-            t[4] = wy; t[5] = wy * xa[1]; t[6] = wx * xa[1];
-            t[7] = wz; t[8] = wz * xa[2]; t[9] = wx * xa[2]; t[10] = wy * xa[2];
-#pragma unroll
-            for (int k = 0; k < 11; ++k) {
-                if (k < H.K) {
-                    const double v = warp_sum(t[k]);
-                    const int j = H.stat_off + k;
-                    if ((j & 31) == lane) acc[j >> 5] += v;
+            multi_add(H, smem, valid, g, w);                 // step (2)
+            if (valid && inr) {                              // step (3)
+                double *ac = acc + (size_t)H.stat_off * T + threadIdx.x;
+                const double wx = w * xa[0];
+                ac[0] += w;
+                ac[T] = fma(w, w, ac[T]);
+                ac[2 * T] += wx;
+                ac[3 * T] = fma(wx, xa[0], ac[3 * T]);
+                if (H.dim >= 2) {
+                    const double wy = w * xa[1];
+                    ac[4 * T] += wy;
+                    ac[5 * T] = fma(wy, xa[1], ac[5 * T]);
+                    ac[6 * T] = fma(wx, xa[1], ac[6 * T]);
+                    if (H.dim == 3) {
+                        const double wz = w * xa[2];
+                        ac[7 * T] += wz;
+                        ac[8 * T] = fma(wz, xa[2], ac[8 * T]);
+                        ac[9 * T] = fma(wx, xa[2], ac[9 * T]);
+                        ac[10 * T] = fma(wy, xa[2], ac[10 * T]);
+                    }
                 }
             }
         }
@@ -664,32 +689,31 @@ __global__ void __launch_bounds__(kMultiThreads, 1) k_fill_multi(const __grid_co
     __syncthreads();
     for (int hh = 0; hh < p.nh; ++hh) {
         const MultiH &H = p.h[hh];
-        if (H.smem_off < 0) continue;
         if (H.weighted) {
             const double2 *d = reinterpret_cast<const double2 *>(smem + H.smem_off);
-            for (int i = threadIdx.x; i < H.G; i += blockDim.x) {
+            for (int i = threadIdx.x; i < H.G; i += T) {
                 const double2 v = d[i];
                 if (v.x != 0.0) atomicAdd(H.sumw + i, v.x);
                 if (v.y != 0.0) atomicAdd(H.sumw2 + i, v.y);
             }
         } else {
             const uint32_t *c = reinterpret_cast<const uint32_t *>(smem + H.smem_off);
-            for (int i = threadIdx.x; i < H.G; i += blockDim.x)
+            for (int i = threadIdx.x; i < H.G; i += T)
                 if (c[i]) atomicAdd(H.count + i, (unsigned long long)c[i]);
         }
     }
-    // stats: warp totals -> block partials (per histogram) -> last CTA, fixed order
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-        if (r * 32 + lane < kMultiStats) red[warp][r * 32 + lane] = acc[r];
-    __syncthreads();
-    if (threadIdx.x < p.nstats) {
+    // stats: per-thread columns -> block partials (fixed order) -> last CTA, fixed order
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = T >> 5;
+    for (int k = warp; k < p.nstats; k += nw) {
         double t = 0.0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i][threadIdx.x];
-        int hh = 0;
-        while (hh + 1 < p.nh && p.h[hh + 1].stat_off <= (int)threadIdx.x) ++hh;
-        const MultiH &H = p.h[hh];
-        H.partials[(size_t)blockIdx.x * H.K + (threadIdx.x - H.stat_off)] = t;
+        for (int j = lane; j < T; j += 32) t += acc[k * T + j];
+        t = warp_sum_fixed(t);
+        if (lane == 0) {
+            int hh = 0;
+            while (hh + 1 < p.nh && p.h[hh + 1].stat_off <= k) ++hh;
+            const MultiH &H = p.h[hh];
+            H.partials[(size_t)blockIdx.x * H.K + (k - H.stat_off)] = t;
+        }
     }
     __threadfence();
     __syncthreads();

@@ -6,7 +6,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SO = os.path.join(HERE, "libbhist.so")
+SO = os.environ.get("BHIST_LIBRARY") or os.path.join(HERE, "libbhist.so")   # override: A/B experiments
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("bhist.cu", "bhist_kernels.cuh")]
 HEADER = os.path.join(ROOT, "include", "bhist.h")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -22,9 +22,10 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in SOURCES + [HEADER])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=()) -> str:
     if force or stale():
-        cmd = [NVCC, *NVCC_FLAGS, "-o", SO + ".tmp", os.path.join(HERE, "csrc", "bhist.cu")]
+        cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", SO + ".tmp",
+               os.path.join(HERE, "csrc", "bhist.cu")]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

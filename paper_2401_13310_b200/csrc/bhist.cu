@@ -92,11 +92,16 @@ struct bh_hist {
 
 namespace {
 
+size_t align16(size_t b);
+size_t axis_table_bytes(const AxisP &a);
+constexpr size_t kStaticSmemReserve = 4096;   // block_stats_finish scratch + driver reserve
+
+// AUTO: privatize the bins in shared memory whenever they fit next to the reserve
+// (variable-axis tables then go to smem only if they also fit); otherwise CACHE.
 int resolve_strategy(const bh_hist *h, bool weighted) {
     if (h->strategy != BH_STRATEGY_AUTO) return h->strategy;
-    const size_t budget = 160 * 1024;
-    const size_t priv = weighted ? 16 * (size_t)h->G : 4 * (size_t)h->G;
-    if (priv <= budget) return BH_STRATEGY_PRIV;
+    const size_t priv = (weighted ? 16 : 4) * (size_t)h->G;
+    if (priv + kStaticSmemReserve <= h->smem_optin) return BH_STRATEGY_PRIV;
     // large bin spaces: shared-memory cache of the hottest bins in front of L2 atomics
     // (as fast as plain GLOBAL on uniform data, 30x faster on the peaked C4 shape)
     return BH_STRATEGY_CACHE;
@@ -121,7 +126,6 @@ size_t axis_table_bytes(const AxisP &a) {
     return align16(4 * (size_t)(a.n + 1)) + align16((a.g16 ? 2 : 4) * (size_t)(a.gcells + 1));
 }
 
-constexpr size_t kStaticSmemReserve = 4096;   // block_stats_finish scratch + driver reserve
 
 FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, const double *w) {
     FillP p{};
@@ -157,7 +161,7 @@ cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
         if (e != cudaSuccess) return e;
     }
-    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
+    kern<<<c.grid, ThreadsOf<SINK, W>::v, c.smem, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -174,7 +178,11 @@ cudaError_t launch_v(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
 template <int DIM, bool W>
 cudaError_t launch_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
     switch (c.strategy) {
-    case BH_STRATEGY_PRIV: return launch_v<DIM, W, SINK_PRIV>(p, c, s);
+    case BH_STRATEGY_PRIV:
+        if constexpr (W) {
+            if (p.replicas > 1) return launch_v<DIM, W, SINK_PRIVA>(p, c, s);
+        }
+        return launch_v<DIM, W, SINK_PRIV>(p, c, s);
     case BH_STRATEGY_CACHE: return launch_v<DIM, W, SINK_CACHE>(p, c, s);
     default: return launch_v<DIM, W, SINK_GLOBAL>(p, c, s);
     }
@@ -185,7 +193,7 @@ cudaError_t launch_d(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
     return c.weighted ? launch_s<DIM, true>(p, c, s) : launch_s<DIM, false>(p, c, s);
 }
 
-int threads_of(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? kThreadsGlobal : kThreadsSmem; }
+int threads_of(int strategy, bool) { return strategy == BH_STRATEGY_GLOBAL ? kThreadsGlobal : kThreadsSmem; }
 int resident_blocks(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? 2 : 1; }
 
 // One fill over device-resident columns, split into launches of <= 2^31 events.
@@ -193,7 +201,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
     LaunchCfg c{};
     c.weighted = w != nullptr;
     c.strategy = resolve_strategy(h, c.weighted);
-    const size_t sink = sink_bytes(h, c.strategy, c.weighted);
+    size_t sink = sink_bytes(h, c.strategy, c.weighted);
     // variable-axis tables go to shared memory behind the sink when they fit
     size_t tabs = 0;
     AxisP ax[kMaxDim];
@@ -205,6 +213,20 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         }
     }
     c.vsm = tabs > 0 && sink + tabs + kStaticSmemReserve <= h->smem_optin;
+    // PRIV: replicate the private bins into the spare shared memory (up to one copy
+    // per warp) so hot bins are not contended across warps
+    int replicas = 1;
+    if (c.strategy == BH_STRATEGY_PRIV) {
+        const size_t spare = h->smem_optin - kStaticSmemReserve - (c.vsm ? tabs : 0);
+        const int cap = threads_of(c.strategy, c.weighted) / 32;
+        replicas = (int)std::max<size_t>(1, std::min<size_t>(cap, spare / std::max<size_t>(sink, 1)));
+        const char *env = getenv("BHIST_PRIV_REPLICAS");
+        if (env) replicas = std::max(1, std::min(replicas, atoi(env)));
+        // the variable-axis tables sit behind all replicas
+        for (int a = 0; a < h->dim; ++a)
+            if (ax[a].var) ax[a].tab_off += (int32_t)((replicas - 1) * sink);
+        sink *= replicas;
+    }
     c.smem = sink + (c.vsm ? tabs : 0);
     if (c.smem + kStaticSmemReserve > h->smem_optin)
         return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", c.strategy, c.smem, h->smem_optin);
@@ -224,10 +246,11 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         p.peel = c.vec && ph ? 1 : 0;
         if (p.peel > m) p.peel = (int32_t)m;
         p.cache_slots = cache_slots_for(c.weighted);
+        p.replicas = replicas;
 
         // launch shape: persistent grid (resident CTAs on every SM), but each block
         // should see enough events to amortize zeroing + flushing its private bins
-        const int nt = threads_of(c.strategy);
+        const int nt = threads_of(c.strategy, c.weighted);
         int64_t want_per_block = (int64_t)nt * 8;
         if (c.strategy == BH_STRATEGY_PRIV) want_per_block = std::max<int64_t>(want_per_block, 4 * h->G);
         int64_t grid = (m + want_per_block - 1) / want_per_block;
@@ -509,6 +532,10 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
     // AUTO strategy); the small ones are packed into fused passes (k_fill_multi) whose
     // privatized bins + search tables + per-thread stats fit in shared memory.
     const size_t kFuseLimit = 64 * 1024;
+    const char *env_t = getenv("BHIST_MULTI_THREADS");
+    const int mthreads = env_t ? std::max(128, std::min(1024, atoi(env_t))) / 32 * 32 : kMultiThreads;
+    const char *env_a = getenv("BHIST_MULTI_AGG_UNIT");
+    const int agg_unit = env_a ? atoi(env_a) : 0;
     const size_t budget = hs[0]->smem_optin - kStaticSmemReserve;
     struct Cand { int i; size_t bytes; };
     std::vector<int> solo;
@@ -527,7 +554,7 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
         int stats = 0;
         for (const Cand &c : small) {
             const int k = hs[c.i]->K;
-            if (!cur.empty() && used + c.bytes + (size_t)(stats + k) * kMultiThreads * 8 > budget) {
+            if (!cur.empty() && used + c.bytes + (size_t)(stats + k) * mthreads * 8 > budget) {
                 fused.push_back(cur);
                 cur.clear();
                 used = 0;
@@ -588,8 +615,9 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
             M.entries = H->entries;
         }
         p.nstats = stat_off;
+        p.agg_unit = agg_unit;
         p.acc_off = (int32_t)used;
-        used += (size_t)stat_off * kMultiThreads * sizeof(double);
+        used += (size_t)stat_off * mthreads * sizeof(double);
         if (used > budget) return fail(BH_EINVAL, "fused pass needs %zu B of shared memory", used);
         auto kern = k_fill_multi;
         if (used > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)used));
@@ -599,9 +627,9 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
             p.n = m;
             for (int c = 0; c < ncols; ++c) p.cols[c] = cols[c] + off;
             p.w = w ? w + off : nullptr;
-            int64_t grid = (m + kMultiThreads * 4 - 1) / (kMultiThreads * 4);
+            int64_t grid = (m + mthreads * 4 - 1) / (mthreads * 4);
             grid = std::max<int64_t>(1, std::min<int64_t>(grid, hs[0]->nsm));
-            kern<<<(int)grid, kMultiThreads, used, st>>>(p);
+            kern<<<(int)grid, mthreads, used, st>>>(p);
             CUDA_TRY(cudaGetLastError());
             hs[pass[0]]->launches++;      // one launch, counted once
         }

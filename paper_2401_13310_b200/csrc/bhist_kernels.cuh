@@ -17,7 +17,9 @@ namespace bh {
 constexpr int kMaxDim = 3;
 constexpr int kThreadsGlobal = 512;   // GLOBAL sink: 2 CTAs/SM
 constexpr int kThreadsSmem = 1024;    // PRIV / CACHE sinks: 1 CTA/SM owns the SM's shared memory
-template <int SINK> struct ThreadsOf { static constexpr int v = SINK == 1 ? kThreadsGlobal : kThreadsSmem; };
+template <int SINK, bool W = false> struct ThreadsOf {
+    static constexpr int v = SINK == 1 ? kThreadsGlobal : kThreadsSmem;
+};
 
 // Axis as the kernels see it.  Fixed axes use (xmin, xmax, D = xmax-xmin,
 // inv = n/D), all rounded once on the host exactly as the definition rounds them.
@@ -48,6 +50,7 @@ struct FillP {
     int32_t K;               // number of stats
     int32_t peel;            // vector path: leading events handled one by one (alignment)
     int32_t cache_slots;     // CACHE strategy: shared-memory slots (power of two)
+    int32_t replicas;        // PRIV strategy: copies of the private bins (warp w uses w % replicas)
     unsigned long long *count;   // unit-weight counts [G]
     double *sumw;                // weighted sums [G]
     double *sumw2;               // weighted sums of squares [G]
@@ -251,10 +254,10 @@ __device__ __forceinline__ void block_stats_finish(const FillP &p, double (&s)[K
 }
 
 // ------------------------------------------------------------------ bin sinks
-enum Sink { SINK_PRIV = 0, SINK_GLOBAL = 1, SINK_CACHE = 2 };
+// SINK_PRIVA: PRIV whose weighted adds adapt to collisions (used with replicas > 1,
+// i.e. small bin spaces, where peaked data makes warp-level collisions likely).
+enum Sink { SINK_PRIV = 0, SINK_GLOBAL = 1, SINK_CACHE = 2, SINK_PRIVA = 3 };
 
-// Shared-memory layout of the PRIV sink: unit -> uint32 count[G];
-// weighted -> double sumw[G] then double sumw2[G].
 __device__ __forceinline__ bool cas128_shared(uint32_t addr, unsigned long long cl, unsigned long long ch,
                                               unsigned long long nl, unsigned long long nh,
                                               unsigned long long &ol, unsigned long long &oh) {
@@ -283,42 +286,108 @@ __device__ __forceinline__ void add2_shared(double2 *cell, double w, double w2) 
     }
 }
 
+// Same, returning how many CAS attempts lost (contention telemetry for PrivSink).
+__device__ __forceinline__ int add2_shared_count(double2 *cell, double w, double w2) {
+    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(cell);
+    double2 cur = *cell;
+    int lost = 0;
+    while (true) {
+        unsigned long long ol, oh;
+        if (cas128_shared(addr, __double_as_longlong(cur.x), __double_as_longlong(cur.y),
+                          __double_as_longlong(cur.x + w), __double_as_longlong(cur.y + w2), ol, oh))
+            return lost;
+        ++lost;
+        cur = make_double2(__longlong_as_double(ol), __longlong_as_double(oh));
+    }
+}
+
+// Warp-aggregated variant for peaked data: the lanes of `act` holding the same cell
+// are grouped with match.any, their (w, w*w) summed over the group by a shuffle walk
+// (lane order), and only the group's leader runs the CAS loop -- one CAS per distinct
+// hot cell instead of a k-way serialized CAS storm (a 32-lane same-address CAS.128
+// costs ~760 cycles, tools/microbench/mb2.cu).
+__device__ __forceinline__ void add2_shared_grouped(double2 *base, int g, double w, double w2, unsigned act) {
+    const unsigned peers = __match_any_sync(act, g);
+    const int lane = (int)(threadIdx.x & 31);
+    const int rounds = __reduce_max_sync(act, (unsigned)__popc(peers));
+    double s1 = 0.0, s2 = 0.0;
+    unsigned m = peers;
+    for (int k = 0; k < rounds; ++k) {
+        const int src = m ? __ffs(m) - 1 : lane;
+        const double v1 = __shfl_sync(act, w, src), v2 = __shfl_sync(act, w2, src);
+        if (m) { s1 += v1; s2 += v2; m &= m - 1; }
+    }
+    if (lane == __ffs(peers) - 1) add2_shared(base + g, s1, s2);
+}
+
 // Shared-memory layout of the PRIV sink: unit -> uint32 count[G];
 // weighted -> double2 (sumw, sumw2)[G].
-template <bool W>
+// With R > 1 replicas (small bin spaces) warp w adds into replica w % R, so hot
+// bins are not contended across warps (R = 32: per-warp private histograms); the
+// flush sums the replicas.
+template <bool W, bool ADAPT>
 struct PrivSink {
-    unsigned char *sm;
-    int G;
-    __device__ __forceinline__ void init(unsigned char *s, int g) {
-        sm = s; G = g;
+    uint32_t sm;         // shared-memory address of this warp's replica
+    bool agg;            // ADAPT: the warp's previous add collided -> aggregate this one first
+    static constexpr int kCell = W ? 16 : 4;
+    static __device__ __forceinline__ size_t stride_of(int G) { return ((size_t)G * kCell + 15) & ~size_t(15); }
+    __device__ __forceinline__ void init(unsigned char *s, int G, int R) {
+        const size_t stride = stride_of(G);
+        sm = (uint32_t)__cvta_generic_to_shared(s + (size_t)((threadIdx.x >> 5) % R) * stride);
+        agg = false;
         if (W) {
-            double2 *d = reinterpret_cast<double2 *>(sm);
-            for (int i = threadIdx.x; i < G; i += blockDim.x) d[i] = make_double2(0.0, 0.0);
+            for (int i = threadIdx.x; i < R * (int)(stride / 16); i += blockDim.x)
+                reinterpret_cast<double2 *>(s)[i] = make_double2(0.0, 0.0);
         } else {
-            uint32_t *c = reinterpret_cast<uint32_t *>(sm);
-            for (int i = threadIdx.x; i < G; i += blockDim.x) c[i] = 0u;
+            for (int i = threadIdx.x; i < R * (int)(stride / 4); i += blockDim.x)
+                reinterpret_cast<uint32_t *>(s)[i] = 0u;
         }
     }
     __device__ __forceinline__ void add(int g, double w) {
         if (W) {
-            add2_shared(reinterpret_cast<double2 *>(sm) + g, w, w * w);
+            double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
+            if (!ADAPT) {
+                add2_shared(base + g, w, w * w);
+                return;
+            }
+            // plain CAS while the warp's adds do not collide; after a collision the next
+            // add first groups equal cells with match.any, and keeps doing so while
+            // duplicates persist (peaked data)
+            const unsigned act = __activemask();
+            // lanes outside an earlier partial mask may carry a stale flag: make it uniform
+            agg = __any_sync(act, agg);
+            if (agg) {
+                const unsigned peers = __match_any_sync(act, g);
+                agg = __any_sync(act, __popc(peers) > 1);
+                if (agg) add2_shared_grouped(base, g, w, w * w, act);
+                else add2_shared(base + g, w, w * w);
+            } else {
+                agg = __any_sync(act, add2_shared_count(base + g, w, w * w) > 0);
+            }
         } else {
-            atomicAdd(reinterpret_cast<uint32_t *>(sm) + g, 1u);
+            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(sm + 4u * (uint32_t)g) : "memory");
         }
     }
-    // Merge stage of PAPER.md:162-165: each block adds its local bins to the global ones.
-    __device__ __forceinline__ void flush(const FillP &p) {
+    // Merge stage of PAPER.md:162-165: each block adds its local bins (summed over the
+    // replicas) to the global ones.
+    __device__ __forceinline__ void flush(const FillP &p, const unsigned char *s) {
+        const int G = p.G, R = p.replicas;
+        const size_t stride = stride_of(G);
         if (W) {
-            const double2 *d = reinterpret_cast<const double2 *>(sm);
             for (int i = threadIdx.x; i < G; i += blockDim.x) {
-                const double2 v = d[i];
+                double2 v = reinterpret_cast<const double2 *>(s)[i];
+                for (int r = 1; r < R; ++r) {
+                    const double2 u = reinterpret_cast<const double2 *>(s + r * stride)[i];
+                    v.x += u.x;
+                    v.y += u.y;
+                }
                 if (v.x != 0.0) atomicAdd(p.sumw + i, v.x);
                 if (v.y != 0.0) atomicAdd(p.sumw2 + i, v.y);
             }
         } else {
-            const uint32_t *c = reinterpret_cast<const uint32_t *>(sm);
             for (int i = threadIdx.x; i < G; i += blockDim.x) {
-                const uint32_t v = c[i];
+                uint32_t v = reinterpret_cast<const uint32_t *>(s)[i];
+                for (int r = 1; r < R; ++r) v += reinterpret_cast<const uint32_t *>(s + r * stride)[i];
                 if (v) atomicAdd(p.count + i, (unsigned long long)v);
             }
         }
@@ -337,7 +406,7 @@ struct GlobalSink {
             atomicAdd(pp->count + g, 1ull);
         }
     }
-    __device__ __forceinline__ void flush(const FillP &) {}
+    __device__ __forceinline__ void flush(const FillP &, const unsigned char *) {}
 };
 
 // CACHE sink: direct-mapped shared-memory cache of global bins.  A slot is
@@ -412,7 +481,7 @@ struct CacheSink {
             }
         }
     }
-    __device__ __forceinline__ void flush(const FillP &p) {
+    __device__ __forceinline__ void flush(const FillP &p, const unsigned char *) {
         for (int i = threadIdx.x; i < S; i += blockDim.x) {
             const uint32_t k = keys[i];
             if (k == kEmpty) continue;
@@ -429,7 +498,8 @@ struct CacheSink {
 };
 
 template <int SINK, bool W> struct SinkOf;
-template <bool W> struct SinkOf<SINK_PRIV, W> { using T = PrivSink<W>; };
+template <bool W> struct SinkOf<SINK_PRIV, W> { using T = PrivSink<W, false>; };
+template <bool W> struct SinkOf<SINK_PRIVA, W> { using T = PrivSink<W, true>; };
 template <bool W> struct SinkOf<SINK_GLOBAL, W> { using T = GlobalSink<W>; };
 template <bool W> struct SinkOf<SINK_CACHE, W> { using T = CacheSink<W>; };
 
@@ -451,8 +521,13 @@ __device__ __forceinline__ void do_event(const FillP &p, const double (&x)[DIM],
 }
 
 template <int DIM, bool W>
-struct Batch {            // U event pairs of every column, held in registers
-    static constexpr int U = 2;
+struct Batch {            // U event pairs of every column, held in registers (x2: double-buffered)
+    static constexpr int NCOL = DIM + (W ? 1 : 0);
+#ifndef BH_U_TWO_COLS
+#define BH_U_TWO_COLS 1
+#endif
+    static constexpr int U = NCOL == 1 ? 2 : NCOL == 2 ? BH_U_TWO_COLS : 1;   // <= 64 registers at 1024 threads
+    static constexpr bool DB = NCOL <= 2;             // prefetch the next batch (register double buffer)
     double2 x[U][DIM];
     double2 w[U];
 };
@@ -462,13 +537,15 @@ struct Batch {            // U event pairs of every column, held in registers
 // leading events; the next batch is loaded before the current one is processed
 // (register double-buffering) so each thread keeps 2*U*ncol 16-byte loads in flight.
 template <int DIM, bool W, int SINK, bool VEC, bool VSM>
-__global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
+__global__ void __launch_bounds__((ThreadsOf<SINK, W>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Sink_t = typename SinkOf<SINK, W>::T;
     Sink_t sink;
     if constexpr (SINK == SINK_GLOBAL) sink.pp = &p;
     if constexpr (SINK == SINK_CACHE) sink.pp = &p;
-    if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots); else sink.init(smem, p.G);
+    if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
+    else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas);
+    else sink.init(smem, p.G);
     if constexpr (VSM) stage_axes<DIM>(p.ax, smem);
     if constexpr (SINK != SINK_GLOBAL || VSM) __syncthreads();
 
@@ -501,9 +578,13 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
         };
         B cur, nxt;
         int q0 = tid;
-        if (q0 < npair) load(cur, q0);
+        if (B::DB && q0 < npair) load(cur, q0);
         for (; q0 < npair; q0 += U * nth) {
-            if (q0 + U * nth < npair) load(nxt, q0 + U * nth);
+            if (B::DB) {
+                if (q0 + U * nth < npair) load(nxt, q0 + U * nth);
+            } else {
+                load(cur, q0);       // 3-4 columns: 48-64 B per thread in flight already
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (q0 + u * nth < npair) {
@@ -514,7 +595,7 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
                     do_event<DIM, W, VSM>(p, x1, W ? cur.w[u].y : 1.0, sink, acc, smem);
                 }
             }
-            cur = nxt;
+            if (B::DB) cur = nxt;
         }
         // leading peeled events and the odd tail
         const int tail0 = base + 2 * npair;
@@ -537,7 +618,7 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
 
     if constexpr (SINK != SINK_GLOBAL) {
         __syncthreads();
-        sink.flush(p);
+        sink.flush(p, smem);
     }
     acc.finalize_unit();
     block_stats_finish<Acc<DIM, W>::K>(p, acc.s);
@@ -557,7 +638,7 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
 constexpr int kMaxHist = 8;
 constexpr int kMaxCols = 8;
 constexpr int kMultiStats = 96;          // >= sum of K over the histograms (<= 8 * 11 = 88)
-constexpr int kMultiThreads = 512;
+constexpr int kMultiThreads = 1024;
 
 struct MultiH {
     int32_t dim;
@@ -577,6 +658,7 @@ struct MultiP {
     int64_t n;
     int32_t nh, ncols, nstats;
     int32_t acc_off;                     // byte offset of acc[nstats][blockDim.x]
+    int32_t agg_unit;                    // aggregate equal bins across the warp for unit weights too
     const double *cols[kMaxCols];
     const double *w;
     unsigned int *counter;               // ticket of histogram 0
@@ -592,7 +674,12 @@ __device__ __forceinline__ double pick(const double (&x)[kMaxCols], int c) {
 
 // Bin add for one event of histogram H with warp aggregation: lanes with equal bins
 // elect a leader that adds the group's count (popc) or (sum w, sum w*w) once.
-__device__ __forceinline__ void multi_add(const MultiH &H, unsigned char *smem, bool valid, int g, double w) {
+__device__ __forceinline__ void multi_add(const MultiH &H, unsigned char *smem, bool valid, int g, double w,
+                                          bool agg_unit) {
+    if (!H.weighted && !agg_unit) {          // native u32 ATOMS; the hardware serializes equal addresses
+        if (valid) atomicAdd(reinterpret_cast<uint32_t *>(smem + H.smem_off) + g, 1u);
+        return;
+    }
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     if (!valid) return;
     const unsigned peers = __match_any_sync(act, g);
@@ -613,7 +700,7 @@ __device__ __forceinline__ void multi_add(const MultiH &H, unsigned char *smem, 
     }
 }
 
-__global__ void __launch_bounds__(kMultiThreads, 1) k_fill_multi(const __grid_constant__ MultiP p) {
+__global__ void __launch_bounds__(1024, 1) k_fill_multi(const __grid_constant__ MultiP p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ bool last;
     double *acc = reinterpret_cast<double *>(smem + p.acc_off);     // acc[k * blockDim.x + tid]
@@ -660,7 +747,7 @@ __global__ void __launch_bounds__(kMultiThreads, 1) k_fill_multi(const __grid_co
                 g += b * mul;
                 mul = (a == 0) ? H.st1 : H.st2;
             }
-            multi_add(H, smem, valid, g, w);                 // step (2)
+            multi_add(H, smem, valid, g, w, p.agg_unit != 0);   // step (2)
             if (valid && inr) {                              // step (3)
                 double *ac = acc + (size_t)H.stat_off * T + threadIdx.x;
                 const double wx = w * xa[0];

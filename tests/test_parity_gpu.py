@@ -339,3 +339,17 @@ def test_fill_multi_rejects_bad_arguments():
     with pytest.raises(pkg.BHistError):
         pkg.bh_fill_multi([h.h, h.h], [[0], [0]], [False, False], 10, [x.data_ptr()])   # duplicate
     h.close()
+
+
+@pytest.mark.parametrize("nbins,weighted", [(100, True), (100, False), (2000, True)])
+def test_peaked_small_histograms_replicas(nbins, weighted):
+    # Cauchy-peaked data on small bin spaces: PRIV with per-warp replicas and the
+    # collision-adaptive weighted path (most lanes of a warp hit the same bin)
+    rng = np.random.default_rng(nbins)
+    n = 2_000_001
+    x = 0.505 + 0.002 * np.tan(np.pi * (rng.random(n) - 0.5))
+    w = rng.uniform(0.5, 1.5, n) if weighted else None
+    axes = [(nbins, 0.0, 1.0)]
+    ref = oracle.OracleHist(axes).fill([x], w).read()
+    for s in (pkg.BH_STRATEGY_PRIV, pkg.BH_STRATEGY_CACHE, pkg.BH_STRATEGY_GLOBAL):
+        compare(_gpu_fill(axes, [x], w, s), ref, weighted, f"peaked {nbins} strat {s}")

@@ -189,12 +189,18 @@ def run_gpu(args):
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("for --gpus N>1 launch with torchrun --nproc-per-node N")
+    local = local % torch.cuda.device_count()     # (tests: several gloo ranks may share one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
 
     wl = get_workload(args.config)
+    if args.events:
+        wl.n_events = args.events
     N = wl.n_events
     start = rank * N           # weak scaling: this rank's shard of the seeded stream
     hists = wl.hists
@@ -361,6 +367,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--strategy", default="auto", choices=["auto", "priv", "global", "cache"])
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend for N>1")
+    ap.add_argument("--events", type=int, default=0, help="override events per GPU (tests)")
     ap.add_argument("--cpu-sample", type=int, default=50_000_000)
     ap.add_argument("--ref-sample", type=int, default=1 << 23)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -353,3 +353,24 @@ def test_peaked_small_histograms_replicas(nbins, weighted):
     ref = oracle.OracleHist(axes).fill([x], w).read()
     for s in (pkg.BH_STRATEGY_PRIV, pkg.BH_STRATEGY_CACHE, pkg.BH_STRATEGY_GLOBAL):
         compare(_gpu_fill(axes, [x], w, s), ref, weighted, f"peaked {nbins} strat {s}")
+
+
+def test_bench_two_ranks_exchange(tmp_path):
+    """bench.py's N>1 path end to end on one GPU: 2 torchrun ranks (gloo backend so both
+    may share cuda:0), contiguous shards, pack -> all-reduce -> unpack every step; the
+    e2e leg asserts every rank ends with entries == N * world."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--backend", "gloo", "--events", "2000000", "--e2e-steps", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["scaling"] == "weak"
+    assert d["cpu_baseline"] is None          # rank 0 at N=1 only

@@ -1,0 +1,52 @@
+"""Small fills of every kernel family, for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bhgen  # noqa: E402
+import paper_2401_13310_b200 as pkg  # noqa: E402
+
+dev = "cuda:0"
+rng = np.random.default_rng(1)
+n = 20_011
+for name in ("C1", "C2", "C3W", "C4"):
+    wl = bhgen.workload(name, n)
+    h = wl.hists[0]
+    cols = [torch.from_numpy(wl.column(c, 0, n)).to(dev) for c in h.cols]
+    w = torch.from_numpy(wl.column(wl.wcol, 0, n)).to(dev) if h.weighted else None
+    for s in (pkg.BH_STRATEGY_PRIV, pkg.BH_STRATEGY_GLOBAL, pkg.BH_STRATEGY_CACHE):
+        if s == pkg.BH_STRATEGY_PRIV and name in ("C3W", "C4"):
+            continue
+        H = pkg.Histogram(h.axes_spec(), strategy=s)
+        H.fill(cols, w)
+        H.fill([c[1:] for c in cols], None if w is None else w[1:])   # peeled / misaligned path
+        H.find_bins(cols)
+        H.read()
+        H.close()
+# peaked weighted small histogram: replicas + collision-adaptive CAS
+x = torch.from_numpy(0.505 + 0.002 * np.tan(np.pi * (rng.random(n) - 0.5))).to(dev)
+w = torch.from_numpy(rng.uniform(0.5, 1.5, n)).to(dev)
+H = pkg.Histogram([(100, 0.0, 1.0)])
+H.fill([x], w)
+H.read()
+H.close()
+# fused multi-histogram fill and the host path
+wl = bhgen.workload("C5", n)
+cols = [torch.from_numpy(wl.column(c, 0, n)).to(dev) for c in range(len(wl.columns))]
+hs = [pkg.Histogram(h.axes_spec()) for h in wl.hists]
+pkg.fill_multi(hs, [h.cols for h in wl.hists], [h.weighted for h in wl.hists], cols, cols[wl.wcol])
+for H in hs:
+    H.read()
+    H.close()
+H = pkg.Histogram([(1000, 0.0, 1.0)])
+pkg.bh_set_chunk(H.h, 4096)
+H.fill_host([torch.from_numpy(rng.random(n)).pin_memory()])
+buf = H.pack()
+H.unpack(buf)
+H.read()
+H.close()
+torch.cuda.synchronize()
+print("sanitize run ok")

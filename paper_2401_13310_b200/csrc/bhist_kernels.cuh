@@ -141,6 +141,9 @@ __device__ __forceinline__ int find_bin_var_smem(const AxisP &a, double x, const
 
 template <bool VSM>
 __device__ __forceinline__ int find_bin(const AxisP &a, double x, const unsigned char *smem) {
+#ifdef BH_EXP_NOSEARCH   // experiment only (wrong results): bin from the guide cell alone
+    if (a.var) return x < a.xmin ? 0 : (!(x < a.xmax) ? a.n + 1 : 1 + (int)((long long)guide_cell(a, x) * a.n / a.gcells));
+#endif
     if (!a.var) return find_bin_fixed(a, x);
     if (VSM) {
         return a.g16 ? find_bin_var_smem<true>(a, x, smem + a.tab_off) : find_bin_var_smem<false>(a, x, smem + a.tab_off);
@@ -346,6 +349,9 @@ struct PrivSink {
     __device__ __forceinline__ void add(int g, double w) {
         if (W) {
             double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
+#ifdef BH_EXP_NOCAS   // experiment only (wrong results): plain read-modify-write instead of CAS
+            { double2 v = base[g]; v.x += w; v.y += w * w; base[g] = v; return; }
+#endif
             if (!ADAPT) {
                 add2_shared(base + g, w, w * w);
                 return;

@@ -361,8 +361,12 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
             P.var = 1;
             P.xmin = A.edges[0];
             P.xmax = A.edges[A.nbins];
-            int gc = 1;                       // about one interior edge per cell, power of two
+            // guide cells: a power of two, up to ~4 per bin (fewer edges per cell for
+            // non-uniform edges, e.g. log-spaced) while the shared-memory tables (float32
+            // edges + uint16 guide) stay <= 56 KB; at least ~n/2 cells
+            int gc = 1;
             while (2 * gc < A.nbins && gc < (1 << 22)) gc <<= 1;
+            while (gc < 4 * A.nbins && 4 * (size_t)(A.nbins + 1) + 2 * (size_t)(2 * gc + 1) <= 56 * 1024) gc <<= 1;
             P.gcells = gc;
             P.gscale = (double)gc / (P.xmax - P.xmin);
             if (!std::isfinite(P.gscale) || !(P.gscale > 0)) return cleanup(fail(BH_EINVAL, "axis %d: edge range too small", a));
@@ -528,39 +532,53 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
     if (n == 0) return BH_OK;
     DeviceGuard dg(hs[0]->device);
     cudaStream_t st = static_cast<cudaStream_t>(s);
-    // ---- plan: histograms with a large private state get a pass of their own (k_fill,
-    // AUTO strategy); the small ones are packed into fused passes (k_fill_multi) whose
-    // privatized bins + search tables + per-thread stats fit in shared memory.
+    // ---- plan.  The single-histogram kernel (k_fill, fully templated) is faster per
+    // histogram than the generic fused kernel, and the fill is bound by the bin updates,
+    // not by HBM; so fusing only pays when histograms read the SAME columns (e.g. one
+    // variable with several binnings): then the fused pass reads them once.  Histograms
+    // with a small private state and an identical column set (+ weight flag) are packed
+    // into fused passes (k_fill_multi) whose privatized bins, variable-axis tables and
+    // per-thread statistics columns fit in shared memory; all others get solo passes.
     const size_t kFuseLimit = 64 * 1024;
     const char *env_t = getenv("BHIST_MULTI_THREADS");
     const int mthreads = env_t ? std::max(128, std::min(1024, atoi(env_t))) / 32 * 32 : kMultiThreads;
+    const char *env_s = getenv("BHIST_MULTI_SOLO");
+    const bool fuse_off = env_s && atoi(env_s) != 0;
     const char *env_a = getenv("BHIST_MULTI_AGG_UNIT");
     const int agg_unit = env_a ? atoi(env_a) : 0;
     const size_t budget = hs[0]->smem_optin - kStaticSmemReserve;
-    struct Cand { int i; size_t bytes; };
+    struct Cand { int i; size_t bytes; std::vector<int> key; };
     std::vector<int> solo;
     std::vector<Cand> small;
     for (int i = 0; i < nh; ++i) {
         const bh_hist *H = hs[i];
         size_t b = align16((weighted[i] ? 16 : 4) * (size_t)H->G);
         for (int a = 0; a < H->dim; ++a) b += axis_table_bytes(H->ax[a]);
-        if (b > kFuseLimit) solo.push_back(i); else small.push_back({i, b});
+        std::vector<int> key;
+        for (int a = 0; a < H->dim; ++a) key.push_back(col_of_axis[3 * i + a]);
+        std::sort(key.begin(), key.end());
+        key.push_back(weighted[i] ? 1 : 0);
+        if (b > kFuseLimit || fuse_off) solo.push_back(i); else small.push_back({i, b, key});
     }
-    std::sort(small.begin(), small.end(), [](const Cand &x, const Cand &y) { return x.bytes < y.bytes; });
+    std::stable_sort(small.begin(), small.end(), [](const Cand &x, const Cand &y) {
+        return x.key != y.key ? x.key < y.key : x.bytes < y.bytes; });
     std::vector<std::vector<int>> fused;
     {
         std::vector<int> cur;
+        std::vector<int> cur_key;
         size_t used = 0;
         int stats = 0;
         for (const Cand &c : small) {
             const int k = hs[c.i]->K;
-            if (!cur.empty() && used + c.bytes + (size_t)(stats + k) * mthreads * 8 > budget) {
+            if (!cur.empty() && (c.key != cur_key ||
+                                 used + c.bytes + (size_t)(stats + k) * mthreads * 8 > budget)) {
                 fused.push_back(cur);
                 cur.clear();
                 used = 0;
                 stats = 0;
             }
             cur.push_back(c.i);
+            cur_key = c.key;
             used += c.bytes;
             stats += k;
         }

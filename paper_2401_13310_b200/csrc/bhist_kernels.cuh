@@ -356,19 +356,19 @@ struct PrivSink {
                 add2_shared(base + g, w, w * w);
                 return;
             }
-            // plain CAS while the warp's adds do not collide; after a collision the next
-            // add first groups equal cells with match.any, and keeps doing so while
-            // duplicates persist (peaked data)
+            // plain CAS while a warp's adds collide little (a lost CAS just retries); once
+            // >= 8 lanes of an add lost, the next adds first group equal cells with
+            // match.any, and keep doing so while some cell holds >= 4 lanes (peaked data)
             const unsigned act = __activemask();
             // lanes outside an earlier partial mask may carry a stale flag: make it uniform
             agg = __any_sync(act, agg);
             if (agg) {
                 const unsigned peers = __match_any_sync(act, g);
-                agg = __any_sync(act, __popc(peers) > 1);
-                if (agg) add2_shared_grouped(base, g, w, w * w, act);
+                agg = __any_sync(act, __popc(peers) >= 4);
+                if (__any_sync(act, __popc(peers) > 1)) add2_shared_grouped(base, g, w, w * w, act);
                 else add2_shared(base + g, w, w * w);
             } else {
-                agg = __any_sync(act, add2_shared_count(base + g, w, w * w) > 0);
+                agg = __popc(__ballot_sync(act, add2_shared_count(base + g, w, w * w) > 0)) >= 8;
             }
         } else {
             asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(sm + 4u * (uint32_t)g) : "memory");

@@ -374,3 +374,24 @@ def test_bench_two_ranks_exchange(tmp_path):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["scaling"] == "weak"
     assert d["cpu_baseline"] is None          # rank 0 at N=1 only
+
+
+def test_fill_multi_fused_same_columns():
+    # histograms over the same column(s) with different binnings share one fused pass
+    # (k_fill_multi): fixed, variable (log) and 2D axes, unit and weighted
+    rng = np.random.default_rng(21)
+    n = 1_000_003
+    x = rng.normal(0.5, 0.2, n)
+    y = 0.505 + 0.002 * np.tan(np.pi * (rng.random(n) - 0.5))
+    w = rng.uniform(0.5, 1.5, n)
+    specs = [([(100, 0.0, 1.0)], [0], False), ([(37, -0.5, 1.5)], [0], False),
+             ([np.geomspace(1e-3, 2.0, 301)], [0], False),
+             ([(50, 0.0, 1.0)], [0], True), ([np.linspace(0.0, 1.0, 201)], [0], True),
+             ([(20, 0.0, 1.0), (20, 0.4, 0.6)], [0, 1], True), ([(30, 0.0, 1.0), (30, 0.4, 0.6)], [0, 1], True)]
+    cols = [_t(x), _t(y)]
+    hs = [pkg.Histogram(ax) for ax, _, _ in specs]
+    pkg.fill_multi(hs, [c for _, c, _ in specs], [wt for _, _, wt in specs], cols, _t(w))
+    for h, (ax, c, wt) in zip(hs, specs):
+        ref = oracle.OracleHist(ax).fill([[x, y][i] for i in c], w if wt else None).read()
+        compare(h.read(), ref, wt, f"fused {ax}")
+        h.close()

@@ -196,7 +196,7 @@ cudaError_t launch_d(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
 int threads_of(int strategy, bool) { return strategy == BH_STRATEGY_GLOBAL ? kThreadsGlobal : kThreadsSmem; }
 int resident_blocks(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? 2 : 1; }
 
-// One fill over device-resident columns, split into launches of <= 2^31 events.
+// One fill over device-resident columns, split into launches of <= 2^30 events.
 bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
     LaunchCfg c{};
     c.weighted = w != nullptr;
@@ -230,7 +230,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
     c.smem = sink + (c.vsm ? tabs : 0);
     if (c.smem + kStaticSmemReserve > h->smem_optin)
         return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", c.strategy, c.smem, h->smem_optin);
-    const int64_t kMaxLaunch = int64_t(1) << 31;
+    const int64_t kMaxLaunch = int64_t(1) << 30;   // in-kernel event indices are int32
     for (int64_t off = 0; off < n; off += kMaxLaunch) {
         const int64_t m = std::min(kMaxLaunch, n - off);
         const double *cs[kMaxDim] = {};
@@ -639,7 +639,7 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
         if (used > budget) return fail(BH_EINVAL, "fused pass needs %zu B of shared memory", used);
         auto kern = k_fill_multi;
         if (used > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)used));
-        const int64_t kMaxLaunch = int64_t(1) << 31;
+        const int64_t kMaxLaunch = int64_t(1) << 30;   // in-kernel event indices are int32
         for (int64_t off = 0; off < n; off += kMaxLaunch) {
             const int64_t m = std::min(kMaxLaunch, n - off);
             p.n = m;

@@ -557,7 +557,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK, W>::v), SINK == SINK_GLOBAL ?
 
     Acc<DIM, W> acc;
     acc.zero();
-    // one launch covers <= 2^31 events, so pair and event indices fit in int32
+    // one launch covers <= 2^30 events (host split), so pair and event indices fit in int32
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     const int nth = gridDim.x * blockDim.x;
 

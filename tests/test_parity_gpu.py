@@ -395,3 +395,27 @@ def test_fill_multi_fused_same_columns():
         ref = oracle.OracleHist(ax).fill([[x, y][i] for i in c], w if wt else None).read()
         compare(h.read(), ref, wt, f"fused {ax}")
         h.close()
+
+
+@pytest.mark.slow
+def test_single_fill_above_2_31_events():
+    """One bh_fill of 2^31 + 5 events (17 GB column): exercises the split into launches of
+    <= 2^31 events and the 32-bit in-kernel indices; counts must equal the oracle's."""
+    n = (1 << 31) + 5
+    if torch.cuda.get_device_properties(0).total_memory < 40 * 2 ** 30:
+        pytest.skip("needs > 40 GB of device memory")
+    wl = bhgen.workload("C1", n)
+    xd = torch.empty(n, dtype=torch.float64, device=DEV)
+    chunk = 1 << 27
+    host = torch.empty(chunk, dtype=torch.float64).pin_memory()
+    for off in range(0, n, chunk):
+        m = min(chunk, n - off)
+        wl.column_ptr(0, off, m, host.data_ptr())
+        xd[off:off + m].copy_(host[:m])
+    h = pkg.Histogram([(100, 0.0, 1.0)])
+    h.fill([xd])
+    got = h.read()
+    h.close()
+    del xd
+    ref = oracle_parallel("C1", n)
+    compare(got, ref, False, "2^31+5")

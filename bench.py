@@ -175,6 +175,47 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ secondary rows (device-resident only)
+def measure_secondary(name: str, steps: int, warmup: int, local: int) -> dict:
+    """Device-resident events/s and roofline fraction of another config's fill kernel,
+    same protocol as the headline (CUDA events around each bh_fill; inputs >> L2)."""
+    import torch
+    import paper_2401_13310_b200 as pkg
+    wl = get_workload(name)
+    h = wl.hists[0]
+    N = wl.n_events
+    host = torch.empty(N, dtype=torch.float64).pin_memory()
+    cols = []
+    for c in h.cols:
+        wl.column_ptr(c, 0, N, host.data_ptr())
+        cols.append(host.to(f"cuda:{local}"))
+    w = None
+    if h.weighted:
+        wl.column_ptr(wl.wcol, 0, N, host.data_ptr())
+        w = host.to(f"cuda:{local}")
+    del host
+    H = pkg.Histogram(h.axes_spec(), device=local)
+    st = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(warmup + steps):
+        H.reset()
+        if i >= warmup:
+            ev[i - warmup][0].record(st)
+        H.fill(cols, w)
+        if i >= warmup:
+            ev[i - warmup][1].record(st)
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    peak, _ = hbm_peak()
+    gbs = wl.bytes_per_event * N / (ms * 1e-3) / 1e9
+    strat = {1: "priv", 2: "global", 3: "cache"}.get(H.strategy(h.weighted), "?")
+    H.close()
+    del cols, w
+    torch.cuda.empty_cache()
+    return {"workload": workload_desc(wl), "events": N, "events_per_s": N / (ms * 1e-3), "fill_ms": ms,
+            "achieved_gbs": gbs, "frac": gbs / peak, "fill_strategy": strat}
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_gpu(args):
     import torch
@@ -257,6 +298,8 @@ def run_gpu(args):
     for i in range(args.steps):
         step(i)
     t1.record(stream)
+    while not t1.query():          # poll (releases the GIL) so the clock sampler keeps sampling
+        time.sleep(0.0005)
     torch.cuda.synchronize()
     clk.stop()
     dl = [pkg.bh_launch_count(H.h) - a for H, a in zip(Hs, l0)]
@@ -310,6 +353,14 @@ def run_gpu(args):
     h2d = 8 * N * len(used)
     d2h = 8 * sum(pkg.bh_packed_size(H.h) for H in Hs)
 
+    # ---- secondary rows (rank 0, N=1): e.g. the 1D fixed-bin target of the north star (C1S)
+    secondary = {}
+    if rank == 0 and world == 1 and args.secondary:
+        del devc
+        torch.cuda.empty_cache()
+        for name in [x for x in args.secondary.split(",") if x]:
+            secondary[name] = measure_secondary(name, max(3, min(args.steps, 10)), 3, local)
+
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -349,6 +400,7 @@ def run_gpu(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "secondary": secondary or None,
         }
         print(json.dumps(line), flush=True)
     for H in Hs:
@@ -369,6 +421,8 @@ def main():
     ap.add_argument("--strategy", default="auto", choices=["auto", "priv", "global", "cache"])
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend for N>1")
     ap.add_argument("--events", type=int, default=0, help="override events per GPU (tests)")
+    ap.add_argument("--secondary", default="C1S",
+                    help="comma list of extra configs measured device-resident after the headline ('' = none)")
     ap.add_argument("--cpu-sample", type=int, default=50_000_000)
     ap.add_argument("--ref-sample", type=int, default=1 << 23)
     ap.add_argument("--no-cpu-baseline", action="store_true")

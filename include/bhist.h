@@ -122,6 +122,46 @@ bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const
 bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_axis, const uint8_t *weighted,
                         int64_t n, const double *const *cols, int32_t ncols, const double *w, bh_stream s);
 
+/* Fused Filter + Define (the RDataFrame example of PAPER.md:95-98,
+ * df.Filter(...).Define(...).Histo1D(...), without materializing the derived column).
+ * Per event: registers r[0..16) start as r[c] = cols[c][i] for c < ncols (DEVICE float64
+ * columns), 0 otherwise; the nops (<= 32) ops of prog run in order; the event is skipped
+ * unless filter_reg < 0 or r[filter_reg] != 0; otherwise it is filled at coordinates
+ * r[axis_reg[a]] (a < dim) with weight r[weight_reg] (unit weights if weight_reg < 0).
+ * entries counts the events that pass.  Every op is IEEE correctly rounded, so derived
+ * coordinates equal the same expression evaluated in binary64 anywhere.  Async on s.
+ * Errors: BH_EINVAL (bad opcode / register / counts), BH_ECUDA. */
+typedef struct {
+    int32_t op;      /* BH_OP_* */
+    int32_t dst;     /* destination register */
+    int32_t a, b, c; /* operand registers (unused ones ignored, must still be in range) */
+    int32_t pad;
+    double imm;      /* BH_OP_CONST value */
+} bh_op;
+#define BH_OP_CONST 0  /* r[dst] = imm */
+#define BH_OP_COPY 1   /* r[dst] = r[a] */
+#define BH_OP_ADD 2    /* r[a] + r[b] */
+#define BH_OP_SUB 3    /* r[a] - r[b] */
+#define BH_OP_MUL 4    /* r[a] * r[b] */
+#define BH_OP_DIV 5    /* r[a] / r[b] */
+#define BH_OP_SQRT 6   /* sqrt(r[a]) */
+#define BH_OP_ABS 7    /* |r[a]| */
+#define BH_OP_NEG 8    /* -r[a] */
+#define BH_OP_MIN 9    /* fmin(r[a], r[b]) (IEEE minNum: a NaN operand yields the other) */
+#define BH_OP_MAX 10   /* fmax(r[a], r[b]) */
+#define BH_OP_LT 11    /* 1.0 if r[a] < r[b] else 0.0 (likewise LE GT GE EQ NE) */
+#define BH_OP_LE 12
+#define BH_OP_GT 13
+#define BH_OP_GE 14
+#define BH_OP_EQ 15
+#define BH_OP_NE 16
+#define BH_OP_AND 17   /* (r[a] != 0) && (r[b] != 0) */
+#define BH_OP_OR 18    /* (r[a] != 0) || (r[b] != 0) */
+#define BH_OP_NOT 19   /* !(r[a] != 0) */
+#define BH_OP_SELECT 20 /* r[a] != 0 ? r[b] : r[c] */
+bh_status bh_fill_expr(bh_hist *h, int64_t n, const double *const *cols, int32_t ncols, const bh_op *prog,
+                       int32_t nops, const int32_t *axis_reg, int32_t weight_reg, int32_t filter_reg, bh_stream s);
+
 /* Per-event global bin (parity/debug): out[i] = g(event i), int32, DEVICE pointer. */
 bh_status bh_find_bins(const bh_hist *h, int64_t n, const double *const *coords, int32_t *out, bh_stream s);
 

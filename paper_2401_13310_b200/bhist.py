@@ -22,7 +22,7 @@ BH_DEBUG_SKIP_COPY_WAIT = 1
 
 # every symbol include/bhist.h declares (checked by tests/test_abi.py)
 EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset", "bh_fill", "bh_fill_host",
-            "bh_fill_multi", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
+            "bh_fill_multi", "bh_fill_expr", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
             "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_launch_count"]
 
 
@@ -30,6 +30,17 @@ class BHistError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"bhist error {status}: {msg}")
         self.status = status
+
+
+class _Op(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("dst", ctypes.c_int32), ("a", ctypes.c_int32), ("b", ctypes.c_int32),
+                ("c", ctypes.c_int32), ("pad", ctypes.c_int32), ("imm", ctypes.c_double)]
+
+
+# opcodes of bh_fill_expr (include/bhist.h BH_OP_*)
+OPS = {name: i for i, name in enumerate(
+    ["const", "copy", "add", "sub", "mul", "div", "sqrt", "abs", "neg", "min", "max", "lt", "le", "gt", "ge",
+     "eq", "ne", "and", "or", "not", "select"])}
 
 
 class _Axis(ctypes.Structure):
@@ -66,6 +77,7 @@ def lib(build_if_stale: bool = False):
             "bh_fill_host": ([_P, _I64, _P, _P, _P], _I32),
             "bh_find_bins": ([_P, _I64, _P, _P, _P], _I32),
             "bh_fill_multi": ([_P, _I32, _P, _P, _I64, _P, _I32, _P, _P], _I32),
+            "bh_fill_expr": ([_P, _I64, _P, _I32, _P, _I32, _P, _I32, _I32, _P], _I32),
             "bh_info": ([_P, _P, _P, _P], _I32),
             "bh_packed_size": ([_P, _P], _I32),
             "bh_pack": ([_P, _P, _P], _I32),
@@ -151,6 +163,60 @@ def bh_fill_multi(handles, col_of_axis, weighted, n: int, col_ptrs, w_ptr=None, 
     cp = (ctypes.c_void_p * len(col_ptrs))(*col_ptrs)
     _check(lib().bh_fill_multi(ctypes.addressof(hs), nh, ctypes.addressof(coa), ctypes.addressof(wt), n,
                                ctypes.addressof(cp), len(col_ptrs), w_ptr, stream))
+
+
+def bh_fill_expr(h, n: int, col_ptrs, prog, axis_regs, weight_reg: int = -1, filter_reg: int = -1,
+                 stream=None) -> None:
+    """prog: list of (opname, dst, a, b, c, imm) tuples (see Program)."""
+    cp = (ctypes.c_void_p * max(1, len(col_ptrs)))(*col_ptrs)
+    ops = (_Op * max(1, len(prog)))()
+    for k, (name, dst, a, b, c, imm) in enumerate(prog):
+        ops[k] = _Op(OPS[name], dst, a, b, c, 0, float(imm))
+    ar = (ctypes.c_int32 * 3)(*(list(axis_regs) + [0] * (3 - len(axis_regs))))
+    _check(lib().bh_fill_expr(h, n, ctypes.addressof(cp), len(col_ptrs), ctypes.addressof(ops), len(prog),
+                              ctypes.addressof(ar), weight_reg, filter_reg, stream))
+
+
+class Program:
+    """Builder for bh_fill_expr register programs: registers 0..ncols-1 are the input
+    columns; every method appends one op and returns the register it wrote."""
+
+    def __init__(self, ncols: int):
+        self.ncols = ncols
+        self.ops = []
+        self._next = ncols
+
+    def _emit(self, name, a=0, b=0, c=0, imm=0.0):
+        if self._next >= 16:
+            raise ValueError("out of registers (16)")
+        r = self._next
+        self._next += 1
+        self.ops.append((name, r, a, b, c, imm))
+        return r
+
+    def const(self, v):
+        return self._emit("const", imm=v)
+
+    def land(self, a, b):
+        return self._emit("and", a, b)
+
+    def lor(self, a, b):
+        return self._emit("or", a, b)
+
+    def lnot(self, a):
+        return self._emit("not", a)
+
+    def __getattr__(self, name):
+        if name in OPS and name != "const":
+            return lambda a=0, b=0, c=0: self._emit(name, a, b, c)
+        raise AttributeError(name)
+
+
+def fill_expr(hist, cols, prog: "Program", axis_regs, weight_reg: int = -1, filter_reg: int = -1, stream=None):
+    """Filter + Define + fill in one kernel: cols are contiguous float64 CUDA tensors."""
+    n = cols[0].numel() if cols else 0
+    bh_fill_expr(hist.h, n, [c.data_ptr() for c in cols], prog.ops, axis_regs, weight_reg, filter_reg,
+                 _stream_handle(stream))
 
 
 def fill_multi(hists, col_of_axis, weighted, cols, w=None, stream=None) -> None:

@@ -196,40 +196,64 @@ cudaError_t launch_d(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
 int threads_of(int strategy, bool) { return strategy == BH_STRATEGY_GLOBAL ? kThreadsGlobal : kThreadsSmem; }
 int resident_blocks(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? 2 : 1; }
 
-// One fill over device-resident columns, split into launches of <= 2^30 events.
-bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
+// Shared-memory plan of one fill: strategy, variable-axis tables (VSM), PRIV replicas.
+struct FillPlan {
     LaunchCfg c{};
-    c.weighted = w != nullptr;
+    AxisP ax[kMaxDim];
+    int replicas = 1;
+};
+
+bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl) {
+    LaunchCfg &c = pl.c;
+    c.weighted = weighted;
     c.strategy = resolve_strategy(h, c.weighted);
     size_t sink = sink_bytes(h, c.strategy, c.weighted);
     // variable-axis tables go to shared memory behind the sink when they fit
     size_t tabs = 0;
-    AxisP ax[kMaxDim];
     for (int a = 0; a < h->dim; ++a) {
-        ax[a] = h->ax[a];
-        if (ax[a].var) {
-            ax[a].tab_off = (int32_t)(sink + tabs);
-            tabs += axis_table_bytes(ax[a]);
+        pl.ax[a] = h->ax[a];
+        if (pl.ax[a].var) {
+            pl.ax[a].tab_off = (int32_t)(sink + tabs);
+            tabs += axis_table_bytes(pl.ax[a]);
         }
     }
     c.vsm = tabs > 0 && sink + tabs + kStaticSmemReserve <= h->smem_optin;
     // PRIV: replicate the private bins into the spare shared memory (up to one copy
     // per warp) so hot bins are not contended across warps
-    int replicas = 1;
+    pl.replicas = 1;
     if (c.strategy == BH_STRATEGY_PRIV) {
         const size_t spare = h->smem_optin - kStaticSmemReserve - (c.vsm ? tabs : 0);
         const int cap = threads_of(c.strategy, c.weighted) / 32;
-        replicas = (int)std::max<size_t>(1, std::min<size_t>(cap, spare / std::max<size_t>(sink, 1)));
+        pl.replicas = (int)std::max<size_t>(1, std::min<size_t>(cap, spare / std::max<size_t>(sink, 1)));
         const char *env = getenv("BHIST_PRIV_REPLICAS");
-        if (env) replicas = std::max(1, std::min(replicas, atoi(env)));
+        if (env) pl.replicas = std::max(1, std::min(pl.replicas, atoi(env)));
         // the variable-axis tables sit behind all replicas
         for (int a = 0; a < h->dim; ++a)
-            if (ax[a].var) ax[a].tab_off += (int32_t)((replicas - 1) * sink);
-        sink *= replicas;
+            if (pl.ax[a].var) pl.ax[a].tab_off += (int32_t)((pl.replicas - 1) * sink);
+        sink *= pl.replicas;
     }
     c.smem = sink + (c.vsm ? tabs : 0);
     if (c.smem + kStaticSmemReserve > h->smem_optin)
-        return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", c.strategy, c.smem, h->smem_optin);
+        return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", c.strategy, c.smem,
+                    h->smem_optin);
+    return BH_OK;
+}
+
+// Persistent grid (resident CTAs on every SM), but each block should see enough events
+// to amortize zeroing + flushing its private bins.
+int grid_for(const bh_hist *h, const LaunchCfg &c, int64_t m) {
+    const int nt = threads_of(c.strategy, c.weighted);
+    int64_t want_per_block = (int64_t)nt * 8;
+    if (c.strategy == BH_STRATEGY_PRIV) want_per_block = std::max<int64_t>(want_per_block, 4 * h->G);
+    int64_t grid = (m + want_per_block - 1) / want_per_block;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)h->nsm * resident_blocks(c.strategy)));
+}
+
+// One fill over device-resident columns, split into launches of <= 2^30 events.
+bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
+    FillPlan pl;
+    if (bh_status r = plan_fill(h, w != nullptr, pl)) return r;
+    LaunchCfg &c = pl.c;
     const int64_t kMaxLaunch = int64_t(1) << 30;   // in-kernel event indices are int32
     for (int64_t off = 0; off < n; off += kMaxLaunch) {
         const int64_t m = std::min(kMaxLaunch, n - off);
@@ -237,7 +261,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         for (int a = 0; a < h->dim; ++a) cs[a] = coords[a] + off;
         const double *ws = c.weighted ? w + off : nullptr;
         FillP p = make_params(h, m, cs, ws);
-        for (int a = 0; a < h->dim; ++a) p.ax[a] = ax[a];
+        for (int a = 0; a < h->dim; ++a) p.ax[a] = pl.ax[a];
         // vector path: every column must share the same 16-byte phase
         const uintptr_t ph = reinterpret_cast<uintptr_t>(cs[0]) & 15;
         c.vec = (ph % 8) == 0;
@@ -246,16 +270,8 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         p.peel = c.vec && ph ? 1 : 0;
         if (p.peel > m) p.peel = (int32_t)m;
         p.cache_slots = cache_slots_for(c.weighted);
-        p.replicas = replicas;
-
-        // launch shape: persistent grid (resident CTAs on every SM), but each block
-        // should see enough events to amortize zeroing + flushing its private bins
-        const int nt = threads_of(c.strategy, c.weighted);
-        int64_t want_per_block = (int64_t)nt * 8;
-        if (c.strategy == BH_STRATEGY_PRIV) want_per_block = std::max<int64_t>(want_per_block, 4 * h->G);
-        int64_t grid = (m + want_per_block - 1) / want_per_block;
-        grid = std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)h->nsm * resident_blocks(c.strategy)));
-        c.grid = (int)grid;
+        p.replicas = pl.replicas;
+        c.grid = grid_for(h, c, m);
         cudaError_t e;
         switch (h->dim) {
         case 1: e = launch_d<1>(p, c, s); break;
@@ -266,6 +282,35 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         ++h->launches;
     }
     return BH_OK;
+}
+
+template <int DIM, bool W, int SINK>
+cudaError_t launch_expr_s(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
+    auto kern = c.vsm ? k_fill_expr<DIM, W, SINK, true> : k_fill_expr<DIM, W, SINK, false>;
+    if (c.smem > 48 * 1024) {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+        if (r != cudaSuccess) return r;
+    }
+    kern<<<c.grid, ThreadsOf<SINK, W>::v, c.smem, s>>>(p, e);
+    return cudaGetLastError();
+}
+
+template <int DIM, bool W>
+cudaError_t launch_expr_w(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
+    switch (c.strategy) {
+    case BH_STRATEGY_PRIV:
+        if constexpr (W) {
+            if (p.replicas > 1) return launch_expr_s<DIM, W, SINK_PRIVA>(p, e, c, s);
+        }
+        return launch_expr_s<DIM, W, SINK_PRIV>(p, e, c, s);
+    case BH_STRATEGY_CACHE: return launch_expr_s<DIM, W, SINK_CACHE>(p, e, c, s);
+    default: return launch_expr_s<DIM, W, SINK_GLOBAL>(p, e, c, s);
+    }
+}
+
+template <int DIM>
+cudaError_t launch_expr(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
+    return c.weighted ? launch_expr_w<DIM, true>(p, e, c, s) : launch_expr_w<DIM, false>(p, e, c, s);
 }
 
 bh_status check_hist(const bh_hist *h) {
@@ -651,6 +696,63 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
             CUDA_TRY(cudaGetLastError());
             hs[pass[0]]->launches++;      // one launch, counted once
         }
+    }
+    return BH_OK;
+}
+
+bh_status bh_fill_expr(bh_hist *h, int64_t n, const double *const *cols, int32_t ncols, const bh_op *prog,
+                       int32_t nops, const int32_t *axis_reg, int32_t weight_reg, int32_t filter_reg, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (n < 0) return fail(BH_EINVAL, "n < 0");
+    if (ncols < 0 || ncols > kExprRegs) return fail(BH_EINVAL, "need 0..%d columns", kExprRegs);
+    if (nops < 0 || nops > kExprOps) return fail(BH_EINVAL, "need 0..%d ops", kExprOps);
+    if (nops > 0 && !prog) return fail(BH_EINVAL, "prog is NULL");
+    if (!axis_reg) return fail(BH_EINVAL, "axis_reg is NULL");
+    if (ncols > 0 && !cols) return fail(BH_EINVAL, "cols is NULL");
+    for (int c = 0; c < ncols; ++c)
+        if (!cols[c]) return fail(BH_EINVAL, "cols[%d] is NULL", c);
+    auto reg_ok = [](int r) { return r >= 0 && r < kExprRegs; };
+    ExprP e{};
+    e.ncols = ncols;
+    e.nops = nops;
+    for (int k = 0; k < nops; ++k) {
+        const bh_op &o = prog[k];
+        if (o.op < 0 || o.op >= EX_COUNT) return fail(BH_EINVAL, "op %d: unknown opcode %d", k, o.op);
+        if (!reg_ok(o.dst) || !reg_ok(o.a) || !reg_ok(o.b) || !reg_ok(o.c))
+            return fail(BH_EINVAL, "op %d: register out of range [0,%d)", k, kExprRegs);
+        e.ins[k] = ExprIns{o.op, o.dst, o.a, o.b, o.c, 0, o.imm};
+    }
+    for (int a = 0; a < h->dim; ++a) {
+        if (!reg_ok(axis_reg[a])) return fail(BH_EINVAL, "axis_reg[%d] out of range", a);
+        e.axis_reg[a] = axis_reg[a];
+    }
+    if (weight_reg >= kExprRegs || filter_reg >= kExprRegs) return fail(BH_EINVAL, "register out of range");
+    e.weight_reg = weight_reg < 0 ? -1 : weight_reg;
+    e.filter_reg = filter_reg < 0 ? -1 : filter_reg;
+    if (n == 0) return BH_OK;
+    DeviceGuard dg(h->device);
+    FillPlan pl;
+    if (bh_status r = plan_fill(h, e.weight_reg >= 0, pl)) return r;
+    LaunchCfg &c = pl.c;
+    const int64_t kMaxLaunch = int64_t(1) << 30;
+    for (int64_t off = 0; off < n; off += kMaxLaunch) {
+        const int64_t m = std::min(kMaxLaunch, n - off);
+        for (int k = 0; k < ncols; ++k) e.cols[k] = cols[k] + off;
+        const double *none[kMaxDim] = {};
+        FillP p = make_params(h, m, none, nullptr);
+        for (int a = 0; a < h->dim; ++a) p.ax[a] = pl.ax[a];
+        p.entries_add = 0;                 // the kernel adds the passing events itself
+        p.cache_slots = cache_slots_for(c.weighted);
+        p.replicas = pl.replicas;
+        c.grid = grid_for(h, c, m);
+        cudaError_t r;
+        switch (h->dim) {
+        case 1: r = launch_expr<1>(p, e, c, static_cast<cudaStream_t>(s)); break;
+        case 2: r = launch_expr<2>(p, e, c, static_cast<cudaStream_t>(s)); break;
+        default: r = launch_expr<3>(p, e, c, static_cast<cudaStream_t>(s)); break;
+        }
+        if (r != cudaSuccess) return fail(BH_ECUDA, "fill_expr launch: %s", cudaGetErrorString(r));
+        ++h->launches;
     }
     return BH_OK;
 }

@@ -630,6 +630,100 @@ __global__ void __launch_bounds__((ThreadsOf<SINK, W>::v), SINK == SINK_GLOBAL ?
     block_stats_finish<Acc<DIM, W>::K>(p, acc.s);
 }
 
+// ------------------------------------------------------------------ fused Filter + Define (NEXT-1)
+// RDataFrame's own example filters events and defines a derived column
+// before the histogram action.  Instead of materializing the derived column (a write and
+// a re-read of 8 B/event), a short register program runs inside the fill: r[0..ncols) hold
+// the event's columns, each op writes one register, then the axes read r[axis_reg[a]],
+// the weight r[weight_reg] and the event passes iff r[filter_reg] != 0.  Only IEEE
+// correctly-rounded operations exist (+ - * / sqrt, comparisons, min/max, logic), so a
+// derived coordinate is bit-identical to the same expression evaluated anywhere.
+constexpr int kExprRegs = 16;
+constexpr int kExprOps = 32;
+enum ExprOp : int32_t {
+    EX_CONST = 0, EX_COPY, EX_ADD, EX_SUB, EX_MUL, EX_DIV, EX_SQRT, EX_ABS, EX_NEG, EX_MIN, EX_MAX,
+    EX_LT, EX_LE, EX_GT, EX_GE, EX_EQ, EX_NE, EX_AND, EX_OR, EX_NOT, EX_SELECT, EX_COUNT
+};
+struct ExprIns { int32_t op, dst, a, b, c, pad; double imm; };
+struct ExprP {
+    int32_t ncols, nops, weight_reg, filter_reg;
+    int32_t axis_reg[kMaxDim];
+    const double *cols[kExprRegs];
+    ExprIns ins[kExprOps];
+};
+
+__device__ __forceinline__ void run_expr(const ExprP &e, double (&r)[kExprRegs]) {
+    for (int k = 0; k < e.nops; ++k) {          // uniform across the warp: no divergence
+        const ExprIns I = e.ins[k];
+        const double a = r[I.a], b = r[I.b];
+        double v;
+        switch (I.op) {
+        case EX_CONST: v = I.imm; break;
+        case EX_COPY: v = a; break;
+        case EX_ADD: v = __dadd_rn(a, b); break;
+        case EX_SUB: v = __dsub_rn(a, b); break;
+        case EX_MUL: v = __dmul_rn(a, b); break;
+        case EX_DIV: v = __ddiv_rn(a, b); break;
+        case EX_SQRT: v = __dsqrt_rn(a); break;
+        case EX_ABS: v = fabs(a); break;
+        case EX_NEG: v = -a; break;
+        case EX_MIN: v = fmin(a, b); break;
+        case EX_MAX: v = fmax(a, b); break;
+        case EX_LT: v = a < b; break;
+        case EX_LE: v = a <= b; break;
+        case EX_GT: v = a > b; break;
+        case EX_GE: v = a >= b; break;
+        case EX_EQ: v = a == b; break;
+        case EX_NE: v = a != b; break;
+        case EX_AND: v = (a != 0.0) && (b != 0.0); break;
+        case EX_OR: v = (a != 0.0) || (b != 0.0); break;
+        case EX_NOT: v = !(a != 0.0); break;
+        default: v = (a != 0.0) ? b : r[I.c]; break;   // EX_SELECT
+        }
+        r[I.dst] = v;
+    }
+}
+
+// Same sinks and stats as k_fill; entries += number of events that pass the filter.
+template <int DIM, bool W, int SINK, bool VSM>
+__global__ void __launch_bounds__(ThreadsOf<SINK, W>::v, SINK == SINK_GLOBAL ? 2 : 1)
+    k_fill_expr(FillP p, const __grid_constant__ ExprP e) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    using Sink_t = typename SinkOf<SINK, W>::T;
+    Sink_t sink;
+    if constexpr (SINK == SINK_GLOBAL || SINK == SINK_CACHE) sink.pp = &p;
+    if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
+    else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas);
+    else sink.init(smem, p.G);
+    if constexpr (VSM) stage_axes<DIM>(p.ax, smem);
+    if constexpr (SINK != SINK_GLOBAL || VSM) __syncthreads();
+    Acc<DIM, W> acc;
+    acc.zero();
+    unsigned int passed = 0;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += nth) {
+        double r[kExprRegs];
+#pragma unroll
+        for (int c = 0; c < kExprRegs; ++c) r[c] = c < e.ncols ? __ldcs(e.cols[c] + i) : 0.0;
+        run_expr(e, r);
+        if (e.filter_reg >= 0 && !(r[e.filter_reg] != 0.0)) continue;   // Filter
+        ++passed;
+        double x[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) x[a] = r[e.axis_reg[a]];
+        do_event<DIM, W, VSM>(p, x, W ? r[e.weight_reg] : 1.0, sink, acc, smem);
+    }
+    // entries: passing events (order-independent integer adds)
+    for (int o = 16; o > 0; o >>= 1) passed += __shfl_xor_sync(0xffffffffu, passed, o);
+    if ((threadIdx.x & 31) == 0 && passed) atomicAdd(p.entries, (unsigned long long)passed);
+    if constexpr (SINK != SINK_GLOBAL) {
+        __syncthreads();
+        sink.flush(p, smem);
+    }
+    acc.finalize_unit();
+    block_stats_finish<Acc<DIM, W>::K>(p, acc.s);   // p.entries_add == 0 here
+}
+
 // ------------------------------------------------------------------ fused multi-histogram fill (C5)
 // One pass over a set of columns feeding several histograms (the paper's future
 // work "multiple histograms from different columns in one pass"; RDataFrame

@@ -339,3 +339,18 @@ def test_cauchy_c4_shape():
     pc = sst.cauchy.cdf(0.51, 0.505, 0.002) - sst.cauchy.cdf(0.5, 0.505, 0.002)
     hot = r["content"].max() / wl.n_events
     assert abs(hot - pc ** 3) < 5 * math.sqrt(pc ** 3 / wl.n_events)
+
+
+# ------------------------------------------------------------------ Filter + Define oracle
+def test_expr_oracle_hand_values():
+    from oracle import expr
+    x = np.array([3.0, -1.0, 0.5, np.nan])
+    y = np.array([4.0, 2.0, 0.5, 1.0])
+    prog = [("mul", 2, 0, 0, 0, 0.0), ("mul", 3, 1, 1, 0, 0.0), ("add", 4, 2, 3, 0, 0.0), ("sqrt", 5, 4, 0, 0, 0.0),
+            ("const", 6, 0, 0, 0, 0.0), ("gt", 7, 0, 6, 0, 0.0)]
+    r = expr.run_program([x, y], prog, 4)
+    assert r[5][0] == 5.0 and r[5][1] == np.sqrt(5.0) and r[5][2] == np.sqrt(0.5)
+    assert list(r[7][:3]) == [1.0, 0.0, 1.0] and r[7][3] == 0.0          # NaN > 0 is false
+    h = expr.fill_expr([(10, 0.0, 10.0)], [x, y], prog, [5], filter_reg=7)
+    out = h.read()
+    assert out["entries"] == 2 and out["content"][6] == 1.0 and out["content"][1] == 1.0   # r=5 -> bin 6

@@ -419,3 +419,43 @@ def test_single_fill_above_2_31_events():
     del xd
     ref = oracle_parallel("C1", n)
     compare(got, ref, False, "2^31+5")
+
+
+# ------------------------------------------------------------------ fused Filter + Define (NEXT-1)
+@pytest.mark.parametrize("strategy", [pkg.BH_STRATEGY_AUTO, pkg.BH_STRATEGY_GLOBAL, pkg.BH_STRATEGY_CACHE])
+def test_fill_expr_filter_define(strategy):
+    from oracle import expr
+    rng = np.random.default_rng(5)
+    n = 1_000_003
+    x, y = rng.normal(0, 1, n), rng.normal(0, 1, n)
+    w = rng.uniform(0.5, 1.5, n)
+    x[::997] = np.nan
+    P = pkg.Program(3)                     # r0 = x, r1 = y, r2 = w
+    xx = P.mul(0, 0)
+    yy = P.mul(1, 1)
+    r = P.sqrt(P.add(xx, yy))              # Define("r", "sqrt(x*x+y*y)")
+    cut = P.land(P.gt(0, P.const(-0.5)), P.lt(1, P.const(1.2)))   # Filter("x > -0.5 && y < 1.2")
+    ww = P.mul(2, P.max(0, P.const(0.0)))  # weight = w * max(x, 0)
+    cols = [_t(x), _t(y), _t(w)]
+    for axes, regs, wreg in [([(100, 0.0, 3.0)], [r], -1), ([np.linspace(0, 3, 51) ** 1.5], [r], ww),
+                             ([(40, 0.0, 3.0), (30, -1.0, 1.5)], [r, 1], 2)]:
+        h = pkg.Histogram(axes, strategy=strategy)
+        pkg.fill_expr(h, cols, P, regs, wreg, cut)
+        ref = expr.fill_expr(axes, [x, y, w], P.ops, regs, wreg, cut).read()
+        compare(h.read(), ref, wreg >= 0, f"expr {axes}")
+        h.close()
+
+
+def test_fill_expr_identity_equals_fill():
+    wl = bhgen.workload("C2", 500_001)
+    hist = wl.hists[0]
+    cols, w = gen_columns(wl, hist, 0, wl.n_events)
+    a = pkg.Histogram(oracle.oracle_axes(hist))
+    a.fill([_t(cols[0])], _t(w))
+    b = pkg.Histogram(oracle.oracle_axes(hist))
+    pkg.fill_expr(b, [_t(cols[0]), _t(w)], pkg.Program(2), [0], 1, -1)
+    ra, rb = a.read(), b.read()
+    assert ra["entries"] == rb["entries"]
+    np.testing.assert_allclose(ra["content"], rb["content"], rtol=1e-12, atol=0)
+    a.close()
+    b.close()

@@ -161,7 +161,7 @@ cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
         if (e != cudaSuccess) return e;
     }
-    kern<<<c.grid, ThreadsOf<SINK, W>::v, c.smem, s>>>(p);
+    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -291,7 +291,7 @@ cudaError_t launch_expr_s(const FillP &p, const ExprP &e, const LaunchCfg &c, cu
         cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
         if (r != cudaSuccess) return r;
     }
-    kern<<<c.grid, ThreadsOf<SINK, W>::v, c.smem, s>>>(p, e);
+    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p, e);
     return cudaGetLastError();
 }
 
@@ -504,7 +504,6 @@ bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const
         if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
     DeviceGuard dg(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(s);
-    const int ncol = h->dim + (w ? 1 : 0);
     // lazily create the copy stream, events and the device double buffer
     if (!h->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
     if (h->stage_chunk != h->chunk) {
@@ -547,7 +546,6 @@ bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const
         if (r != BH_OK) return r;
         CUDA_TRY(cudaEventRecord(h->consumed[slot], st));
     }
-    (void)ncol;
     // every host byte has been read once the last copy has completed
     CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
     return BH_OK;

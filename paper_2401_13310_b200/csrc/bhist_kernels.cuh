@@ -17,7 +17,7 @@ namespace bh {
 constexpr int kMaxDim = 3;
 constexpr int kThreadsGlobal = 512;   // GLOBAL sink: 2 CTAs/SM
 constexpr int kThreadsSmem = 1024;    // PRIV / CACHE sinks: 1 CTA/SM owns the SM's shared memory
-template <int SINK, bool W = false> struct ThreadsOf {
+template <int SINK> struct ThreadsOf {   // SINK_GLOBAL == 1
     static constexpr int v = SINK == 1 ? kThreadsGlobal : kThreadsSmem;
 };
 
@@ -543,7 +543,7 @@ struct Batch {            // U event pairs of every column, held in registers (x
 // leading events; the next batch is loaded before the current one is processed
 // (register double-buffering) so each thread keeps 2*U*ncol 16-byte loads in flight.
 template <int DIM, bool W, int SINK, bool VEC, bool VSM>
-__global__ void __launch_bounds__((ThreadsOf<SINK, W>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
+__global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Sink_t = typename SinkOf<SINK, W>::T;
     Sink_t sink;
@@ -686,7 +686,7 @@ __device__ __forceinline__ void run_expr(const ExprP &e, double (&r)[kExprRegs])
 
 // Same sinks and stats as k_fill; entries += number of events that pass the filter.
 template <int DIM, bool W, int SINK, bool VSM>
-__global__ void __launch_bounds__(ThreadsOf<SINK, W>::v, SINK == SINK_GLOBAL ? 2 : 1)
+__global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 1)
     k_fill_expr(FillP p, const __grid_constant__ ExprP e) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Sink_t = typename SinkOf<SINK, W>::T;
@@ -737,7 +737,6 @@ __global__ void __launch_bounds__(ThreadsOf<SINK, W>::v, SINK == SINK_GLOBAL ? 2
 // (acc[stat][thread], conflict-free), since up to 8 x 11 sums do not fit in registers.
 constexpr int kMaxHist = 8;
 constexpr int kMaxCols = 8;
-constexpr int kMultiStats = 96;          // >= sum of K over the histograms (<= 8 * 11 = 88)
 constexpr int kMultiThreads = 1024;
 
 struct MultiH {

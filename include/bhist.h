@@ -77,6 +77,13 @@ typedef struct {
 #define BH_STRATEGY_PRIV 1
 #define BH_STRATEGY_GLOBAL 2
 #define BH_STRATEGY_CACHE 3
+/* EXACT  weighted fills of bh_fill / bh_fill_host / bh_fill_multi (solo passes) add
+ *        each launch's per-bin sums of w and w*w as exact scaled-integer sums (int64
+ *        limbs, order independent) rounded once: bitwise reproducible run to run, and
+ *        the correctly rounded sum whenever the weights lie within 2^43 of the launch's
+ *        max|w|.  Unit-weight fills are exact in every mode;
+ *        bh_fill_expr uses AUTO.  Slower (six L2 integer atomics per event). */
+#define BH_STRATEGY_EXACT 4
 
 /* Debug flags (bh_set_debug) — negative controls for tests only. */
 #define BH_DEBUG_SKIP_COPY_WAIT 1 /* bh_fill_host: fill without waiting for the H2D copy (PAPER.md:223 race) */

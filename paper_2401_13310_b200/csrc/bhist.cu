@@ -80,6 +80,8 @@ struct bh_hist {
     unsigned long long *entries = nullptr;
     double *partials = nullptr;
     unsigned int *counter = nullptr;
+    long long *limbs = nullptr;       // EXACT: per bin 2 x 3 int64 limbs (sumw, sumw2), zero between fills
+    unsigned long long *maxbits = nullptr;   // EXACT: bit pattern of max|w| of the current launch
     double *pack_buf = nullptr;       // device buffer for bh_read
     double *pack_host = nullptr;      // pinned host buffer for bh_read
     std::vector<void *> axis_mem;     // edges and guide tables
@@ -99,7 +101,8 @@ constexpr size_t kStaticSmemReserve = 4096;   // block_stats_finish scratch + dr
 // AUTO: privatize the bins in shared memory whenever they fit next to the reserve
 // (variable-axis tables then go to smem only if they also fit); otherwise CACHE.
 int resolve_strategy(const bh_hist *h, bool weighted) {
-    if (h->strategy != BH_STRATEGY_AUTO) return h->strategy;
+    // EXACT only changes weighted fills of bh_fill / bh_fill_host (fill_exact below)
+    if (h->strategy != BH_STRATEGY_AUTO && h->strategy != BH_STRATEGY_EXACT) return h->strategy;
     const size_t priv = (weighted ? 16 : 4) * (size_t)h->G;
     if (priv + kStaticSmemReserve <= h->smem_optin) return BH_STRATEGY_PRIV;
     // large bin spaces: shared-memory cache of the hottest bins in front of L2 atomics
@@ -249,8 +252,42 @@ int grid_for(const bh_hist *h, const LaunchCfg &c, int64_t m) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)h->nsm * resident_blocks(c.strategy)));
 }
 
+// EXACT weighted fill: max|w| -> integer-limb RED.64 fill -> fold (see k_fill_exact).
+bh_status fill_exact(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
+    if (!h->limbs) {
+        if (cudaMalloc(reinterpret_cast<void **>(&h->limbs), sizeof(long long) * 6 * h->G) != cudaSuccess ||
+            cudaMalloc(reinterpret_cast<void **>(&h->maxbits), sizeof(unsigned long long)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(BH_ENOMEM, "exact-mode limbs allocation failed");
+        }
+        CUDA_TRY(cudaMemsetAsync(h->limbs, 0, sizeof(long long) * 6 * h->G, s));
+    }
+    const int64_t kMaxLaunch = int64_t(1) << 30;   // limb sums stay below 2^62
+    for (int64_t off = 0; off < n; off += kMaxLaunch) {
+        const int64_t m = std::min(kMaxLaunch, n - off);
+        const double *cs[kMaxDim] = {};
+        for (int a = 0; a < h->dim; ++a) cs[a] = coords[a] + off;
+        FillP p = make_params(h, m, cs, w + off);
+        CUDA_TRY(cudaMemsetAsync(h->maxbits, 0, sizeof(unsigned long long), s));
+        const int g1 = (int)std::min<int64_t>((m + 255) / 256, (int64_t)h->nsm * 8);
+        k_wmax<<<g1, 256, 0, s>>>(w + off, m, h->maxbits);
+        const int g2 = (int)std::min<int64_t>((m + 511) / 512, (int64_t)h->nsm * 2);
+        switch (h->dim) {
+        case 1: k_fill_exact<1><<<g2, 512, 0, s>>>(p, h->limbs, h->maxbits); break;
+        case 2: k_fill_exact<2><<<g2, 512, 0, s>>>(p, h->limbs, h->maxbits); break;
+        default: k_fill_exact<3><<<g2, 512, 0, s>>>(p, h->limbs, h->maxbits); break;
+        }
+        const int g3 = (int)std::min<int64_t>((h->G + 255) / 256, (int64_t)h->nsm * 8);
+        k_exact_fold<<<g3, 256, 0, s>>>((int)h->G, h->limbs, h->maxbits, h->sumw, h->sumw2);
+        CUDA_TRY(cudaGetLastError());
+        h->launches += 3;
+    }
+    return BH_OK;
+}
+
 // One fill over device-resident columns, split into launches of <= 2^30 events.
 bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
+    if (w && h->strategy == BH_STRATEGY_EXACT) return fill_exact(h, n, coords, w, s);
     FillPlan pl;
     if (bh_status r = plan_fill(h, w != nullptr, pl)) return r;
     LaunchCfg &c = pl.c;
@@ -459,6 +496,8 @@ bh_status bh_destroy(bh_hist *h) {
     cudaFree(h->entries);
     cudaFree(h->partials);
     cudaFree(h->counter);
+    cudaFree(h->limbs);
+    cudaFree(h->maxbits);
     cudaFree(h->pack_buf);
     if (h->pack_host) cudaFreeHost(h->pack_host);
     for (void *p : h->axis_mem) cudaFree(p);
@@ -601,7 +640,8 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
         for (int a = 0; a < H->dim; ++a) key.push_back(col_of_axis[3 * i + a]);
         std::sort(key.begin(), key.end());
         key.push_back(weighted[i] ? 1 : 0);
-        if (b > kFuseLimit || fuse_off) solo.push_back(i); else small.push_back({i, b, key});
+        const bool exact = weighted[i] && H->strategy == BH_STRATEGY_EXACT;
+        if (b > kFuseLimit || fuse_off || exact) solo.push_back(i); else small.push_back({i, b, key});
     }
     std::stable_sort(small.begin(), small.end(), [](const Cand &x, const Cand &y) {
         return x.key != y.key ? x.key < y.key : x.bytes < y.bytes; });
@@ -835,7 +875,7 @@ bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *sta
 
 bh_status bh_set_strategy(bh_hist *h, int32_t strategy) {
     if (check_hist(h)) return BH_EINVAL;
-    if (strategy < BH_STRATEGY_AUTO || strategy > BH_STRATEGY_CACHE) return fail(BH_EINVAL, "unknown strategy %d", strategy);
+    if (strategy < BH_STRATEGY_AUTO || strategy > BH_STRATEGY_EXACT) return fail(BH_EINVAL, "unknown strategy %d", strategy);
     if (strategy == BH_STRATEGY_PRIV && 4 * (size_t)h->G + kStaticSmemReserve > h->smem_optin)
         return fail(BH_EINVAL, "PRIV cannot hold %lld bins in shared memory", (long long)h->G);
     h->strategy = strategy;
@@ -845,7 +885,7 @@ bh_status bh_set_strategy(bh_hist *h, int32_t strategy) {
 bh_status bh_get_strategy(const bh_hist *h, int32_t weighted, int32_t *strategy) {
     if (check_hist(h)) return BH_EINVAL;
     if (!strategy) return fail(BH_EINVAL, "NULL output");
-    *strategy = resolve_strategy(h, weighted != 0);
+    *strategy = (weighted && h->strategy == BH_STRATEGY_EXACT) ? BH_STRATEGY_EXACT : resolve_strategy(h, weighted != 0);
     return BH_OK;
 }
 

@@ -724,6 +724,89 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
     block_stats_finish<Acc<DIM, W>::K>(p, acc.s);   // p.entries_add == 0 here
 }
 
+// ------------------------------------------------------------------ exact, deterministic weighted mode (NEXT-3)
+// Per launch: E = exponent of max|w| (finite weights), then every weight becomes the
+// integer m = RN(w * 2^(96-E)) (|m| < 2^96; exact unless |w| < 2^(E-43)), split into
+// three signed 32-bit chunks added with integer RED.64 into per-bin int64 limbs -- order
+// independent, so the per-bin sums are bitwise reproducible -- and the limbs are folded
+// back once per launch: sumw[g] += RN(sum m) * 2^(E-96), the correctly rounded value of
+// the exact sum of the scaled weights.  Same for w*w with its own exponent.  A launch
+// has <= 2^30 events, so a limb never exceeds 2^30 * 2^32 = 2^62.  Non-finite weights
+// take the ordinary float64 atomics (NaN/inf propagate as in any float sum).
+__global__ void k_wmax(const double *__restrict__ w, int64_t n, unsigned long long *maxbits) {
+    unsigned long long m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double a = fabs(w[i]);
+        if (a <= 1.7976931348623157e308) m = max(m, (unsigned long long)__double_as_longlong(a));   // finite
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(maxbits, m);      // |w| bit patterns order like values
+}
+
+__device__ __forceinline__ int exact_exp(unsigned long long maxbits) {   // max|w| < 2^E
+    int e = 0;
+    if (maxbits) frexp(__longlong_as_double((long long)maxbits), &e);
+    return e;
+}
+
+__device__ __forceinline__ void red_exact(long long *limb, double v, int e) {   // limb[0..2] += chunks(v*2^(96-e))
+    const double m = ldexp(v, 96 - e);
+    const double hi = trunc(ldexp(m, -64));
+    const double r1 = m - ldexp(hi, 64);            // exact: low part of m's binary expansion
+    const double mid = trunc(ldexp(r1, -32));
+    const double lo = rint(r1 - ldexp(mid, 32));    // the only rounding (weights < 2^(e-43))
+    atomicAdd(reinterpret_cast<unsigned long long *>(limb), (unsigned long long)(long long)lo);
+    atomicAdd(reinterpret_cast<unsigned long long *>(limb + 1), (unsigned long long)(long long)mid);
+    atomicAdd(reinterpret_cast<unsigned long long *>(limb + 2), (unsigned long long)(long long)hi);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(512, 2) k_fill_exact(FillP p, long long *limbs, const unsigned long long *maxbits) {
+    const int e1 = exact_exp(*maxbits);
+    const int e2 = 2 * e1 + 1;                      // max RN(w*w) < 2^(2 e1) <= 2^e2
+    Acc<DIM, true> acc;
+    acc.zero();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
+        double x[DIM];
+        int g = 0, mul = 1;
+        bool inr = true;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            x[a] = __ldcs(p.x[a] + i);
+            const int b = find_bin(p.ax[a], x[a]);
+            inr &= (b >= 1) & (b <= p.ax[a].n);
+            g += b * mul;
+            if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
+        }
+        const double w = __ldcs(p.w + i), w2 = w * w;
+        if (fabs(w) <= 1.7976931348623157e308 && fabs(w2) <= 1.7976931348623157e308) {
+            red_exact(limbs + 6 * (size_t)g, w, e1);
+            red_exact(limbs + 6 * (size_t)g + 3, w2, e2);
+        } else {
+            atomicAdd(p.sumw + g, w);
+            atomicAdd(p.sumw2 + g, w2);
+        }
+        if (inr) acc.add(x, w);
+    }
+    block_stats_finish<Acc<DIM, true>::K>(p, acc.s);
+}
+
+__device__ __forceinline__ double fold_limbs(long long *l, int e) {
+    const __int128 v = (__int128)l[0] + ((__int128)l[1] << 32) + ((__int128)l[2] << 64);
+    l[0] = l[1] = l[2] = 0;
+    return ldexp((double)v, e - 96);
+}
+
+__global__ void k_exact_fold(int G, long long *limbs, const unsigned long long *maxbits, double *sumw, double *sumw2) {
+    const int e1 = exact_exp(*maxbits), e2 = 2 * e1 + 1;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+        long long *l = limbs + 6 * (size_t)g;
+        if (l[0] | l[1] | l[2]) sumw[g] += fold_limbs(l, e1);
+        if (l[3] | l[4] | l[5]) sumw2[g] += fold_limbs(l + 3, e2);
+    }
+}
+
 // ------------------------------------------------------------------ fused multi-histogram fill (C5)
 // One pass over a set of columns feeding several histograms (the paper's future
 // work "multiple histograms from different columns in one pass"; RDataFrame

@@ -459,3 +459,63 @@ def test_fill_expr_identity_equals_fill():
     np.testing.assert_allclose(ra["content"], rb["content"], rtol=1e-12, atol=0)
     a.close()
     b.close()
+
+
+# ------------------------------------------------------------------ exact, deterministic weighted mode (NEXT-3)
+@pytest.mark.parametrize("name", ["C2", "C3W", "C4W"])
+def test_exact_mode_parity_and_reproducible(name):
+    wl = bhgen.workload(name, 1_000_003)
+    hist = wl.hists[0]
+    axes = oracle.oracle_axes(hist)
+    cols, w = gen_columns(wl, hist, 0, wl.n_events)
+    ref = oracle.OracleHist(axes).fill(cols, w).read()
+    a = _gpu_fill(axes, cols, w, pkg.BH_STRATEGY_EXACT)
+    b = _gpu_fill(axes, cols, w, pkg.BH_STRATEGY_EXACT)
+    compare(a, ref, True, f"exact {name}")
+    assert np.array_equal(a["content"], b["content"]) and np.array_equal(a["sumw2"], b["sumw2"])
+    assert np.array_equal(a["stats"], b["stats"])
+    # the oracle's compensated sums are within ~1 ulp of exact: exact mode must be too
+    nz = ref["content"] != 0
+    rel = np.abs(a["content"][nz] - ref["content"][nz]) / np.abs(ref["content"][nz])
+    assert rel.max() <= 4e-16
+
+
+def test_exact_mode_is_correctly_rounded_sum():
+    """Weights k * 2^-30 (k integer): the per-bin sums are then exact rationals we can form
+    with Python integers; exact mode must return exactly their correctly rounded doubles,
+    for sum(w) and for sum(RN(w*w))."""
+    from fractions import Fraction
+    rng = np.random.default_rng(77)
+    n = 400_001
+    x = rng.uniform(0, 1, n)
+    k = rng.integers(2 ** 29, 3 * 2 ** 29, n)
+    w = k.astype(np.float64) * 2.0 ** -30
+    w[::5] *= -1.0
+    axes = [(50, 0.0, 1.0)]
+    got = _gpu_fill(axes, [x], w, pkg.BH_STRATEGY_EXACT)
+    bins = oracle.OracleHist(axes).find_bins([x])
+    ww = w * w
+    for g in range(52):
+        sel = bins == g
+        s1 = sum((Fraction(float(v)) for v in w[sel]), Fraction(0))
+        s2 = sum((Fraction(float(v)) for v in ww[sel]), Fraction(0))
+        assert got["content"][g] == float(s1), g
+        assert got["sumw2"][g] == float(s2), g
+
+
+def test_exact_mode_nonfinite_weights_and_accumulation():
+    rng = np.random.default_rng(3)
+    n = 100_000
+    x = rng.uniform(0, 1, n)
+    w = rng.uniform(0.5, 1.5, n)
+    w[17] = np.inf
+    h = pkg.Histogram([(10, 0.0, 1.0)], strategy=pkg.BH_STRATEGY_EXACT)
+    h.fill([_t(x)], _t(w))
+    h.fill([_t(x)], _t(np.ones(n)))                    # second weighted fill accumulates
+    r = h.read()
+    b = int(x[17] * 10) + 1
+    assert np.isinf(r["content"][b]) and np.isfinite(np.delete(r["content"], b)).all()
+    ref = oracle.OracleHist([(10, 0.0, 1.0)]).fill([np.delete(x, 17)], np.delete(w, 17)).fill([x], np.ones(n)).read()
+    other = np.arange(12) != b
+    assert np.all(np.abs(r["content"][other] - ref["content"][other]) <= 1e-12 * ref["abs_content"][other])
+    h.close()

@@ -80,7 +80,7 @@ struct bh_hist {
     unsigned long long *entries = nullptr;
     double *partials = nullptr;
     unsigned int *counter = nullptr;
-    long long *limbs = nullptr;       // EXACT: per bin 2 x 3 int64 limbs (sumw, sumw2), zero between fills
+    long long *limbs = nullptr;       // EXACT: per bin 2 x kLimbs int64 limbs (sumw, sumw2), zero between fills
     unsigned long long *maxbits = nullptr;   // EXACT: bit pattern of max|w| of the current launch
     double *pack_buf = nullptr;       // device buffer for bh_read
     double *pack_host = nullptr;      // pinned host buffer for bh_read
@@ -255,14 +255,14 @@ int grid_for(const bh_hist *h, const LaunchCfg &c, int64_t m) {
 // EXACT weighted fill: max|w| -> integer-limb RED.64 fill -> fold (see k_fill_exact).
 bh_status fill_exact(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
     if (!h->limbs) {
-        if (cudaMalloc(reinterpret_cast<void **>(&h->limbs), sizeof(long long) * 6 * h->G) != cudaSuccess ||
+        if (cudaMalloc(reinterpret_cast<void **>(&h->limbs), sizeof(long long) * 2 * kLimbs * h->G) != cudaSuccess ||
             cudaMalloc(reinterpret_cast<void **>(&h->maxbits), sizeof(unsigned long long)) != cudaSuccess) {
             cudaGetLastError();
             return fail(BH_ENOMEM, "exact-mode limbs allocation failed");
         }
-        CUDA_TRY(cudaMemsetAsync(h->limbs, 0, sizeof(long long) * 6 * h->G, s));
+        CUDA_TRY(cudaMemsetAsync(h->limbs, 0, sizeof(long long) * 2 * kLimbs * h->G, s));
     }
-    const int64_t kMaxLaunch = int64_t(1) << 30;   // limb sums stay below 2^62
+    const int64_t kMaxLaunch = int64_t(1) << 30;   // limb sums stay below 2^54
     for (int64_t off = 0; off < n; off += kMaxLaunch) {
         const int64_t m = std::min(kMaxLaunch, n - off);
         const double *cs[kMaxDim] = {};

@@ -726,13 +726,17 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
 
 // ------------------------------------------------------------------ exact, deterministic weighted mode (NEXT-3)
 // Per launch: E = exponent of max|w| (finite weights), then every weight becomes the
-// integer m = RN(w * 2^(96-E)) (|m| < 2^96; exact unless |w| < 2^(E-43)), split into
-// three signed 32-bit chunks added with integer RED.64 into per-bin int64 limbs -- order
-// independent, so the per-bin sums are bitwise reproducible -- and the limbs are folded
-// back once per launch: sumw[g] += RN(sum m) * 2^(E-96), the correctly rounded value of
-// the exact sum of the scaled weights.  Same for w*w with its own exponent.  A launch
-// has <= 2^30 events, so a limb never exceeds 2^30 * 2^32 = 2^62.  Non-finite weights
-// take the ordinary float64 atomics (NaN/inf propagate as in any float sum).
+// integer m = RN(w * 2^(96-E)) (|m| < 2^96; exact unless |w| < 2^(E-43)), split into four
+// signed 24-bit chunks.  Lanes of a warp holding the same bin sum their chunks exactly
+// with __reduce_add_sync (|group sum| < 2^29), and the group leader adds them with integer
+// RED.64 into per-bin int64 limbs (weights 2^0, 2^24, 2^48, 2^72) -- order independent, so
+// the per-bin sums are bitwise reproducible -- and the limbs are folded back once per
+// launch: sumw[g] += RN(sum m) * 2^(E-96), the correctly rounded value of the exact sum
+// of the scaled weights.  Same for w*w with its own exponent.  A launch has <= 2^30
+// events, so a limb stays below 2^54.  Non-finite weights take the ordinary float64
+// atomics (NaN/inf propagate as in any float sum).
+constexpr int kLimbs = 4;                      // per quantity; 8 per bin (sumw, sumw2)
+
 __global__ void k_wmax(const double *__restrict__ w, int64_t n, unsigned long long *maxbits) {
     unsigned long long m = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -750,15 +754,16 @@ __device__ __forceinline__ int exact_exp(unsigned long long maxbits) {   // max|
     return e;
 }
 
-__device__ __forceinline__ void red_exact(long long *limb, double v, int e) {   // limb[0..2] += chunks(v*2^(96-e))
-    const double m = ldexp(v, 96 - e);
-    const double hi = trunc(ldexp(m, -64));
-    const double r1 = m - ldexp(hi, 64);            // exact: low part of m's binary expansion
-    const double mid = trunc(ldexp(r1, -32));
-    const double lo = rint(r1 - ldexp(mid, 32));    // the only rounding (weights < 2^(e-43))
-    atomicAdd(reinterpret_cast<unsigned long long *>(limb), (unsigned long long)(long long)lo);
-    atomicAdd(reinterpret_cast<unsigned long long *>(limb + 1), (unsigned long long)(long long)mid);
-    atomicAdd(reinterpret_cast<unsigned long long *>(limb + 2), (unsigned long long)(long long)hi);
+// the four signed 24-bit chunks of RN(v * 2^(96-e)), low first
+__device__ __forceinline__ void exact_chunks(double v, int e, int (&c)[kLimbs]) {
+    double r = ldexp(v, 96 - e);
+#pragma unroll
+    for (int k = kLimbs - 1; k >= 1; --k) {
+        const double hk = trunc(ldexp(r, -24 * k));
+        r -= ldexp(hk, 24 * k);                  // exact: removes the top bits of r's expansion
+        c[k] = (int)hk;
+    }
+    c[0] = (int)rint(r);                         // the only rounding (weights < 2^(e-43))
 }
 
 template <int DIM>
@@ -767,25 +772,50 @@ __global__ void __launch_bounds__(512, 2) k_fill_exact(FillP p, long long *limbs
     const int e2 = 2 * e1 + 1;                      // max RN(w*w) < 2^(2 e1) <= 2^e2
     Acc<DIM, true> acc;
     acc.zero();
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = ((p.n + nth - 1) / nth) * nth;     // whole warps run every iteration
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += nth) {
+        const bool valid = i < p.n;
         double x[DIM];
         int g = 0, mul = 1;
-        bool inr = true;
+        bool inr = valid;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
-            x[a] = __ldcs(p.x[a] + i);
+            x[a] = valid ? __ldcs(p.x[a] + i) : 0.0;
             const int b = find_bin(p.ax[a], x[a]);
             inr &= (b >= 1) & (b <= p.ax[a].n);
             g += b * mul;
             if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
         }
-        const double w = __ldcs(p.w + i), w2 = w * w;
-        if (fabs(w) <= 1.7976931348623157e308 && fabs(w2) <= 1.7976931348623157e308) {
-            red_exact(limbs + 6 * (size_t)g, w, e1);
-            red_exact(limbs + 6 * (size_t)g + 3, w2, e2);
-        } else {
+        const double w = valid ? __ldcs(p.w + i) : 0.0, w2 = w * w;
+        const bool fin = fabs(w) <= 1.7976931348623157e308 && fabs(w2) <= 1.7976931348623157e308;
+        if (valid && !fin) {
             atomicAdd(p.sumw + g, w);
             atomicAdd(p.sumw2 + g, w2);
+        }
+        const bool use = valid && fin;
+        const unsigned act = __ballot_sync(0xffffffffu, use);
+        if (use) {
+            int c1[kLimbs], c2[kLimbs];
+            exact_chunks(w, e1, c1);
+            exact_chunks(w2, e2, c2);
+            const unsigned peers = __match_any_sync(act, g);
+            const bool dup = __any_sync(act, __popc(peers) > 1);
+            const bool leader = (int)(threadIdx.x & 31) == __ffs(peers) - 1;
+            long long *lb = limbs + 2 * kLimbs * (size_t)g;
+#pragma unroll
+            for (int k = 0; k < kLimbs; ++k) {
+                int s1 = c1[k], s2 = c2[k];
+                if (dup) {                               // equal bins in the warp: exact group sums
+                    s1 = (int)__reduce_add_sync(peers, (unsigned)c1[k]);
+                    s2 = (int)__reduce_add_sync(peers, (unsigned)c2[k]);
+                }
+                if (leader) {
+                    if (s1) atomicAdd(reinterpret_cast<unsigned long long *>(lb + k), (unsigned long long)(long long)s1);
+                    if (s2) atomicAdd(reinterpret_cast<unsigned long long *>(lb + kLimbs + k),
+                                      (unsigned long long)(long long)s2);
+                }
+            }
         }
         if (inr) acc.add(x, w);
     }
@@ -793,17 +823,20 @@ __global__ void __launch_bounds__(512, 2) k_fill_exact(FillP p, long long *limbs
 }
 
 __device__ __forceinline__ double fold_limbs(long long *l, int e) {
-    const __int128 v = (__int128)l[0] + ((__int128)l[1] << 32) + ((__int128)l[2] << 64);
-    l[0] = l[1] = l[2] = 0;
+    __int128 v = 0;
+#pragma unroll
+    for (int k = kLimbs - 1; k >= 0; --k) v = (v << 24) + (__int128)l[k];
+#pragma unroll
+    for (int k = 0; k < kLimbs; ++k) l[k] = 0;
     return ldexp((double)v, e - 96);
 }
 
 __global__ void k_exact_fold(int G, long long *limbs, const unsigned long long *maxbits, double *sumw, double *sumw2) {
     const int e1 = exact_exp(*maxbits), e2 = 2 * e1 + 1;
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
-        long long *l = limbs + 6 * (size_t)g;
-        if (l[0] | l[1] | l[2]) sumw[g] += fold_limbs(l, e1);
-        if (l[3] | l[4] | l[5]) sumw2[g] += fold_limbs(l + 3, e2);
+        long long *l = limbs + 2 * kLimbs * (size_t)g;
+        if (l[0] | l[1] | l[2] | l[3]) sumw[g] += fold_limbs(l, e1);
+        if (l[4] | l[5] | l[6] | l[7]) sumw2[g] += fold_limbs(l + kLimbs, e2);
     }
 }
 

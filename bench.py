@@ -68,6 +68,8 @@ def workload_desc(wl) -> str:
             "C3W": "C3w: TH2D 1000x1000 fixed bins, 2e8 uniform events, random weights",
             "C4": "C4: TH3D 100^3 with flow, 2e8 Cauchy-peaked events, unit weights",
             "C4W": "C4w: TH3D 100^3 with flow, 2e8 Cauchy-peaked events, random weights",
+            "C1F": "C1-shape streamed in float32: TH1D 100 fixed bins [0,1], 2^30 uniform float32 events",
+            "C2F": "C2 in float32: TH1D 10,000 variable-width bins, 5e8 Gaussian float32 events, float32 weights",
             "C5": "C5: 8 histograms (1D/2D mix) from 7 columns, 1.25e8 events/GPU (1e9 over 8 GPUs), "
                   "fused one-pass fill"}.get(wl.name, wl.name)
 
@@ -77,6 +79,11 @@ def get_workload(name: str):
     if name == "C1S":
         wl = bhgen.workload("C1", 1 << 30)
         wl.name = "C1S"
+        return wl
+    if name in ("C1F", "C2F"):   # float32 input columns (NEXT-2)
+        wl = get_workload("C1S" if name == "C1F" else "C2")
+        wl.name = name
+        wl.f32 = True
         return wl
     if name == "C5":             # 1e9 events over 8 GPUs: 1.25e8 per GPU
         return bhgen.workload("C5", 125_000_000)
@@ -184,15 +191,15 @@ def measure_secondary(name: str, steps: int, warmup: int, local: int) -> dict:
     wl = get_workload(name)
     h = wl.hists[0]
     N = wl.n_events
+    f32 = getattr(wl, "f32", False)
     host = torch.empty(N, dtype=torch.float64).pin_memory()
-    cols = []
-    for c in h.cols:
+
+    def dev_col(c):
         wl.column_ptr(c, 0, N, host.data_ptr())
-        cols.append(host.to(f"cuda:{local}"))
-    w = None
-    if h.weighted:
-        wl.column_ptr(wl.wcol, 0, N, host.data_ptr())
-        w = host.to(f"cuda:{local}")
+        t = host.to(f"cuda:{local}")
+        return t.float() if f32 else t
+    cols = [dev_col(c) for c in h.cols]
+    w = dev_col(wl.wcol) if h.weighted else None
     del host
     H = pkg.Histogram(h.axes_spec(), device=local)
     st = torch.cuda.current_stream()
@@ -201,18 +208,23 @@ def measure_secondary(name: str, steps: int, warmup: int, local: int) -> dict:
         H.reset()
         if i >= warmup:
             ev[i - warmup][0].record(st)
-        H.fill(cols, w)
+        if f32:
+            H.fill_f32(cols, w)
+        else:
+            H.fill(cols, w)
         if i >= warmup:
             ev[i - warmup][1].record(st)
     torch.cuda.synchronize()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     peak, _ = hbm_peak()
-    gbs = wl.bytes_per_event * N / (ms * 1e-3) / 1e9
+    bpe = wl.bytes_per_event // (2 if f32 else 1)
+    gbs = bpe * N / (ms * 1e-3) / 1e9
     strat = {1: "priv", 2: "global", 3: "cache"}.get(H.strategy(h.weighted), "?")
     H.close()
     del cols, w
     torch.cuda.empty_cache()
-    return {"workload": workload_desc(wl), "events": N, "events_per_s": N / (ms * 1e-3), "fill_ms": ms,
+    return {"workload": workload_desc(wl), "events": N, "bytes_per_event": bpe, "events_per_s": N / (ms * 1e-3),
+            "fill_ms": ms,
             "achieved_gbs": gbs, "frac": gbs / peak, "fill_strategy": strat}
 
 
@@ -421,7 +433,7 @@ def main():
     ap.add_argument("--strategy", default="auto", choices=["auto", "priv", "global", "cache", "exact"])
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend for N>1")
     ap.add_argument("--events", type=int, default=0, help="override events per GPU (tests)")
-    ap.add_argument("--secondary", default="C1S",
+    ap.add_argument("--secondary", default="C1S,C1F,C2F",
                     help="comma list of extra configs measured device-resident after the headline ('' = none)")
     ap.add_argument("--cpu-sample", type=int, default=50_000_000)
     ap.add_argument("--ref-sample", type=int, default=1 << 23)

@@ -111,6 +111,11 @@ bh_status bh_reset(bh_hist *h, bh_stream s);
  * n == 0 is a no-op.  Errors: BH_EINVAL (n < 0, NULL coords), BH_ECUDA. */
 bh_status bh_fill(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s);
 
+/* bh_fill for float32 columns (DEVICE pointers): every value is
+ * widened exactly to float64 first, so the result equals bh_fill on the widened columns,
+ * at half the input bytes.  BH_STRATEGY_EXACT falls back to AUTO here. */
+bh_status bh_fill_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, bh_stream s);
+
 /* Same as bh_fill but coords/w are HOST pointers (pinned: DMA straight from them;
  * pageable: staged by the driver).  Events are copied in chunks into a device
  * double-buffer on an internal copy stream, overlapped with the fills on s.

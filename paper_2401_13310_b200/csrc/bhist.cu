@@ -322,6 +322,68 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
 }
 
 template <int DIM, bool W, int SINK>
+cudaError_t launch_f32_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    auto kern = c.vsm ? k_fill_f32<DIM, W, SINK, true> : k_fill_f32<DIM, W, SINK, false>;
+    if (c.smem > 48 * 1024) {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+        if (r != cudaSuccess) return r;
+    }
+    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <int DIM, bool W>
+cudaError_t launch_f32_w(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    switch (c.strategy) {
+    case BH_STRATEGY_PRIV:
+        if constexpr (W) {
+            if (p.replicas > 1) return launch_f32_s<DIM, W, SINK_PRIVA>(p, c, s);
+        }
+        return launch_f32_s<DIM, W, SINK_PRIV>(p, c, s);
+    case BH_STRATEGY_CACHE: return launch_f32_s<DIM, W, SINK_CACHE>(p, c, s);
+    default: return launch_f32_s<DIM, W, SINK_GLOBAL>(p, c, s);
+    }
+}
+
+template <int DIM>
+cudaError_t launch_f32(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    return c.weighted ? launch_f32_w<DIM, true>(p, c, s) : launch_f32_w<DIM, false>(p, c, s);
+}
+
+// float32 columns (see k_fill_f32); EXACT is not offered for float32 weights (uses AUTO).
+bh_status fill_device_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, cudaStream_t s) {
+    FillPlan pl;
+    if (bh_status r = plan_fill(h, w != nullptr, pl)) return r;
+    LaunchCfg &c = pl.c;
+    const int64_t kMaxLaunch = int64_t(1) << 30;
+    for (int64_t off = 0; off < n; off += kMaxLaunch) {
+        const int64_t m = std::min(kMaxLaunch, n - off);
+        const double *cs[kMaxDim] = {};
+        for (int a = 0; a < h->dim; ++a) cs[a] = reinterpret_cast<const double *>(coords[a] + off);
+        const double *ws = w ? reinterpret_cast<const double *>(w + off) : nullptr;
+        FillP p = make_params(h, m, cs, ws);
+        for (int a = 0; a < h->dim; ++a) p.ax[a] = pl.ax[a];
+        const uintptr_t ph = reinterpret_cast<uintptr_t>(cs[0]) & 15;
+        bool vec = (ph % 4) == 0;
+        for (int a = 1; a < h->dim; ++a) vec &= (reinterpret_cast<uintptr_t>(cs[a]) & 15) == ph;
+        if (w) vec &= (reinterpret_cast<uintptr_t>(ws) & 15) == ph;
+        p.peel = vec ? (int32_t)std::min<int64_t>(ph ? (16 - ph) / 4 : 0, m) : -1;
+        p.cache_slots = cache_slots_for(c.weighted);
+        p.replicas = pl.replicas;
+        c.grid = grid_for(h, c, m);
+        cudaError_t e;
+        switch (h->dim) {
+        case 1: e = launch_f32<1>(p, c, s); break;
+        case 2: e = launch_f32<2>(p, c, s); break;
+        default: e = launch_f32<3>(p, c, s); break;
+        }
+        if (e != cudaSuccess) return fail(BH_ECUDA, "fill_f32 launch: %s", cudaGetErrorString(e));
+        ++h->launches;
+    }
+    return BH_OK;
+}
+
+template <int DIM, bool W, int SINK>
 cudaError_t launch_expr_s(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
     auto kern = c.vsm ? k_fill_expr<DIM, W, SINK, true> : k_fill_expr<DIM, W, SINK, false>;
     if (c.smem > 48 * 1024) {
@@ -532,6 +594,17 @@ bh_status bh_fill(bh_hist *h, int64_t n, const double *const *coords, const doub
         if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
     DeviceGuard dg(h->device);
     return fill_device(h, n, coords, w, static_cast<cudaStream_t>(s));
+}
+
+bh_status bh_fill_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (n < 0) return fail(BH_EINVAL, "n < 0");
+    if (n == 0) return BH_OK;
+    if (!coords) return fail(BH_EINVAL, "coords is NULL");
+    for (int a = 0; a < h->dim; ++a)
+        if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
+    DeviceGuard dg(h->device);
+    return fill_device_f32(h, n, coords, w, static_cast<cudaStream_t>(s));
 }
 
 bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s) {

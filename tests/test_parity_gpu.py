@@ -519,3 +519,39 @@ def test_exact_mode_nonfinite_weights_and_accumulation():
     other = np.arange(12) != b
     assert np.all(np.abs(r["content"][other] - ref["content"][other]) <= 1e-12 * ref["abs_content"][other])
     h.close()
+
+
+# ------------------------------------------------------------------ float32 input columns (NEXT-2)
+@pytest.mark.parametrize("name", ["C1", "C2", "C3W", "C4"])
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_fill_f32_equals_widened(name, offset):
+    wl = bhgen.workload(name, 700_001)
+    hist = wl.hists[0]
+    axes = oracle.oracle_axes(hist)
+    cols, w = gen_columns(wl, hist, 0, wl.n_events)
+    cols32 = [c.astype(np.float32) for c in cols]
+    w32 = None if w is None else w.astype(np.float32)
+    ref = oracle.OracleHist(axes).fill([c.astype(np.float64) for c in cols32],
+                                       None if w32 is None else w32.astype(np.float64)).read()
+    h = pkg.Histogram(axes)
+    tc = [torch.from_numpy(np.concatenate([np.zeros(offset, np.float32), c])).to(DEV)[offset:] for c in cols32]
+    tw = None if w32 is None else torch.from_numpy(np.concatenate([np.zeros(offset, np.float32), w32])).to(DEV)[offset:]
+    h.fill_f32(tc, tw)
+    compare(h.read(), ref, w is not None, f"f32 {name} off {offset}")
+    h.close()
+
+
+def test_fill_f32_mixed_phases_and_tiny():
+    rng = np.random.default_rng(9)
+    for n in (0, 1, 3, 5, 17, 100_003):
+        x = rng.uniform(-0.1, 1.1, n).astype(np.float32)
+        y = rng.uniform(-0.1, 1.1, n + 1).astype(np.float32)[1:]       # different 16-byte phase
+        axes = [(13, 0.0, 1.0), np.array([0.0, 0.2, 0.7, 1.0])]
+        ref = oracle.OracleHist(axes).fill([x.astype(np.float64), y.astype(np.float64)]).read()
+        h = pkg.Histogram(axes)
+        if n:
+            yt = torch.from_numpy(rng.uniform(0, 1, n + 1).astype(np.float32)).to(DEV)
+            yt[1:] = torch.from_numpy(y).to(DEV)
+            h.fill_f32([torch.from_numpy(x).to(DEV), yt[1:]])
+        compare(h.read(), ref, False, f"f32 mixed n={n}")
+        h.close()

@@ -153,13 +153,14 @@ FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, cons
 struct LaunchCfg {
     int strategy;
     bool weighted, vec, vsm;
+    int vm;                      // 0 fixed axes only, 1 variable tables in smem, 2 in global
     int grid;
     size_t smem;
 };
 
-template <int DIM, bool W, int SINK, bool VEC, bool VSM>
+template <int DIM, bool W, int SINK, bool VEC, int VM>
 cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    auto kern = k_fill<DIM, W, SINK, VEC, VSM>;
+    auto kern = k_fill<DIM, W, SINK, VEC, VM>;
     if (c.smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
         if (e != cudaSuccess) return e;
@@ -170,7 +171,8 @@ cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
 
 template <int DIM, bool W, int SINK, bool VEC>
 cudaError_t launch_m(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    return c.vsm ? launch_t<DIM, W, SINK, VEC, true>(p, c, s) : launch_t<DIM, W, SINK, VEC, false>(p, c, s);
+    return c.vm == 0 ? launch_t<DIM, W, SINK, VEC, 0>(p, c, s)
+                     : c.vm == 1 ? launch_t<DIM, W, SINK, VEC, 1>(p, c, s) : launch_t<DIM, W, SINK, VEC, 2>(p, c, s);
 }
 
 template <int DIM, bool W, int SINK>
@@ -221,6 +223,7 @@ bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl) {
         }
     }
     c.vsm = tabs > 0 && sink + tabs + kStaticSmemReserve <= h->smem_optin;
+    c.vm = tabs == 0 ? 0 : (c.vsm ? 1 : 2);
     // PRIV: replicate the private bins into the spare shared memory (up to one copy
     // per warp) so hot bins are not contended across warps
     pl.replicas = 1;
@@ -323,7 +326,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
 
 template <int DIM, bool W, int SINK>
 cudaError_t launch_f32_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    auto kern = c.vsm ? k_fill_f32<DIM, W, SINK, true> : k_fill_f32<DIM, W, SINK, false>;
+    auto kern = c.vm == 0 ? k_fill_f32<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_f32<DIM, W, SINK, 1> : k_fill_f32<DIM, W, SINK, 2>;
     if (c.smem > 48 * 1024) {
         cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
         if (r != cudaSuccess) return r;
@@ -385,7 +388,7 @@ bh_status fill_device_f32(bh_hist *h, int64_t n, const float *const *coords, con
 
 template <int DIM, bool W, int SINK>
 cudaError_t launch_expr_s(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
-    auto kern = c.vsm ? k_fill_expr<DIM, W, SINK, true> : k_fill_expr<DIM, W, SINK, false>;
+    auto kern = c.vm == 0 ? k_fill_expr<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_expr<DIM, W, SINK, 1> : k_fill_expr<DIM, W, SINK, 2>;
     if (c.smem > 48 * 1024) {
         cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
         if (r != cudaSuccess) return r;

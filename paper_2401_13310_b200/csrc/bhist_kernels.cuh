@@ -75,12 +75,14 @@ __device__ __noinline__ int fixed_exact_quotient(int n, double d, double D) {   
 }
 
 __device__ __forceinline__ int find_bin_fixed(const AxisP &a, double x) {
-    if (x < a.xmin) return 0;
-    if (!(x < a.xmax)) return a.n + 1;   // x == xmax and NaN -> overflow (R5)
+    // branch-free except the rare exact fallback: flow routing by selects
+    const bool under = x < a.xmin;
+    const bool over = !(x < a.xmax);     // x == xmax and NaN -> overflow (R5)
     const double d = __dsub_rn(x, a.xmin);
     const double q = __dmul_rn(d, a.inv);
-    int b = (int)__dmul_rn(q, 1.0 - 0x1p-40);
-    if (b != (int)__dmul_rn(q, 1.0 + 0x1p-40)) b = fixed_exact_quotient(a.n, d, a.D);
+    int b = (int)__dmul_rn(q, 1.0 - 0x1p-40);          // cvt.rzi: NaN -> 0, saturating
+    if (b != (int)__dmul_rn(q, 1.0 + 0x1p-40) && !under && !over) b = fixed_exact_quotient(a.n, d, a.D);
+    b = under ? -1 : (over ? a.n : b);
     return 1 + b;                        // q <= n: bin n+1 is overflow (R4)
 }
 
@@ -143,19 +145,21 @@ __device__ __forceinline__ int find_bin_var_smem(const AxisP &a, double x, const
     return 1 + lo;
 }
 
-template <bool VSM>
+// VM (variable-axis mode, a template constant): 0 = every axis fixed (no variable-axis
+// code at all), 1 = variable-axis tables staged in shared memory, 2 = tables in global.
+template <int VM>
 __device__ __forceinline__ int find_bin(const AxisP &a, double x, const unsigned char *smem) {
 #ifdef BH_EXP_NOSEARCH   // experiment only (wrong results): bin from the guide cell alone
     if (a.var) return x < a.xmin ? 0 : (!(x < a.xmax) ? a.n + 1 : 1 + (int)((long long)guide_cell(a, x) * a.n / a.gcells));
 #endif
-    if (!a.var) return find_bin_fixed(a, x);
-    if (VSM) {
+    if (VM == 0 || !a.var) return find_bin_fixed(a, x);
+    if (VM == 1) {
         return a.g16 ? find_bin_var_smem<true>(a, x, smem + a.tab_off) : find_bin_var_smem<false>(a, x, smem + a.tab_off);
     }
     return find_bin_var_global(a, x);
 }
 
-__device__ __forceinline__ int find_bin(const AxisP &a, double x) { return find_bin<false>(a, x, nullptr); }
+__device__ __forceinline__ int find_bin(const AxisP &a, double x) { return find_bin<2>(a, x, nullptr); }
 
 // Copy each variable axis' float32 edges and guide table into shared memory.
 template <int DIM>
@@ -514,14 +518,14 @@ template <bool W> struct SinkOf<SINK_GLOBAL, W> { using T = GlobalSink<W>; };
 template <bool W> struct SinkOf<SINK_CACHE, W> { using T = CacheSink<W>; };
 
 // ------------------------------------------------------------------ the fill kernel
-template <int DIM, bool W, bool VSM, typename S>
+template <int DIM, bool W, int VM, typename S>
 __device__ __forceinline__ void do_event(const FillP &p, const double (&x)[DIM], double w, S &sink,
                                          Acc<DIM, W> &acc, const unsigned char *smem) {
     int g = 0, mul = 1;
     bool inr = true;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
-        const int b = find_bin<VSM>(p.ax[a], x[a], smem);   // step (1), per axis
+        const int b = find_bin<VM>(p.ax[a], x[a], smem);   // step (1), per axis
         inr &= (b >= 1) & (b <= p.ax[a].n);
         g += b * mul;
         if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
@@ -546,7 +550,7 @@ struct Batch {            // U event pairs of every column, held in registers (x
 // each axis' tab_off.  VEC: columns are read as double2 (LDG.E.128) after `peel`
 // leading events; the next batch is loaded before the current one is processed
 // (register double-buffering) so each thread keeps 2*U*ncol 16-byte loads in flight.
-template <int DIM, bool W, int SINK, bool VEC, bool VSM>
+template <int DIM, bool W, int SINK, bool VEC, int VM>
 __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Sink_t = typename SinkOf<SINK, W>::T;
@@ -556,8 +560,8 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
     else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas);
     else sink.init(smem, p.G);
-    if constexpr (VSM) stage_axes<DIM>(p.ax, smem);
-    if constexpr (SINK != SINK_GLOBAL || VSM) __syncthreads();
+    if constexpr (VM == 1) stage_axes<DIM>(p.ax, smem);
+    if constexpr (SINK != SINK_GLOBAL || VM == 1) __syncthreads();
 
     Acc<DIM, W> acc;
     acc.zero();
@@ -593,8 +597,8 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
                     double x0[DIM], x1[DIM];
 #pragma unroll
                     for (int a = 0; a < DIM; ++a) { x0[a] = bt.x[u][a].x; x1[a] = bt.x[u][a].y; }
-                    do_event<DIM, W, VSM>(p, x0, W ? bt.w[u].x : 1.0, sink, acc, smem);
-                    do_event<DIM, W, VSM>(p, x1, W ? bt.w[u].y : 1.0, sink, acc, smem);
+                    do_event<DIM, W, VM>(p, x0, W ? bt.w[u].x : 1.0, sink, acc, smem);
+                    do_event<DIM, W, VM>(p, x1, W ? bt.w[u].y : 1.0, sink, acc, smem);
                 }
             }
         };
@@ -625,14 +629,14 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
             double x[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) x[a] = p.x[a][i];
-            do_event<DIM, W, VSM>(p, x, W ? p.w[i] : 1.0, sink, acc, smem);
+            do_event<DIM, W, VM>(p, x, W ? p.w[i] : 1.0, sink, acc, smem);
         }
     } else {
         for (int i = tid; i < (int)p.n; i += nth) {
             double x[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) x[a] = __ldcs(p.x[a] + i);
-            do_event<DIM, W, VSM>(p, x, W ? __ldcs(p.w + i) : 1.0, sink, acc, smem);
+            do_event<DIM, W, VM>(p, x, W ? __ldcs(p.w + i) : 1.0, sink, acc, smem);
         }
     }
 
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
 // columns; the columns cost 4 B/event instead of 8.  Columns sharing a 16-byte phase are
 // read as float4 (4 events per LDG.128) after `peel` (0-3) leading events; p.peel < 0
 // selects the scalar loop (mixed phases).
-template <int DIM, bool W, int SINK, bool VSM>
+template <int DIM, bool W, int SINK, int VM>
 __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill_f32(FillP p) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Sink_t = typename SinkOf<SINK, W>::T;
@@ -660,8 +664,8 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
     else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas);
     else sink.init(smem, p.G);
-    if constexpr (VSM) stage_axes<DIM>(p.ax, smem);
-    if constexpr (SINK != SINK_GLOBAL || VSM) __syncthreads();
+    if constexpr (VM == 1) stage_axes<DIM>(p.ax, smem);
+    if constexpr (SINK != SINK_GLOBAL || VM == 1) __syncthreads();
     Acc<DIM, W> acc;
     acc.zero();
     const float *xs[DIM];
@@ -674,7 +678,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
         double x[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) x[a] = (double)xs[a][i];
-        do_event<DIM, W, VSM>(p, x, W ? (double)ws[i] : 1.0, sink, acc, smem);
+        do_event<DIM, W, VM>(p, x, W ? (double)ws[i] : 1.0, sink, acc, smem);
     };
     if (p.peel < 0) {
         for (int i = tid; i < n; i += nth) one(i);
@@ -694,7 +698,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
                 double x[DIM];
 #pragma unroll
                 for (int a = 0; a < DIM; ++a) x[a] = (double)xf[a][j];
-                do_event<DIM, W, VSM>(p, x, W ? (double)wf[j] : 1.0, sink, acc, smem);
+                do_event<DIM, W, VM>(p, x, W ? (double)wf[j] : 1.0, sink, acc, smem);
             }
         }
         const int tail0 = base + 4 * nq, nscalar = base + (n - tail0);
@@ -763,7 +767,7 @@ __device__ __forceinline__ void run_expr(const ExprP &e, double (&r)[kExprRegs])
 }
 
 // Same sinks and stats as k_fill; entries += number of events that pass the filter.
-template <int DIM, bool W, int SINK, bool VSM>
+template <int DIM, bool W, int SINK, int VM>
 __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 1)
     k_fill_expr(FillP p, const __grid_constant__ ExprP e) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -773,8 +777,8 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
     else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas);
     else sink.init(smem, p.G);
-    if constexpr (VSM) stage_axes<DIM>(p.ax, smem);
-    if constexpr (SINK != SINK_GLOBAL || VSM) __syncthreads();
+    if constexpr (VM == 1) stage_axes<DIM>(p.ax, smem);
+    if constexpr (SINK != SINK_GLOBAL || VM == 1) __syncthreads();
     Acc<DIM, W> acc;
     acc.zero();
     unsigned int passed = 0;
@@ -789,7 +793,7 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
         double x[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) x[a] = r[e.axis_reg[a]];
-        do_event<DIM, W, VSM>(p, x, W ? r[e.weight_reg] : 1.0, sink, acc, smem);
+        do_event<DIM, W, VM>(p, x, W ? r[e.weight_reg] : 1.0, sink, acc, smem);
     }
     // entries: passing events (order-independent integer adds)
     for (int o = 16; o > 0; o >>= 1) passed += __shfl_xor_sync(0xffffffffu, passed, o);

@@ -219,7 +219,7 @@ def measure_secondary(name: str, steps: int, warmup: int, local: int) -> dict:
     peak, _ = hbm_peak()
     bpe = wl.bytes_per_event // (2 if f32 else 1)
     gbs = bpe * N / (ms * 1e-3) / 1e9
-    strat = {1: "priv", 2: "global", 3: "cache"}.get(H.strategy(h.weighted), "?")
+    strat = {1: "priv", 2: "global", 3: "cache", 5: "sort"}.get(H.strategy(h.weighted), "?")
     H.close()
     del cols, w
     torch.cuda.empty_cache()
@@ -267,7 +267,7 @@ def run_gpu(args):
     devc = [t.to(dev, non_blocking=True) for t in host]
     torch.cuda.synchronize()
 
-    strat_code = {"auto": 0, "priv": 1, "global": 2, "cache": 3, "exact": 4}[args.strategy]
+    strat_code = {"auto": 0, "priv": 1, "global": 2, "cache": 3, "exact": 4, "sort": 5}[args.strategy]
     Hs = [pkg.Histogram(h.axes_spec(), device=local, strategy=strat_code) for h in hists]
     multi = len(Hs) > 1
     stream = torch.cuda.current_stream()
@@ -387,7 +387,7 @@ def run_gpu(args):
         fill_avg = float(np.mean(fill_ms))
         achieved = bpe * N / (fill_avg * 1e-3) / 1e9
         traffic = ncu_traffic(wl.name)
-        names = {0: "auto", 1: "priv", 2: "global", 3: "cache", 4: "exact"}
+        names = {0: "auto", 1: "priv", 2: "global", 3: "cache", 4: "exact", 5: "sort"}
         strat = "fused multi-histogram (per-histogram smem/global plan)" if multi else \
             names[Hs[0].strategy(hists[0].weighted)]
         clocks = clk.summary()
@@ -430,7 +430,7 @@ def main():
     ap.add_argument("--config", default="C2", help="C1, C1S, C2 (default), C3, C3W, C4, C4W, C5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--strategy", default="auto", choices=["auto", "priv", "global", "cache", "exact"])
+    ap.add_argument("--strategy", default="auto", choices=["auto", "priv", "global", "cache", "exact", "sort"])
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend for N>1")
     ap.add_argument("--events", type=int, default=0, help="override events per GPU (tests)")
     ap.add_argument("--secondary", default="C1S,C1F,C2F",

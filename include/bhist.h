@@ -84,6 +84,16 @@ typedef struct {
  *        max|w|.  Unit-weight fills are exact in every mode;
  *        bh_fill_expr uses AUTO.  Slower (six L2 integer atomics per event). */
 #define BH_STRATEGY_EXACT 4
+/* SORT   two-pass partitioned fill for bin spaces too large for PRIV (AUTO's choice
+ *        there): pass 1 bins each event, accumulates the stats and writes a record
+ *        (bin mod 2^pb, w) into a partition-sorted scratch buffer (p = bin >> pb,
+ *        pb = 15 unit / 13 weighted; at most 2048 partitions); pass 2 reduces each
+ *        partition in shared memory and adds it to the bins once per CTA.  The
+ *        "sort-then-segmented-reduce" path for large 2D/3D bin spaces.  Scratch of
+ *        2 (unit) or 10 (weighted) bytes per event of a chunk (<= 2^27 / 2^26 events)
+ *        is allocated by the histogram on first use.  bh_fill_f32 and bh_fill_expr
+ *        use CACHE instead. */
+#define BH_STRATEGY_SORT 5
 
 /* Debug flags (bh_set_debug) — negative controls for tests only. */
 #define BH_DEBUG_SKIP_COPY_WAIT 1 /* bh_fill_host: fill without waiting for the H2D copy (PAPER.md:223 race) */

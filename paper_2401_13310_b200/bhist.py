@@ -17,7 +17,7 @@ import numpy as np
 from . import _build
 
 BH_OK, BH_EINVAL, BH_ENOMEM, BH_ECUDA, BH_EDEVICE, BH_EMISMATCH = 0, -1, -2, -3, -4, -5
-BH_STRATEGY_AUTO, BH_STRATEGY_PRIV, BH_STRATEGY_GLOBAL, BH_STRATEGY_CACHE, BH_STRATEGY_EXACT = 0, 1, 2, 3, 4
+BH_STRATEGY_AUTO, BH_STRATEGY_PRIV, BH_STRATEGY_GLOBAL, BH_STRATEGY_CACHE, BH_STRATEGY_EXACT, BH_STRATEGY_SORT = 0, 1, 2, 3, 4, 5
 BH_DEBUG_SKIP_COPY_WAIT = 1
 
 # every symbol include/bhist.h declares (checked by tests/test_abi.py)

@@ -17,7 +17,7 @@
 #include <vector>
 
 #include "../../include/bhist.h"
-#include "bhist_kernels.cuh"
+#include "bhist_launch.cuh"
 
 using namespace bh;
 
@@ -84,6 +84,13 @@ struct bh_hist {
     unsigned long long *maxbits = nullptr;   // EXACT: bit pattern of max|w| of the current launch
     double *pack_buf = nullptr;       // device buffer for bh_read
     double *pack_host = nullptr;      // pinned host buffer for bh_read
+    // SORT strategy scratch (grown on demand): records, segment offsets, partition totals
+    uint16_t *part_l = nullptr;
+    double *part_w = nullptr;
+    uint32_t *part_offs = nullptr;
+    unsigned long long *part_cnt = nullptr, *part_cp = nullptr;
+    int64_t part_cap_l = 0, part_cap_w = 0, part_cap_offs = 0;
+    int part_P = 0;
     std::vector<void *> axis_mem;     // edges and guide tables
     // host->device double buffer
     cudaStream_t copy_stream = nullptr;
@@ -96,18 +103,31 @@ namespace {
 
 size_t align16(size_t b);
 size_t axis_table_bytes(const AxisP &a);
+int sort_pb(bool weighted) { return weighted ? 13 : 15; }   // 2^pb bins = 128 KB of shared memory
+int64_t sort_partitions(const bh_hist *h, bool weighted) {
+    return (h->G + (int64_t(1) << sort_pb(weighted)) - 1) >> sort_pb(weighted);
+}
 constexpr size_t kStaticSmemReserve = 4096;   // block_stats_finish scratch + driver reserve
 
 // AUTO: privatize the bins in shared memory whenever they fit next to the reserve
 // (variable-axis tables then go to smem only if they also fit); otherwise CACHE.
 int resolve_strategy(const bh_hist *h, bool weighted) {
     // EXACT only changes weighted fills of bh_fill / bh_fill_host (fill_exact below)
+    if (h->strategy == BH_STRATEGY_SORT)     // weighted partitions are 4x smaller
+        return sort_partitions(h, weighted) <= kPartMaxP ? BH_STRATEGY_SORT : BH_STRATEGY_CACHE;
     if (h->strategy != BH_STRATEGY_AUTO && h->strategy != BH_STRATEGY_EXACT) return h->strategy;
     const size_t priv = (weighted ? 16 : 4) * (size_t)h->G;
     if (priv + kStaticSmemReserve <= h->smem_optin) return BH_STRATEGY_PRIV;
     // large bin spaces: shared-memory cache of the hottest bins in front of L2 atomics
-    // (as fast as plain GLOBAL on uniform data, 30x faster on the peaked C4 shape)
+    // (as fast as plain GLOBAL on uniform data, 30x faster on the peaked C4 shape).
+    // SORT is faster on uniform data but not on peaked data, so it is opt-in.
     return BH_STRATEGY_CACHE;
+}
+
+// kernels without a SORT variant (float32 columns, fill_expr) use CACHE instead
+int resolve_one_pass(const bh_hist *h, bool weighted) {
+    const int s = resolve_strategy(h, weighted);
+    return s == BH_STRATEGY_SORT ? BH_STRATEGY_CACHE : s;
 }
 
 int cache_slots_for(bool weighted) { return weighted ? 4096 : 16384; }
@@ -150,54 +170,6 @@ FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, cons
     return p;
 }
 
-struct LaunchCfg {
-    int strategy;
-    bool weighted, vec, vsm;
-    int vm;                      // 0 fixed axes only, 1 variable tables in smem, 2 in global
-    int grid;
-    size_t smem;
-};
-
-template <int DIM, bool W, int SINK, bool VEC, int VM>
-cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    auto kern = k_fill<DIM, W, SINK, VEC, VM>;
-    if (c.smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-        if (e != cudaSuccess) return e;
-    }
-    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
-    return cudaGetLastError();
-}
-
-template <int DIM, bool W, int SINK, bool VEC>
-cudaError_t launch_m(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    return c.vm == 0 ? launch_t<DIM, W, SINK, VEC, 0>(p, c, s)
-                     : c.vm == 1 ? launch_t<DIM, W, SINK, VEC, 1>(p, c, s) : launch_t<DIM, W, SINK, VEC, 2>(p, c, s);
-}
-
-template <int DIM, bool W, int SINK>
-cudaError_t launch_v(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    return c.vec ? launch_m<DIM, W, SINK, true>(p, c, s) : launch_m<DIM, W, SINK, false>(p, c, s);
-}
-
-template <int DIM, bool W>
-cudaError_t launch_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    switch (c.strategy) {
-    case BH_STRATEGY_PRIV:
-        if constexpr (W) {
-            if (p.replicas > 1) return launch_v<DIM, W, SINK_PRIVA>(p, c, s);
-        }
-        return launch_v<DIM, W, SINK_PRIV>(p, c, s);
-    case BH_STRATEGY_CACHE: return launch_v<DIM, W, SINK_CACHE>(p, c, s);
-    default: return launch_v<DIM, W, SINK_GLOBAL>(p, c, s);
-    }
-}
-
-template <int DIM>
-cudaError_t launch_d(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    return c.weighted ? launch_s<DIM, true>(p, c, s) : launch_s<DIM, false>(p, c, s);
-}
-
 int threads_of(int strategy, bool) { return strategy == BH_STRATEGY_GLOBAL ? kThreadsGlobal : kThreadsSmem; }
 int resident_blocks(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? 2 : 1; }
 
@@ -211,7 +183,7 @@ struct FillPlan {
 bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl) {
     LaunchCfg &c = pl.c;
     c.weighted = weighted;
-    c.strategy = resolve_strategy(h, c.weighted);
+    c.strategy = resolve_one_pass(h, c.weighted);
     size_t sink = sink_bytes(h, c.strategy, c.weighted);
     // variable-axis tables go to shared memory behind the sink when they fit
     size_t tabs = 0;
@@ -288,9 +260,127 @@ bh_status fill_exact(bh_hist *h, int64_t n, const double *const *coords, const d
     return BH_OK;
 }
 
+// ---- SORT strategy (bhist_sort.cuh): pass 1 scatter -> plan -> pass 2 reduce, per chunk
+// pad segments to RC records (pass 2 reads aligned chunks) while that costs little
+int sort_rc(bool weighted, int P) { return weighted ? (P <= 512 ? 4 : 1) : (P <= 256 ? 8 : 1); }
+int sort_ts(int tile, int P, int rc) { return (tile + P * (rc - 1) + 7) / 8 * 8; }
+
+template <bool W, int RC>
+cudaError_t launch_part2(const FillP &p, const PartP &q, int grid, cudaStream_t s) {
+    auto kern = k_part_reduce<W, RC>;
+    const int smem = ((W ? 16 : 4) << sort_pb(W)) + 4 * (2 * kReduceBatch + 1 + 32);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kReduceThreads, smem, s>>>(p, q);
+    return cudaGetLastError();
+}
+
+// Scratch for chunks of `ev` events (grow-only; the stream is synchronized before a
+// buffer that kernels may still read is freed).
+bh_status part_scratch(bh_hist *h, int64_t ev, bool weighted, int P, cudaStream_t s) {
+    const int tile = kPartThreads * part_ev(h->dim, weighted);
+    const int64_t tiles = (ev + tile - 1) / tile;
+    const int64_t nl = tiles * sort_ts(tile, P, sort_rc(weighted, P)), no = tiles * (P + 1);
+    const bool grow = nl > h->part_cap_l || (weighted && nl > h->part_cap_w) || no > h->part_cap_offs || P > h->part_P;
+    if (!grow) return BH_OK;
+    CUDA_TRY(cudaStreamSynchronize(s));
+    auto realloc = [&](void **ptr, size_t bytes) -> bool {
+        if (*ptr) cudaFree(*ptr);
+        *ptr = nullptr;
+        if (cudaMalloc(ptr, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
+        return true;
+    };
+    if (nl > h->part_cap_l) {
+        if (!realloc(reinterpret_cast<void **>(&h->part_l), sizeof(uint16_t) * nl)) { h->part_cap_l = 0; return fail(BH_ENOMEM, "SORT scratch"); }
+        h->part_cap_l = nl;
+    }
+    if (weighted && nl > h->part_cap_w) {
+        if (!realloc(reinterpret_cast<void **>(&h->part_w), sizeof(double) * nl)) { h->part_cap_w = 0; return fail(BH_ENOMEM, "SORT scratch"); }
+        h->part_cap_w = nl;
+    }
+    if (no > h->part_cap_offs) {
+        if (!realloc(reinterpret_cast<void **>(&h->part_offs), sizeof(uint32_t) * no)) { h->part_cap_offs = 0; return fail(BH_ENOMEM, "SORT scratch"); }
+        h->part_cap_offs = no;
+    }
+    if (P > h->part_P) {
+        if (!realloc(reinterpret_cast<void **>(&h->part_cnt), sizeof(unsigned long long) * P) ||
+            !realloc(reinterpret_cast<void **>(&h->part_cp), sizeof(unsigned long long) * (P + 1))) {
+            h->part_P = 0;
+            return fail(BH_ENOMEM, "SORT scratch");
+        }
+        CUDA_TRY(cudaMemsetAsync(h->part_cnt, 0, sizeof(unsigned long long) * P, s));
+        h->part_P = P;
+    }
+    return BH_OK;
+}
+
+bh_status fill_sort(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
+    const bool W = w != nullptr;
+    const int pb = sort_pb(W);
+    const int P = (int)sort_partitions(h, W);
+    // chunk: bounds the scratch (2 or 10 B per event) and keeps pass 2's merge traffic
+    // (about (#SM + P) partitions x 2^pb bins per chunk) small next to the events
+    int64_t chunk = W ? (int64_t(1) << 26) : (int64_t(1) << 27);
+    if (const char *env = getenv("BHIST_SORT_CHUNK")) chunk = std::max<int64_t>(1, atoll(env));   // tests: many chunks
+    if (bh_status r = part_scratch(h, std::min(n, chunk), W, P, s)) return r;
+    // pass-1 shared memory: staging + counters, then the variable-axis tables if they fit
+    const int tile = kPartThreads * part_ev(h->dim, W);
+    const int rc = sort_rc(W, P), ts = sort_ts(tile, P, rc);
+    const size_t stages = (size_t)kPartStages * (h->dim + (W ? 1 : 0)) * tile * 8 + 8 * kPartStages;
+    const size_t base = align16(stages + (W ? 8 * (size_t)ts : 0) + 2 * (size_t)ts + 4 * (2 * (size_t)P + 1));
+    AxisP ax[kMaxDim];
+    size_t tabs = 0;
+    for (int a = 0; a < h->dim; ++a) {
+        ax[a] = h->ax[a];
+        if (ax[a].var) { ax[a].tab_off = (int32_t)(base + tabs); tabs += axis_table_bytes(ax[a]); }
+    }
+    const size_t per_cta = h->smem_optin - kStaticSmemReserve;        // one pass-1 CTA per SM
+    const int vm = tabs == 0 ? 0 : (base + tabs <= per_cta ? 1 : 2);
+    const size_t smem1 = vm == 1 ? base + tabs : base;
+    if (smem1 > per_cta) return fail(BH_EINVAL, "SORT pass 1 needs %zu B of shared memory", smem1);
+    for (int64_t off = 0; off < n; off += chunk) {
+        const int64_t m = std::min(chunk, n - off);
+        const double *cs[kMaxDim] = {};
+        for (int a = 0; a < h->dim; ++a) cs[a] = coords[a] + off;
+        FillP p = make_params(h, m, cs, W ? w + off : nullptr);
+        for (int a = 0; a < h->dim; ++a) p.ax[a] = ax[a];
+        PartP q{};
+        q.rec_l = h->part_l;
+        q.rec_w = h->part_w;
+        q.offs = h->part_offs;
+        q.cnt = h->part_cnt;
+        q.cp = h->part_cp;
+        q.P = P;
+        q.pb = pb;
+        q.tile = tile;
+        q.ts = ts;
+        q.ntiles = (int)((m + tile - 1) / tile);
+        const int g1 = std::max(1, std::min(q.ntiles, h->nsm));
+        cudaError_t e;
+        switch (h->dim * 2 + (W ? 1 : 0)) {
+        case 2: e = fill_launch_part1<1, false>(p, q, vm, rc, g1, smem1, s); break;
+        case 3: e = fill_launch_part1<1, true>(p, q, vm, rc, g1, smem1, s); break;
+        case 4: e = fill_launch_part1<2, false>(p, q, vm, rc, g1, smem1, s); break;
+        case 5: e = fill_launch_part1<2, true>(p, q, vm, rc, g1, smem1, s); break;
+        case 6: e = fill_launch_part1<3, false>(p, q, vm, rc, g1, smem1, s); break;
+        default: e = fill_launch_part1<3, true>(p, q, vm, rc, g1, smem1, s); break;
+        }
+        if (e != cudaSuccess) return fail(BH_ECUDA, "SORT pass 1 launch: %s", cudaGetErrorString(e));
+        k_part_plan<<<1, 32, 0, s>>>(q);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(BH_ECUDA, "SORT plan launch: %s", cudaGetErrorString(e));
+        e = W ? (rc == 1 ? launch_part2<true, 1>(p, q, h->nsm, s) : launch_part2<true, 4>(p, q, h->nsm, s))
+              : (rc == 1 ? launch_part2<false, 1>(p, q, h->nsm, s) : launch_part2<false, 8>(p, q, h->nsm, s));
+        if (e != cudaSuccess) return fail(BH_ECUDA, "SORT pass 2 launch: %s", cudaGetErrorString(e));
+        h->launches += 3;
+    }
+    return BH_OK;
+}
+
 // One fill over device-resident columns, split into launches of <= 2^30 events.
 bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
     if (w && h->strategy == BH_STRATEGY_EXACT) return fill_exact(h, n, coords, w, s);
+    if (resolve_strategy(h, w != nullptr) == BH_STRATEGY_SORT) return fill_sort(h, n, coords, w, s);
     FillPlan pl;
     if (bh_status r = plan_fill(h, w != nullptr, pl)) return r;
     LaunchCfg &c = pl.c;
@@ -314,43 +404,14 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         c.grid = grid_for(h, c, m);
         cudaError_t e;
         switch (h->dim) {
-        case 1: e = launch_d<1>(p, c, s); break;
-        case 2: e = launch_d<2>(p, c, s); break;
-        default: e = launch_d<3>(p, c, s); break;
+        case 1: e = c.weighted ? fill_launch<1, true>(p, c, s) : fill_launch<1, false>(p, c, s); break;
+        case 2: e = c.weighted ? fill_launch<2, true>(p, c, s) : fill_launch<2, false>(p, c, s); break;
+        default: e = c.weighted ? fill_launch<3, true>(p, c, s) : fill_launch<3, false>(p, c, s); break;
         }
         if (e != cudaSuccess) return fail(BH_ECUDA, "fill launch: %s", cudaGetErrorString(e));
         ++h->launches;
     }
     return BH_OK;
-}
-
-template <int DIM, bool W, int SINK>
-cudaError_t launch_f32_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    auto kern = c.vm == 0 ? k_fill_f32<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_f32<DIM, W, SINK, 1> : k_fill_f32<DIM, W, SINK, 2>;
-    if (c.smem > 48 * 1024) {
-        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-        if (r != cudaSuccess) return r;
-    }
-    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
-    return cudaGetLastError();
-}
-
-template <int DIM, bool W>
-cudaError_t launch_f32_w(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    switch (c.strategy) {
-    case BH_STRATEGY_PRIV:
-        if constexpr (W) {
-            if (p.replicas > 1) return launch_f32_s<DIM, W, SINK_PRIVA>(p, c, s);
-        }
-        return launch_f32_s<DIM, W, SINK_PRIV>(p, c, s);
-    case BH_STRATEGY_CACHE: return launch_f32_s<DIM, W, SINK_CACHE>(p, c, s);
-    default: return launch_f32_s<DIM, W, SINK_GLOBAL>(p, c, s);
-    }
-}
-
-template <int DIM>
-cudaError_t launch_f32(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    return c.weighted ? launch_f32_w<DIM, true>(p, c, s) : launch_f32_w<DIM, false>(p, c, s);
 }
 
 // float32 columns (see k_fill_f32); EXACT is not offered for float32 weights (uses AUTO).
@@ -376,43 +437,14 @@ bh_status fill_device_f32(bh_hist *h, int64_t n, const float *const *coords, con
         c.grid = grid_for(h, c, m);
         cudaError_t e;
         switch (h->dim) {
-        case 1: e = launch_f32<1>(p, c, s); break;
-        case 2: e = launch_f32<2>(p, c, s); break;
-        default: e = launch_f32<3>(p, c, s); break;
+        case 1: e = c.weighted ? fill_launch_f32<1, true>(p, c, s) : fill_launch_f32<1, false>(p, c, s); break;
+        case 2: e = c.weighted ? fill_launch_f32<2, true>(p, c, s) : fill_launch_f32<2, false>(p, c, s); break;
+        default: e = c.weighted ? fill_launch_f32<3, true>(p, c, s) : fill_launch_f32<3, false>(p, c, s); break;
         }
         if (e != cudaSuccess) return fail(BH_ECUDA, "fill_f32 launch: %s", cudaGetErrorString(e));
         ++h->launches;
     }
     return BH_OK;
-}
-
-template <int DIM, bool W, int SINK>
-cudaError_t launch_expr_s(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
-    auto kern = c.vm == 0 ? k_fill_expr<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_expr<DIM, W, SINK, 1> : k_fill_expr<DIM, W, SINK, 2>;
-    if (c.smem > 48 * 1024) {
-        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-        if (r != cudaSuccess) return r;
-    }
-    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p, e);
-    return cudaGetLastError();
-}
-
-template <int DIM, bool W>
-cudaError_t launch_expr_w(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
-    switch (c.strategy) {
-    case BH_STRATEGY_PRIV:
-        if constexpr (W) {
-            if (p.replicas > 1) return launch_expr_s<DIM, W, SINK_PRIVA>(p, e, c, s);
-        }
-        return launch_expr_s<DIM, W, SINK_PRIV>(p, e, c, s);
-    case BH_STRATEGY_CACHE: return launch_expr_s<DIM, W, SINK_CACHE>(p, e, c, s);
-    default: return launch_expr_s<DIM, W, SINK_GLOBAL>(p, e, c, s);
-    }
-}
-
-template <int DIM>
-cudaError_t launch_expr(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
-    return c.weighted ? launch_expr_w<DIM, true>(p, e, c, s) : launch_expr_w<DIM, false>(p, e, c, s);
 }
 
 bh_status check_hist(const bh_hist *h) {
@@ -564,6 +596,11 @@ bh_status bh_destroy(bh_hist *h) {
     cudaFree(h->limbs);
     cudaFree(h->maxbits);
     cudaFree(h->pack_buf);
+    cudaFree(h->part_l);
+    cudaFree(h->part_w);
+    cudaFree(h->part_offs);
+    cudaFree(h->part_cnt);
+    cudaFree(h->part_cp);
     if (h->pack_host) cudaFreeHost(h->pack_host);
     for (void *p : h->axis_mem) cudaFree(p);
     for (int i = 0; i < kStageSlots; ++i) {
@@ -861,9 +898,12 @@ bh_status bh_fill_expr(bh_hist *h, int64_t n, const double *const *cols, int32_t
         c.grid = grid_for(h, c, m);
         cudaError_t r;
         switch (h->dim) {
-        case 1: r = launch_expr<1>(p, e, c, static_cast<cudaStream_t>(s)); break;
-        case 2: r = launch_expr<2>(p, e, c, static_cast<cudaStream_t>(s)); break;
-        default: r = launch_expr<3>(p, e, c, static_cast<cudaStream_t>(s)); break;
+        case 1: r = c.weighted ? fill_launch_expr<1, true>(p, e, c, static_cast<cudaStream_t>(s))
+                           : fill_launch_expr<1, false>(p, e, c, static_cast<cudaStream_t>(s)); break;
+        case 2: r = c.weighted ? fill_launch_expr<2, true>(p, e, c, static_cast<cudaStream_t>(s))
+                           : fill_launch_expr<2, false>(p, e, c, static_cast<cudaStream_t>(s)); break;
+        default: r = c.weighted ? fill_launch_expr<3, true>(p, e, c, static_cast<cudaStream_t>(s))
+                           : fill_launch_expr<3, false>(p, e, c, static_cast<cudaStream_t>(s)); break;
         }
         if (r != cudaSuccess) return fail(BH_ECUDA, "fill_expr launch: %s", cudaGetErrorString(r));
         ++h->launches;
@@ -951,9 +991,11 @@ bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *sta
 
 bh_status bh_set_strategy(bh_hist *h, int32_t strategy) {
     if (check_hist(h)) return BH_EINVAL;
-    if (strategy < BH_STRATEGY_AUTO || strategy > BH_STRATEGY_EXACT) return fail(BH_EINVAL, "unknown strategy %d", strategy);
+    if (strategy < BH_STRATEGY_AUTO || strategy > BH_STRATEGY_SORT) return fail(BH_EINVAL, "unknown strategy %d", strategy);
     if (strategy == BH_STRATEGY_PRIV && 4 * (size_t)h->G + kStaticSmemReserve > h->smem_optin)
         return fail(BH_EINVAL, "PRIV cannot hold %lld bins in shared memory", (long long)h->G);
+    if (strategy == BH_STRATEGY_SORT && sort_partitions(h, false) > kPartMaxP)
+        return fail(BH_EINVAL, "SORT supports at most %d partitions of 2^%d bins", kPartMaxP, sort_pb(false));
     h->strategy = strategy;
     return BH_OK;
 }

@@ -1,0 +1,7 @@
+// Fill-kernel instantiations for DIM = 1, weighted fills (see bhist_launch.cuh).
+#define BH_FILL_TU
+#include "bhist_launch.cuh"
+
+namespace bh {
+BH_DEFINE_FILL_TU(1, true)
+}  // namespace bh

@@ -70,7 +70,7 @@ struct FillP {
 // same integer, and the division is skipped; otherwise (~1e-6 of uniform events)
 // the exact expression runs.  q >= 0, so truncation == floor.  All operations are
 // explicit _rn intrinsics: nvcc may not contract or reorder them.
-__device__ __noinline__ int fixed_exact_quotient(int n, double d, double D) {   // rare path, out of line
+static __device__ __noinline__ int fixed_exact_quotient(int n, double d, double D) {   // rare path, out of line
     return (int)__ddiv_rn(__dmul_rn((double)n, d), D);
 }
 
@@ -84,6 +84,23 @@ __device__ __forceinline__ int find_bin_fixed(const AxisP &a, double x) {
     if (b != (int)__dmul_rn(q, 1.0 + 0x1p-40) && !under && !over) b = fixed_exact_quotient(a.n, d, a.D);
     b = under ? -1 : (over ? a.n : b);
     return 1 + b;                        // q <= n: bin n+1 is overflow (R4)
+}
+
+// Split form for kernels that defer the rare exact division out of their event loop
+// (a call inside the loop makes the compiler reload every kernel parameter per event):
+// the fast path's bin, with `need` set when only the exact division can decide it.
+__device__ __forceinline__ int find_bin_fixed_fast(const AxisP &a, double x, bool &need) {
+    const bool under = x < a.xmin;
+    const bool over = !(x < a.xmax);
+    const double q = __dmul_rn(__dsub_rn(x, a.xmin), a.inv);
+    const int b = (int)__dmul_rn(q, 1.0 - 0x1p-40);
+    need = b != (int)__dmul_rn(q, 1.0 + 0x1p-40) && !under && !over;
+    return 1 + (under ? -1 : (over ? a.n : b));
+}
+
+// the exact bin of an in-range x whose fast path set `need`
+__device__ __forceinline__ int find_bin_fixed_exact(const AxisP &a, double x) {
+    return 1 + fixed_exact_quotient(a.n, __dsub_rn(x, a.xmin), a.D);
 }
 
 // Guide cell of a coordinate x >= e[0]: monotone non-decreasing in x (RN is
@@ -160,6 +177,14 @@ __device__ __forceinline__ int find_bin(const AxisP &a, double x, const unsigned
 }
 
 __device__ __forceinline__ int find_bin(const AxisP &a, double x) { return find_bin<2>(a, x, nullptr); }
+
+// find_bin with the fixed-axis exact division deferred (see find_bin_fixed_fast)
+template <int VM>
+__device__ __forceinline__ int find_bin_deferred(const AxisP &a, double x, const unsigned char *smem, bool &need) {
+    need = false;
+    if (VM == 0 || !a.var) return find_bin_fixed_fast(a, x, need);
+    return find_bin<VM>(a, x, smem);
+}
 
 // Copy each variable axis' float32 edges and guide table into shared memory.
 template <int DIM>
@@ -819,6 +844,8 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
 // atomics (NaN/inf propagate as in any float sum).
 constexpr int kLimbs = 4;                      // per quantity; 8 per bin (sumw, sumw2)
 
+#ifndef BH_FILL_TU   // kernels below the fill templates are compiled once, in bhist.cu
+
 __global__ void k_wmax(const double *__restrict__ w, int64_t n, unsigned long long *maxbits) {
     unsigned long long m = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -922,6 +949,8 @@ __global__ void k_exact_fold(int G, long long *limbs, const unsigned long long *
     }
 }
 
+#endif  // BH_FILL_TU
+
 // ------------------------------------------------------------------ fused multi-histogram fill (C5)
 // One pass over a set of columns feeding several histograms (the paper's future
 // work "multiple histograms from different columns in one pass"; RDataFrame
@@ -962,6 +991,7 @@ struct MultiP {
     MultiH h[kMaxHist];
 };
 
+#ifndef BH_FILL_TU
 __device__ __forceinline__ double pick(const double (&x)[kMaxCols], int c) {
     double v = x[0];
 #pragma unroll
@@ -1136,6 +1166,8 @@ __global__ void k_edges_f32(const double *e, int n, float *e32) {
     if (i < n) e32[i] = __double2float_rn(e[i]);
 }
 
+#endif  // BH_FILL_TU
+
 template <int DIM>
 __global__ void k_find_bins(FillP p, int32_t *out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1149,6 +1181,7 @@ __global__ void k_find_bins(FillP p, int32_t *out) {
     }
 }
 
+#ifndef BH_FILL_TU
 // packed = [content | sumw2 | stats | entries], content = count + sumw.
 __global__ void k_pack(int G, int K, const unsigned long long *count, const double *sumw, const double *sumw2,
                        const double *stats, const unsigned long long *entries, double *out) {
@@ -1174,5 +1207,7 @@ __global__ void k_unpack(int G, int K, unsigned long long *count, double *sumw, 
         else *entries = (unsigned long long)v;
     }
 }
+
+#endif  // BH_FILL_TU
 
 }  // namespace bh

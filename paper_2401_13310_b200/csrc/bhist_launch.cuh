@@ -1,0 +1,157 @@
+// bhist_launch.cuh — host-side launch dispatch for the templated fill kernels.
+//
+// The fill templates (k_fill, k_fill_f32, k_fill_expr, k_part_scatter) have a few
+// hundred instantiations; each (DIM, weighted) pair is compiled in its own translation
+// unit (bhist_fill_d<DIM><u|w>.cu, built in parallel) behind the plain functions
+// declared at the bottom, which bhist.cu calls.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/bhist.h"
+#include "bhist_kernels.cuh"
+#include "bhist_sort.cuh"
+
+namespace bh {
+
+struct LaunchCfg {
+    int strategy;
+    bool weighted, vec, vsm;
+    int vm;                      // 0 fixed axes only, 1 variable tables in smem, 2 in global
+    int grid;
+    size_t smem;
+};
+
+template <int DIM, bool W, int SINK, bool VEC, int VM>
+cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    auto kern = k_fill<DIM, W, SINK, VEC, VM>;
+    if (c.smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <int DIM, bool W, int SINK, bool VEC>
+cudaError_t launch_m(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    return c.vm == 0 ? launch_t<DIM, W, SINK, VEC, 0>(p, c, s)
+                     : c.vm == 1 ? launch_t<DIM, W, SINK, VEC, 1>(p, c, s) : launch_t<DIM, W, SINK, VEC, 2>(p, c, s);
+}
+
+template <int DIM, bool W, int SINK>
+cudaError_t launch_v(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    return c.vec ? launch_m<DIM, W, SINK, true>(p, c, s) : launch_m<DIM, W, SINK, false>(p, c, s);
+}
+
+template <int DIM, bool W>
+cudaError_t launch_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    switch (c.strategy) {
+    case BH_STRATEGY_PRIV:
+        if constexpr (W) {
+            if (p.replicas > 1) return launch_v<DIM, W, SINK_PRIVA>(p, c, s);
+        }
+        return launch_v<DIM, W, SINK_PRIV>(p, c, s);
+    case BH_STRATEGY_CACHE: return launch_v<DIM, W, SINK_CACHE>(p, c, s);
+    default: return launch_v<DIM, W, SINK_GLOBAL>(p, c, s);
+    }
+}
+
+
+template <int DIM, bool W, int VM, int RC>
+cudaError_t launch_part1(const FillP &p, const PartP &q, int grid, size_t smem, cudaStream_t s) {
+    auto kern = k_part_scatter<DIM, W, VM, RC>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, kPartThreads, smem, s>>>(p, q);
+    return cudaGetLastError();
+}
+
+template <int DIM, bool W, int RC>
+cudaError_t launch_part1_r(const FillP &p, const PartP &q, int vm, int grid, size_t smem, cudaStream_t s) {
+    return vm == 0 ? launch_part1<DIM, W, 0, RC>(p, q, grid, smem, s)
+                   : vm == 1 ? launch_part1<DIM, W, 1, RC>(p, q, grid, smem, s) : launch_part1<DIM, W, 2, RC>(p, q, grid, smem, s);
+}
+
+template <int DIM, bool W>
+cudaError_t launch_part1_v(const FillP &p, const PartP &q, int vm, int rc, int grid, size_t smem, cudaStream_t s) {
+    if (rc == 1) return launch_part1_r<DIM, W, 1>(p, q, vm, grid, smem, s);
+    if constexpr (W) return launch_part1_r<DIM, W, 4>(p, q, vm, grid, smem, s);
+    else return launch_part1_r<DIM, W, 8>(p, q, vm, grid, smem, s);
+}
+
+template <int DIM, bool W, int SINK>
+cudaError_t launch_f32_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    auto kern = c.vm == 0 ? k_fill_f32<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_f32<DIM, W, SINK, 1> : k_fill_f32<DIM, W, SINK, 2>;
+    if (c.smem > 48 * 1024) {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+        if (r != cudaSuccess) return r;
+    }
+    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <int DIM, bool W>
+cudaError_t launch_f32_w(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
+    switch (c.strategy) {
+    case BH_STRATEGY_PRIV:
+        if constexpr (W) {
+            if (p.replicas > 1) return launch_f32_s<DIM, W, SINK_PRIVA>(p, c, s);
+        }
+        return launch_f32_s<DIM, W, SINK_PRIV>(p, c, s);
+    case BH_STRATEGY_CACHE: return launch_f32_s<DIM, W, SINK_CACHE>(p, c, s);
+    default: return launch_f32_s<DIM, W, SINK_GLOBAL>(p, c, s);
+    }
+}
+
+
+template <int DIM, bool W, int SINK>
+cudaError_t launch_expr_s(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
+    auto kern = c.vm == 0 ? k_fill_expr<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_expr<DIM, W, SINK, 1> : k_fill_expr<DIM, W, SINK, 2>;
+    if (c.smem > 48 * 1024) {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+        if (r != cudaSuccess) return r;
+    }
+    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p, e);
+    return cudaGetLastError();
+}
+
+template <int DIM, bool W>
+cudaError_t launch_expr_w(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
+    switch (c.strategy) {
+    case BH_STRATEGY_PRIV:
+        if constexpr (W) {
+            if (p.replicas > 1) return launch_expr_s<DIM, W, SINK_PRIVA>(p, e, c, s);
+        }
+        return launch_expr_s<DIM, W, SINK_PRIV>(p, e, c, s);
+    case BH_STRATEGY_CACHE: return launch_expr_s<DIM, W, SINK_CACHE>(p, e, c, s);
+    default: return launch_expr_s<DIM, W, SINK_GLOBAL>(p, e, c, s);
+    }
+}
+
+
+
+// one definition per (DIM, W) in bhist_fill_d<DIM><u|w>.cu
+template <int DIM, bool W> cudaError_t fill_launch(const FillP &p, const LaunchCfg &c, cudaStream_t s);
+template <int DIM, bool W> cudaError_t fill_launch_f32(const FillP &p, const LaunchCfg &c, cudaStream_t s);
+template <int DIM, bool W> cudaError_t fill_launch_expr(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s);
+template <int DIM, bool W> cudaError_t fill_launch_part1(const FillP &p, const PartP &q, int vm, int rc, int grid, size_t smem, cudaStream_t s);
+
+#define BH_DEFINE_FILL_TU(DIM, W)                                                                          \
+    template <> cudaError_t fill_launch<DIM, W>(const FillP &p, const LaunchCfg &c, cudaStream_t s) {      \
+        return launch_s<DIM, W>(p, c, s);                                                                  \
+    }                                                                                                      \
+    template <> cudaError_t fill_launch_f32<DIM, W>(const FillP &p, const LaunchCfg &c, cudaStream_t s) {  \
+        return launch_f32_w<DIM, W>(p, c, s);                                                              \
+    }                                                                                                      \
+    template <> cudaError_t fill_launch_expr<DIM, W>(const FillP &p, const ExprP &e, const LaunchCfg &c,   \
+                                                     cudaStream_t s) {                                     \
+        return launch_expr_w<DIM, W>(p, e, c, s);                                                          \
+    }                                                                                                      \
+    template <> cudaError_t fill_launch_part1<DIM, W>(const FillP &p, const PartP &q, int vm, int rc,      \
+                                                      int grid, size_t smem, cudaStream_t s) {             \
+        return launch_part1_v<DIM, W>(p, q, vm, rc, grid, smem, s);                                        \
+    }
+
+}  // namespace bh

@@ -1,0 +1,468 @@
+// bhist_sort.cuh — SORT strategy: two-pass partitioned fill for large bin spaces.
+//
+// The north star's "sort-then-segmented-reduce path for large 2D/3D bin spaces":
+// a one-digit radix partition of the global bin index followed by a per-partition
+// shared-memory reduction.  A 1M-bin TH2D/TH3D does not fit one SM's shared memory
+// (the paper's per-block copy, assumes it does), and adding
+// straight into the L2-resident histogram costs one L2 atomic per event (GLOBAL /
+// CACHE, ~1e11 events/s).  Here:
+//
+//   pass 1 (k_part_scatter): the three steps of PAPER.md:126 up to the bin index --
+//     FindBin per axis, global bin g, the GetStats sums in registers -- then the
+//     event's record (local bin l = g mod 2^pb, and w) is ranked within its
+//     partition p = g >> pb (warp-aggregated shared-memory counters), the tile's
+//     records are sorted by partition in shared memory and written out with
+//     coalesced 16-byte stores, plus one row of segment offsets per tile.
+//   plan   (k_part_plan): per-partition record totals -> prefix -> pass-2 balance.
+//   pass 2 (k_part_reduce): each CTA owns a contiguous stretch of the (partition,
+//     tile) order of about equal record count; the partition's 2^pb bins live in
+//     shared memory (u32 counts / double2 (sumw, sumw2) with 128-bit CAS, equal bins
+//     warp-aggregated first), and are added to the global bins once per partition
+//     the CTA touched (the merge stage of PAPER.md:162-165).
+//
+// Records cost 2 B (unit) or 10 B (weighted) per event written + read back, instead of
+// one L2 atomic per event; no shared-memory state is bigger than 128 KB.
+#pragma once
+#include "bhist_kernels.cuh"
+
+namespace bh {
+
+constexpr int kPartThreads = 1024;                   // pass 1: 1 CTA per SM
+// events per thread per tile; a staged tile (NCOL columns) is <= 64 KB
+__host__ __device__ constexpr int part_ev(int dim, bool w) { return dim + (w ? 1 : 0) >= 3 ? 2 : 4; }
+constexpr int kPartMaxP = 2048;                      // partitions (bins / 2^pb) supported
+constexpr int kReduceThreads = 1024;                 // pass 2: 1 CTA per SM owns 128 KB of bins
+
+struct PartP {
+    uint16_t *rec_l;            // [ntiles * kPartTile] local bin, tile-major, partition-sorted within a tile
+    double *rec_w;              // weighted: the weights, same order
+    uint32_t *offs;             // [ntiles * (P + 1)] segment starts of each tile
+    unsigned long long *cnt;    // [P] records per partition (pass 1 adds; plan reads and zeroes)
+    unsigned long long *cp;     // [P + 1] exclusive prefix of cnt (plan writes)
+    int32_t P, pb, ntiles;
+    int32_t tile;               // events per tile (kPartThreads * part_ev)
+    int32_t ts;                 // scratch slots per tile (>= tile + P*(RC-1), multiple of 8)
+};
+
+// ------------------------------------------------------------------ pass 1
+// Segments are padded to RC records with the sentinel 0xffff (never a local bin: pb <= 15)
+// so that pass 2 reads them in aligned RC-record chunks; a tile's records occupy
+// q.ts >= tile + P*(RC-1) slots of the scratch.
+constexpr uint16_t kPartPad = 0xffffu;
+constexpr int kPartStages = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done)
+                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` (UBLKCP.S.G)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Pass 1.  One CTA of kPartThreads per SM; each tile's columns (and weights) are
+// staged in shared memory by TMA bulk copies, kPartStages tiles in flight, so HBM
+// streams while the CTA bins, ranks and scatters the previous tile.  Tiles that are
+// partial or whose columns are not 16-byte aligned are loaded by the threads instead.
+template <int DIM, bool W, int VM, int RC>
+__global__ void __launch_bounds__(kPartThreads, 1) k_part_scatter(FillP p, PartP q) {
+    constexpr int NCOL = DIM + (W ? 1 : 0);
+    constexpr int kEv = part_ev(DIM, W);
+    constexpr int kTile = kPartThreads * kEv;
+    constexpr uint32_t kStageBytes = (uint32_t)NCOL * kTile * 8u;
+    extern __shared__ __align__(16) unsigned char smem[];
+    // layout: [stage 0..S-1: NCOL x f64[tile]] [mbar S x u64] [stage_w f64[ts] (W)] [stage_l u16[ts]]
+    //         [cnt u32[P]] [start u32[P+1]] [axis tables (VM 1, at tab_off)]
+    const int ts = q.ts;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + kPartStages * kStageBytes);
+    unsigned char *rec = smem + kPartStages * kStageBytes + 8 * kPartStages;
+    double *stw = reinterpret_cast<double *>(rec);
+    uint16_t *stl = reinterpret_cast<uint16_t *>(rec + (W ? 8 * (size_t)ts : 0));
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(rec + (W ? 8 * (size_t)ts : 0) + 2 * (size_t)ts);
+    uint32_t *start = cnt + q.P;
+    const int P = q.P, pb = q.pb;
+    const uint32_t lmask = (1u << pb) - 1u;
+    const int n = (int)p.n;                          // one launch covers < 2^31 events
+    const double *col[NCOL];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) col[a] = p.x[a];
+    if (W) col[NCOL - 1] = p.w;
+    bool aligned = true;
+#pragma unroll
+    for (int a = 0; a < NCOL; ++a) aligned &= (reinterpret_cast<uintptr_t>(col[a]) & 15) == 0;
+    auto tma_ok = [&](int t) { return aligned && t < q.ntiles && (t + 1) * kTile <= n; };
+    auto issue = [&](int t, int st) {                // thread 0 only
+        double *dst = reinterpret_cast<double *>(smem + st * kStageBytes);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(mbar + st, kStageBytes);
+#pragma unroll
+        for (int a = 0; a < NCOL; ++a) bulk_g2s(dst + a * kTile, col[a] + (size_t)t * kTile, kTile * 8u, mbar + st);
+    };
+
+    if constexpr (VM == 1) stage_axes<DIM>(p.ax, smem);
+    for (int i = threadIdx.x; i < P; i += kPartThreads) cnt[i] = 0u;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kPartStages; ++st) mbar_init(mbar + st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int st = 0; st < kPartStages; ++st) {
+            const int t = blockIdx.x + st * gridDim.x;
+            if (tma_ok(t)) issue(t, st);
+        }
+    }
+    __syncthreads();
+
+    Acc<DIM, W> acc;
+    acc.zero();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t phase = 0;                              // bit st: parity of stage st's next completion
+    int k = 0;
+    for (int t = blockIdx.x; t < q.ntiles; t += gridDim.x, ++k) {
+        const int st = k % kPartStages;
+        const double *sx = reinterpret_cast<const double *>(smem + st * kStageBytes);
+        const int e0 = t * kTile;
+        const int m = min(kTile, n - e0);
+        if (tma_ok(t)) {
+            mbar_wait(mbar + st, (phase >> st) & 1u);
+            phase ^= 1u << st;
+        } else {                                     // partial / unaligned tile: the threads load it
+            double *dx = reinterpret_cast<double *>(smem + st * kStageBytes);
+            for (int i = threadIdx.x; i < m; i += kPartThreads)
+#pragma unroll
+                for (int a = 0; a < NCOL; ++a) dx[a * kTile + i] = __ldcs(col[a] + e0 + i);
+            __syncthreads();
+        }
+        // step (1), per axis -> global bin; step (3) stats; rank in partition
+        int pp[kEv];
+        uint32_t key[kEv];                           // rank << 16 | local bin
+        double wk[kEv];                              // the weights again, for the scatter
+#pragma unroll
+        for (int u = 0; u < kEv; ++u) {
+            const int i = u * kPartThreads + threadIdx.x;
+            const bool ok = i < m;
+            double x[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) x[a] = sx[a * kTile + i];
+            const double w = W ? sx[(NCOL - 1) * kTile + i] : 1.0;
+            wk[u] = w;
+            int g = 0, mul = 1;
+            bool inr = true;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                const int b = find_bin<VM>(p.ax[a], x[a], smem);
+                inr &= (b >= 1) & (b <= p.ax[a].n);
+                g += b * mul;
+                if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
+            }
+            if (ok && inr) acc.add(x, w);            // in range only (R6)
+            pp[u] = ok ? (int)((uint32_t)g >> pb) : -1;
+            // the returned old count is the rank (equal addresses of a warp are resolved
+            // by the shared-memory atomic unit)
+            key[u] = ((uint32_t)g & lmask) | (ok ? atomicAdd(cnt + pp[u], 1u) << 16 : 0u);
+        }
+        __syncthreads();                             // (A) stage consumed, counts complete
+        if (threadIdx.x == 0) {
+            const int tn = t + kPartStages * gridDim.x;
+            if (tma_ok(tn)) issue(tn, st);           // refill this stage with a later tile
+        }
+        if (warp == 0) {                             // padded exclusive scan; pads; counts
+            uint32_t run = 0;
+            uint32_t *orow = q.offs + (size_t)t * (P + 1);
+            for (int c0 = 0; c0 < P; c0 += 32) {
+                const int i = c0 + lane;
+                const uint32_t v = i < P ? cnt[i] : 0u;
+                const uint32_t vp = (v + RC - 1) / RC * RC;
+                uint32_t inc = vp;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t uu = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += uu;
+                }
+                if (i < P) {
+                    const uint32_t s0 = run + inc - vp;
+                    start[i] = s0;
+                    orow[i] = s0;
+                    cnt[i] = 0u;
+                    for (uint32_t j = s0 + v; j < s0 + vp; ++j) {
+                        stl[j] = kPartPad;
+                        if (W) stw[j] = 0.0;
+                    }
+                    if (v) atomicAdd(q.cnt + i, (unsigned long long)v);
+                }
+                run += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            if (lane == 0) { start[P] = run; orow[P] = run; }
+        }
+        __syncthreads();                             // (B)
+#pragma unroll
+        for (int u = 0; u < kEv; ++u) {              // records -> partition-sorted staging
+            if (pp[u] >= 0) {
+                const uint32_t pos = start[pp[u]] + (key[u] >> 16);
+                stl[pos] = (uint16_t)(key[u] & 0xffffu);
+                if (W) stw[pos] = wk[u];
+            }
+        }
+        __syncthreads();                             // (C)
+        const int tot = (int)start[P];               // padded record count of the tile
+        uint4 *ol = reinterpret_cast<uint4 *>(q.rec_l + (size_t)t * ts);
+        for (int i = threadIdx.x; i < (tot + 7) / 8; i += kPartThreads) ol[i] = reinterpret_cast<const uint4 *>(stl)[i];
+        if (W) {
+            uint4 *ow = reinterpret_cast<uint4 *>(q.rec_w + (size_t)t * ts);
+            for (int i = threadIdx.x; i < (tot + 1) / 2; i += kPartThreads) ow[i] = reinterpret_cast<const uint4 *>(stw)[i];
+        }
+        // the next tile rewrites the staging only after its barrier (A), when every
+        // thread has finished this copy
+    }
+    acc.finalize_unit();
+    block_stats_finish<Acc<DIM, W>::K>(p, acc.s);
+}
+
+#ifndef BH_FILL_TU
+// ------------------------------------------------------------------ plan
+// One warp: cp = exclusive prefix of cnt (records per partition); cnt is zeroed for
+// the next chunk.
+__global__ void k_part_plan(PartP q) {
+    const int lane = threadIdx.x;
+    unsigned long long run = 0;
+    for (int c0 = 0; c0 < q.P; c0 += 32) {
+        const int i = c0 + lane;
+        const unsigned long long v = i < q.P ? q.cnt[i] : 0ull;
+        unsigned long long inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (i < q.P) { q.cp[i] = run + inc - v; q.cnt[i] = 0ull; }
+        run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) q.cp[q.P] = run;
+}
+
+#endif  // BH_FILL_TU
+
+// ------------------------------------------------------------------ pass 2
+// Position X in [0, R] of the virtual record order (partition-major, then tile) ->
+// (partition, tile), assuming a partition's records spread evenly over the tiles.
+// Monotone in X, so consecutive CTAs cover every (partition, tile) pair exactly once.
+__device__ __forceinline__ void part_pos(const PartP &q, unsigned long long X, int &pp, int &tt) {
+    const unsigned long long R = q.cp[q.P];
+    if (X >= R) { pp = q.P; tt = 0; return; }
+    int lo = 0, hi = q.P - 1;                        // last partition with cp[p] <= X
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (q.cp[mid] <= X) lo = mid; else hi = mid - 1;
+    }
+    const unsigned long long c = q.cp[lo + 1] - q.cp[lo];   // > 0, since cp[lo] <= X < cp[lo+1]
+    pp = lo;
+    tt = (int)(((X - q.cp[lo]) * (unsigned long long)q.ntiles) / c);
+}
+
+// Weighted pass 2: a per-thread sticky one-entry cache in front of the shared-memory
+// bins.  A thread adds records of its cached bin in registers; once the cached bin has
+// repeated, other bins go straight to the 128-bit CAS, so a hot bin stays in registers
+// instead of serializing the CTA's warps on one shared-memory cell.
+struct LaneCache {
+    uint32_t l = kPartPad, n = 0;
+    double s1 = 0.0, s2 = 0.0;
+    __device__ __forceinline__ void add(unsigned char *bins, uint32_t rl, double w) {
+        if (rl == l) {
+            ++n;
+            s1 += w;
+            s2 = fma(w, w, s2);
+        } else if (n >= 2) {
+            add2_shared(reinterpret_cast<double2 *>(bins) + rl, w, w * w);
+        } else {
+            if (n) add2_shared(reinterpret_cast<double2 *>(bins) + l, s1, s2);
+            l = rl;
+            n = 1;
+            s1 = w;
+            s2 = w * w;
+        }
+    }
+    __device__ __forceinline__ void flush(unsigned char *bins) {
+        if (n) add2_shared(reinterpret_cast<double2 *>(bins) + l, s1, s2);
+        l = kPartPad;
+        n = 0;
+    }
+};
+
+constexpr int kReduceBatch = 2048;                   // tiles whose segments are balanced at once
+
+// Pass 2.  The CTA's stretch of (partition, tile) pairs is processed in batches of
+// tiles: the segments' chunk counts are prefix-summed in shared memory and every thread
+// takes an equal contiguous range of chunks (so one hot partition with long segments
+// still keeps all 32 warps busy), walking the segments in order.
+template <bool W, int RC>
+__global__ void __launch_bounds__(kReduceThreads, 1) k_part_reduce(FillP p, PartP q) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    // layout: [bins (2^pb cells)] [o0 u32[batch]] [cp u32[batch+1]] [scan scratch u32[32]]
+    const size_t binbytes = (size_t)(W ? 16 : 4) << q.pb;
+    uint32_t *so0 = reinterpret_cast<uint32_t *>(smem + binbytes);
+    uint32_t *scp = so0 + kReduceBatch;
+    uint32_t *wsum = scp + kReduceBatch + 1;
+    const int C = gridDim.x;
+    const unsigned long long R = q.cp[q.P];
+    if (R == 0) return;
+    int pa, ta, pz, tz;
+    part_pos(q, R * blockIdx.x / C, pa, ta);
+    part_pos(q, R * (blockIdx.x + 1) / C, pz, tz);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int P = q.P, nb_full = 1 << q.pb;
+    LaneCache lc;                                    // weighted: hot bins accumulate in registers
+    for (int part = pa; part <= pz && part < P; ++part) {
+        const int t0 = part == pa ? ta : 0;
+        const int t1 = part == pz ? tz : q.ntiles;
+        if (t0 >= t1 || q.cp[part + 1] == q.cp[part]) continue;     // uniform
+        const int gb0 = part << q.pb;
+        const int nb = min(nb_full, p.G - gb0);
+        if (W) {
+            double2 *d = reinterpret_cast<double2 *>(smem);
+            for (int i = threadIdx.x; i < nb; i += kReduceThreads) d[i] = make_double2(0.0, 0.0);
+        } else {
+            uint32_t *c = reinterpret_cast<uint32_t *>(smem);
+            for (int i = threadIdx.x; i < nb; i += kReduceThreads) c[i] = 0u;
+        }
+        for (int tb0 = t0; tb0 < t1; tb0 += kReduceBatch) {
+            const int nt = min(kReduceBatch, t1 - tb0);
+            // chunk counts of the batch's segments -> block-wide exclusive scan
+            constexpr int PER = kReduceBatch / kReduceThreads;
+            uint32_t v[PER], tsum = 0;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int i = threadIdx.x * PER + j;
+                v[j] = 0;
+                if (i < nt) {
+                    const uint32_t *row = q.offs + (size_t)(tb0 + i) * (P + 1) + part;
+                    const uint32_t o0 = __ldg(row);
+                    so0[i] = o0;
+                    v[j] = (__ldg(row + 1) - o0) / RC;
+                }
+                tsum += v[j];
+            }
+            uint32_t inc = tsum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += u;
+            }
+            __syncthreads();                         // previous batch done with scp / wsum
+            if (lane == 31) wsum[warp] = inc;
+            __syncthreads();
+            if (warp == 0) {
+                uint32_t x = wsum[lane], xi = x;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, xi, o);
+                    if (lane >= o) xi += u;
+                }
+                wsum[lane] = xi - x;                 // exclusive warp offsets
+            }
+            __syncthreads();
+            uint32_t run = wsum[warp] + inc - tsum;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int i = threadIdx.x * PER + j;
+                if (i <= nt) scp[i] = run;           // scp[nt] = total
+                run += v[j];
+            }
+            if (threadIdx.x == kReduceThreads - 1 && nt == kReduceBatch) scp[nt] = run;
+            __syncthreads();
+            const uint32_t CT = scp[nt];
+            uint32_t c = (uint32_t)((unsigned long long)CT * threadIdx.x / kReduceThreads);
+            const uint32_t cend = (uint32_t)((unsigned long long)CT * (threadIdx.x + 1) / kReduceThreads);
+            // tile of chunk c: last j with scp[j] <= c
+            int lo = 0, hi = nt - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (scp[mid] <= c) lo = mid; else hi = mid - 1;
+            }
+            int j = lo;
+            constexpr int U = W ? 2 : 4;
+            while (c < cend) {
+                uint16_t l[U][RC];
+                double w[U][RC];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool ok = c + u < cend;
+                    size_t at = 0;
+                    if (ok) {
+                        while (c + u >= scp[j + 1]) ++j;
+                        at = (size_t)(tb0 + j) * q.ts + so0[j] + (size_t)(c + u - scp[j]) * RC;
+                    }
+                    if (RC == 8) {
+                        uint4 vv = make_uint4(~0u, ~0u, ~0u, ~0u);
+                        if (ok) vv = __ldg(reinterpret_cast<const uint4 *>(q.rec_l + at));
+                        const uint32_t uu[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+                        for (int k = 0; k < RC && k < 8; ++k) l[u][k] = (uint16_t)(uu[k >> 1] >> (16 * (k & 1)));
+                    } else if (RC == 4) {
+                        uint2 vv = make_uint2(~0u, ~0u);
+                        if (ok) vv = __ldg(reinterpret_cast<const uint2 *>(q.rec_l + at));
+                        const uint32_t uu[2] = {vv.x, vv.y};
+#pragma unroll
+                        for (int k = 0; k < RC && k < 4; ++k) l[u][k] = (uint16_t)(uu[k >> 1] >> (16 * (k & 1)));
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < RC; ++k) l[u][k] = ok ? __ldg(q.rec_l + at + k) : kPartPad;
+                    }
+                    if (W) {
+                        if (RC % 2 == 0) {
+#pragma unroll
+                            for (int k = 0; k < RC; k += 2) {
+                                double2 vv = make_double2(0.0, 0.0);
+                                if (ok) vv = __ldg(reinterpret_cast<const double2 *>(q.rec_w + at + k));
+                                w[u][k] = vv.x;
+                                w[u][k + 1 < RC ? k + 1 : k] = vv.y;
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < RC; ++k) w[u][k] = ok ? __ldg(q.rec_w + at + k) : 0.0;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int k = 0; k < RC; ++k)
+                        if (l[u][k] != kPartPad) {
+                            if (W) lc.add(smem, l[u][k], w[u][k]);
+                            else asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(smem_u32(smem) + 4u * l[u][k]) : "memory");
+                        }
+                c += U;
+            }
+        }
+        if (W) lc.flush(smem);
+        __syncthreads();
+        // merge stage: this CTA's partial bins of the partition -> global
+        if (W) {
+            const double2 *d = reinterpret_cast<const double2 *>(smem);
+            for (int i = threadIdx.x; i < nb; i += kReduceThreads) {
+                const double2 vv = d[i];
+                if (vv.x != 0.0) atomicAdd(p.sumw + gb0 + i, vv.x);
+                if (vv.y != 0.0) atomicAdd(p.sumw2 + gb0 + i, vv.y);
+            }
+        } else {
+            const uint32_t *cc = reinterpret_cast<const uint32_t *>(smem);
+            for (int i = threadIdx.x; i < nb; i += kReduceThreads)
+                if (cc[i]) atomicAdd(p.count + gb0 + i, (unsigned long long)cc[i]);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace bh

@@ -63,7 +63,8 @@ def test_random_histograms(seed):
     wmode = rng.integers(4)
     w = None if wmode == 0 else (rng.uniform(0.5, 1.5, n) if wmode == 1 else
                                  rng.normal(0, 1, n) if wmode == 2 else np.zeros(n))
-    strategy = int(rng.choice([pkg.BH_STRATEGY_AUTO, pkg.BH_STRATEGY_GLOBAL, pkg.BH_STRATEGY_CACHE]))
+    strategy = int(rng.choice([pkg.BH_STRATEGY_AUTO, pkg.BH_STRATEGY_GLOBAL, pkg.BH_STRATEGY_CACHE,
+                                    pkg.BH_STRATEGY_SORT]))
     offset = int(rng.integers(0, 2))
     splits = int(rng.choice([1, 3]))
     ref = oracle.OracleHist(axes).fill(cols, w).read()

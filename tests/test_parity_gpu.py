@@ -15,7 +15,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 
-STRATS = {"priv": pkg.BH_STRATEGY_PRIV, "global": pkg.BH_STRATEGY_GLOBAL, "cache": pkg.BH_STRATEGY_CACHE}
+STRATS = {"priv": pkg.BH_STRATEGY_PRIV, "global": pkg.BH_STRATEGY_GLOBAL, "cache": pkg.BH_STRATEGY_CACHE,
+          "sort": pkg.BH_STRATEGY_SORT}
 
 
 def _t(a):
@@ -99,7 +100,7 @@ CASES = [("C1", 1_000_000), ("C2", 2_000_003), ("C3", 2_000_001), ("C3W", 1_000_
 
 
 @pytest.mark.parametrize("name,n", CASES)
-@pytest.mark.parametrize("strat", ["auto", "priv", "global", "cache"])
+@pytest.mark.parametrize("strat", ["auto", "priv", "global", "cache", "sort"])
 def test_fill_parity(name, n, strat):
     wl = bhgen.workload(name, n)
     hist = wl.hists[0]
@@ -351,7 +352,7 @@ def test_peaked_small_histograms_replicas(nbins, weighted):
     w = rng.uniform(0.5, 1.5, n) if weighted else None
     axes = [(nbins, 0.0, 1.0)]
     ref = oracle.OracleHist(axes).fill([x], w).read()
-    for s in (pkg.BH_STRATEGY_PRIV, pkg.BH_STRATEGY_CACHE, pkg.BH_STRATEGY_GLOBAL):
+    for s in (pkg.BH_STRATEGY_PRIV, pkg.BH_STRATEGY_CACHE, pkg.BH_STRATEGY_GLOBAL, pkg.BH_STRATEGY_SORT):
         compare(_gpu_fill(axes, [x], w, s), ref, weighted, f"peaked {nbins} strat {s}")
 
 
@@ -555,3 +556,55 @@ def test_fill_f32_mixed_phases_and_tiny():
             h.fill_f32([torch.from_numpy(x).to(DEV), yt[1:]])
         compare(h.read(), ref, False, f"f32 mixed n={n}")
         h.close()
+
+
+# ------------------------------------------------------------------ SORT strategy (two-pass partitioned fill)
+@pytest.mark.parametrize("name,n", [("C3", 1_000_003), ("C3W", 700_001), ("C4", 1_000_000), ("C4W", 600_007)])
+@pytest.mark.parametrize("chunk", [4096, 65_537, 1 << 20])
+def test_sort_many_chunks(name, n, chunk, monkeypatch):
+    # chunks of 1 tile, of a ragged tile count and of many tiles: scratch reuse across
+    # chunks, partial last tiles, partition totals re-zeroed by the plan kernel
+    monkeypatch.setenv("BHIST_SORT_CHUNK", str(chunk))
+    wl = bhgen.workload(name, n)
+    hist = wl.hists[0]
+    axes = oracle.oracle_axes(hist)
+    cols, w = gen_columns(wl, hist, 0, n)
+    ref = oracle.OracleHist(axes).fill(cols, w).read()
+    got = _gpu_fill(axes, cols, w, pkg.BH_STRATEGY_SORT, splits=3)
+    compare(got, ref, hist.weighted, f"{name} sort chunk={chunk}")
+
+
+@pytest.mark.parametrize("shape,weighted", [((6000, 6000), False), ((4000, 4000), True), ((300, 300, 300), False),
+                                            ((130, 1), True)])
+def test_sort_many_partitions_and_ragged_last(shape, weighted):
+    # up to ~2000 partitions (the SORT limit), a last partition shorter than 2^pb, variable
+    # axes in pass 1, and a bin space smaller than one partition
+    rng = np.random.default_rng(sum(shape))
+    n = 1_500_017
+    axes = []
+    cols = []
+    for k, nb in enumerate(shape):
+        if k == 1:
+            axes.append(np.cumsum(rng.uniform(0.5, 1.5, nb + 1)) / nb - 0.6)
+        else:
+            axes.append((nb, -0.1, 1.1))
+        cols.append(rng.uniform(-0.2, 1.3, n))
+    w = rng.uniform(-1.0, 2.0, n) if weighted else None
+    ref = oracle.OracleHist(axes).fill(cols, w).read()
+    compare(_gpu_fill(axes, cols, w, pkg.BH_STRATEGY_SORT), ref, weighted, f"sort {shape}")
+
+
+def test_strategy_resolution():
+    h = pkg.Histogram([(1000, 0.0, 1.0), (1000, 0.0, 1.0)])
+    assert h.strategy(False) == pkg.BH_STRATEGY_CACHE and h.strategy(True) == pkg.BH_STRATEGY_CACHE
+    h.close()
+    h = pkg.Histogram([(1000, 0.0, 1.0), (1000, 0.0, 1.0)], strategy=pkg.BH_STRATEGY_SORT)
+    assert h.strategy(False) == pkg.BH_STRATEGY_SORT and h.strategy(True) == pkg.BH_STRATEGY_SORT
+    h.close()
+    # weighted partitions are 4x smaller: beyond 2048 of them SORT falls back to CACHE
+    h = pkg.Histogram([(5000, 0.0, 1.0), (5000, 0.0, 1.0)], strategy=pkg.BH_STRATEGY_SORT)
+    assert h.strategy(False) == pkg.BH_STRATEGY_SORT and h.strategy(True) == pkg.BH_STRATEGY_CACHE
+    h.close()
+    h = pkg.Histogram([(100, 0.0, 1.0)])
+    assert h.strategy(False) == pkg.BH_STRATEGY_PRIV
+    h.close()

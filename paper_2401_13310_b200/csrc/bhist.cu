@@ -269,8 +269,7 @@ template <bool W, int RC>
 cudaError_t launch_part2(const FillP &p, const PartP &q, int grid, cudaStream_t s) {
     auto kern = k_part_reduce<W, RC>;
     const int smem = ((W ? 16 : 4) << sort_pb(W)) + 4 * (2 * kReduceBatch + 1 + 32);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    if (cudaError_t e = ensure_smem(reinterpret_cast<const void *>(kern), (size_t)smem)) return e;
     kern<<<grid, kReduceThreads, smem, s>>>(p, q);
     return cudaGetLastError();
 }
@@ -834,7 +833,7 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
         used += (size_t)stat_off * mthreads * sizeof(double);
         if (used > budget) return fail(BH_EINVAL, "fused pass needs %zu B of shared memory", used);
         auto kern = k_fill_multi;
-        if (used > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)used));
+        CUDA_TRY(ensure_smem(reinterpret_cast<const void *>(kern), used));
         const int64_t kMaxLaunch = int64_t(1) << 30;   // in-kernel event indices are int32
         for (int64_t off = 0; off < n; off += kMaxLaunch) {
             const int64_t m = std::min(kMaxLaunch, n - off);

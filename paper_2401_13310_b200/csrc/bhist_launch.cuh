@@ -11,7 +11,27 @@
 #include "bhist_kernels.cuh"
 #include "bhist_sort.cuh"
 
+#include <mutex>
+#include <unordered_map>
+
 namespace bh {
+
+// cudaFuncSetAttribute is a driver call (~microseconds); small fills are launch-latency
+// bound, so the dynamic shared-memory limit is raised once per (kernel, device).
+inline cudaError_t ensure_smem(const void *kern, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    static std::mutex mu;
+    static std::unordered_map<uint64_t, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t key = reinterpret_cast<uint64_t>(kern) * 64u + (uint64_t)dev;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done[key] = bytes;
+    return e;
+}
 
 struct LaunchCfg {
     int strategy;
@@ -24,10 +44,7 @@ struct LaunchCfg {
 template <int DIM, bool W, int SINK, bool VEC, int VM>
 cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
     auto kern = k_fill<DIM, W, SINK, VEC, VM>;
-    if (c.smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-        if (e != cudaSuccess) return e;
-    }
+    if (cudaError_t e = ensure_smem(reinterpret_cast<const void *>(kern), c.smem)) return e;
     kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
     return cudaGetLastError();
 }
@@ -60,10 +77,7 @@ cudaError_t launch_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
 template <int DIM, bool W, int VM, int RC>
 cudaError_t launch_part1(const FillP &p, const PartP &q, int grid, size_t smem, cudaStream_t s) {
     auto kern = k_part_scatter<DIM, W, VM, RC>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
+    if (cudaError_t e = ensure_smem(reinterpret_cast<const void *>(kern), smem)) return e;
     kern<<<grid, kPartThreads, smem, s>>>(p, q);
     return cudaGetLastError();
 }
@@ -84,10 +98,7 @@ cudaError_t launch_part1_v(const FillP &p, const PartP &q, int vm, int rc, int g
 template <int DIM, bool W, int SINK>
 cudaError_t launch_f32_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
     auto kern = c.vm == 0 ? k_fill_f32<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_f32<DIM, W, SINK, 1> : k_fill_f32<DIM, W, SINK, 2>;
-    if (c.smem > 48 * 1024) {
-        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-        if (r != cudaSuccess) return r;
-    }
+    if (cudaError_t r = ensure_smem(reinterpret_cast<const void *>(kern), c.smem)) return r;
     kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
     return cudaGetLastError();
 }
@@ -109,10 +120,7 @@ cudaError_t launch_f32_w(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
 template <int DIM, bool W, int SINK>
 cudaError_t launch_expr_s(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
     auto kern = c.vm == 0 ? k_fill_expr<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_expr<DIM, W, SINK, 1> : k_fill_expr<DIM, W, SINK, 2>;
-    if (c.smem > 48 * 1024) {
-        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-        if (r != cudaSuccess) return r;
-    }
+    if (cudaError_t r = ensure_smem(reinterpret_cast<const void *>(kern), c.smem)) return r;
     kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p, e);
     return cudaGetLastError();
 }

@@ -27,7 +27,7 @@
 
 namespace bh {
 
-constexpr int kPartThreads = 1024;                   // pass 1: 1 CTA per SM
+constexpr int kPartThreads = 1024;                   // pass 1: 1 CTA per SM (2 x 512 measured no faster)
 // events per thread per tile; a staged tile (NCOL columns) is <= 64 KB
 __host__ __device__ constexpr int part_ev(int dim, bool w) { return dim + (w ? 1 : 0) >= 3 ? 2 : 4; }
 constexpr int kPartMaxP = 2048;                      // partitions (bins / 2^pb) supported
@@ -339,6 +339,7 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_part_reduce(FillP p, Part
         }
         for (int tb0 = t0; tb0 < t1; tb0 += kReduceBatch) {
             const int nt = min(kReduceBatch, t1 - tb0);
+            __syncthreads();                         // every thread is done with the previous batch
             // chunk counts of the batch's segments -> block-wide exclusive scan
             constexpr int PER = kReduceBatch / kReduceThreads;
             uint32_t v[PER], tsum = 0;
@@ -360,7 +361,6 @@ __global__ void __launch_bounds__(kReduceThreads, 1) k_part_reduce(FillP p, Part
                 const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o) inc += u;
             }
-            __syncthreads();                         // previous batch done with scp / wsum
             if (lane == 31) wsum[warp] = inc;
             __syncthreads();
             if (warp == 0) {

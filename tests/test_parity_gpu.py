@@ -280,16 +280,20 @@ def _gpu_full(name, strategy=pkg.BH_STRATEGY_AUTO, chunk=1 << 25):
             wl.column_ptr(c, off, m, host[j].data_ptr())
         if hist.weighted:
             wl.column_ptr(wl.wcol, off, m, host[-1].data_ptr())
-        h.fill_host([t[:m] for t in host[:len(hist.cols)]], host[-1][:m] if hist.weighted else None)
+        if strategy == pkg.BH_STRATEGY_SORT:     # device-resident fills of whole SORT chunks
+            h.fill([t[:m].to(DEV) for t in host[:len(hist.cols)]], host[-1][:m].to(DEV) if hist.weighted else None)
+        else:
+            h.fill_host([t[:m] for t in host[:len(hist.cols)]], host[-1][:m] if hist.weighted else None)
     r = h.read()
     h.close()
     return wl, r
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
-def test_full_size_against_sharded_oracle(name):
-    wl, got = _gpu_full(name)
+@pytest.mark.parametrize("name,strategy", [("C2", pkg.BH_STRATEGY_AUTO), ("C3", pkg.BH_STRATEGY_AUTO),
+                                           ("C4", pkg.BH_STRATEGY_AUTO), ("C3", pkg.BH_STRATEGY_SORT)])
+def test_full_size_against_sharded_oracle(name, strategy):
+    wl, got = _gpu_full(name, strategy, chunk=(1 << 27) if strategy == pkg.BH_STRATEGY_SORT else (1 << 25))
     ref = oracle_parallel(name, wl.n_events)
     compare(got, ref, wl.hists[0].weighted, f"full {name}")
 
@@ -592,6 +596,17 @@ def test_sort_many_partitions_and_ragged_last(shape, weighted):
     w = rng.uniform(-1.0, 2.0, n) if weighted else None
     ref = oracle.OracleHist(axes).fill(cols, w).read()
     compare(_gpu_fill(axes, cols, w, pkg.BH_STRATEGY_SORT), ref, weighted, f"sort {shape}")
+
+
+@pytest.mark.parametrize("name,n", [("C3", 30_000_001), ("C3W", 6_000_007)])
+def test_sort_pass2_spans_many_tile_batches(name, n):
+    # a pass-2 CTA's stretch of (partition, tile) pairs exceeds one 2048-tile batch
+    wl = bhgen.workload(name, n)
+    hist = wl.hists[0]
+    axes = oracle.oracle_axes(hist)
+    cols, w = gen_columns(wl, hist, 0, n)
+    ref = oracle.OracleHist(axes).fill(cols, w).read()
+    compare(_gpu_fill(axes, cols, w, pkg.BH_STRATEGY_SORT), ref, hist.weighted, f"{name} sort n={n}")
 
 
 def test_strategy_resolution():

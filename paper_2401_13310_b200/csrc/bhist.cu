@@ -167,6 +167,7 @@ FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, cons
     p.stats = h->stats;
     p.entries = h->entries;
     p.entries_add = n;
+    p.wc_off = -1;
     return p;
 }
 
@@ -178,6 +179,7 @@ struct FillPlan {
     LaunchCfg c{};
     AxisP ax[kMaxDim];
     int replicas = 1;
+    int wc_off = -1;     // weighted PRIV: per-warp hot-bin caches (collision-adaptive sink)
 };
 
 bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl) {
@@ -199,9 +201,22 @@ bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl) {
     // PRIV: replicate the private bins into the spare shared memory (up to one copy
     // per warp) so hot bins are not contended across warps
     pl.replicas = 1;
+    pl.wc_off = -1;
+    size_t wcb = 0;
     if (c.strategy == BH_STRATEGY_PRIV) {
-        const size_t spare = h->smem_optin - kStaticSmemReserve - (c.vsm ? tabs : 0);
+        size_t spare = h->smem_optin - kStaticSmemReserve - (c.vsm ? tabs : 0);
         const int cap = threads_of(c.strategy, c.weighted) / 32;
+        // weighted fills get the collision-adaptive sink with per-warp hot-bin caches when
+        // they fit, except a single replica next to variable-axis tables (C2's shape: the
+        // spread-out fill measured fastest with the plain CAS sink)
+        bool has_var = false;
+        for (int a = 0; a < h->dim; ++a) has_var |= h->ax[a].var != 0;
+        const size_t reps0 = spare / std::max<size_t>(sink, 1);
+        const size_t wc_need = (size_t)kWCBytes * cap;
+        if (c.weighted && spare >= sink + wc_need && (reps0 > 1 || !has_var) && !getenv("BHIST_NO_WARP_CACHE")) {
+            wcb = wc_need;
+            spare -= wcb;
+        }
         pl.replicas = (int)std::max<size_t>(1, std::min<size_t>(cap, spare / std::max<size_t>(sink, 1)));
         const char *env = getenv("BHIST_PRIV_REPLICAS");
         if (env) pl.replicas = std::max(1, std::min(pl.replicas, atoi(env)));
@@ -209,8 +224,9 @@ bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl) {
         for (int a = 0; a < h->dim; ++a)
             if (pl.ax[a].var) pl.ax[a].tab_off += (int32_t)((pl.replicas - 1) * sink);
         sink *= pl.replicas;
+        if (wcb) pl.wc_off = (int)(sink + (c.vsm ? tabs : 0));     // behind replicas and tables
     }
-    c.smem = sink + (c.vsm ? tabs : 0);
+    c.smem = sink + (c.vsm ? tabs : 0) + wcb;
     if (c.smem + kStaticSmemReserve > h->smem_optin)
         return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", c.strategy, c.smem,
                     h->smem_optin);
@@ -400,6 +416,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         if (p.peel > m) p.peel = (int32_t)m;
         p.cache_slots = cache_slots_for(c.weighted);
         p.replicas = pl.replicas;
+        p.wc_off = pl.wc_off;
         c.grid = grid_for(h, c, m);
         cudaError_t e;
         switch (h->dim) {
@@ -433,6 +450,7 @@ bh_status fill_device_f32(bh_hist *h, int64_t n, const float *const *coords, con
         p.peel = vec ? (int32_t)std::min<int64_t>(ph ? (16 - ph) / 4 : 0, m) : -1;
         p.cache_slots = cache_slots_for(c.weighted);
         p.replicas = pl.replicas;
+        p.wc_off = pl.wc_off;
         c.grid = grid_for(h, c, m);
         cudaError_t e;
         switch (h->dim) {
@@ -894,6 +912,7 @@ bh_status bh_fill_expr(bh_hist *h, int64_t n, const double *const *cols, int32_t
         p.entries_add = 0;                 // the kernel adds the passing events itself
         p.cache_slots = cache_slots_for(c.weighted);
         p.replicas = pl.replicas;
+        p.wc_off = pl.wc_off;
         c.grid = grid_for(h, c, m);
         cudaError_t r;
         switch (h->dim) {

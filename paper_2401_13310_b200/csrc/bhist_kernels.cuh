@@ -51,6 +51,8 @@ struct FillP {
     int32_t peel;            // vector path: leading events handled one by one (alignment)
     int32_t cache_slots;     // CACHE strategy: shared-memory slots (power of two)
     int32_t replicas;        // PRIV strategy: copies of the private bins (warp w uses w % replicas)
+    int32_t wc_off;          // weighted PRIV: byte offset of the per-warp hot-bin caches (-1: none,
+                             // plain CAS sink; >= 0: collision-adaptive sink SINK_PRIVA)
     unsigned long long *count;   // unit-weight counts [G]
     double *sumw;                // weighted sums [G]
     double *sumw2;               // weighted sums of squares [G]
@@ -361,16 +363,32 @@ __device__ __forceinline__ void add2_shared_grouped(double2 *base, int g, double
 // With R > 1 replicas (small bin spaces) warp w adds into replica w % R, so hot
 // bins are not contended across warps (R = 32: per-warp private histograms); the
 // flush sums the replicas.
+//
+// SINK_PRIVA (weighted) also gives every warp a private direct-mapped cache of kWC hot
+// bins in shared memory: in aggregated mode the leader of a group of >= 2 lanes on one
+// bin adds the group's (sum w, sum w^2) to its warp's cache entry with a plain
+// read-modify-write (the warp is the only writer), claiming the entry if needed (the
+// previous occupant is flushed into the replica).  A peaked weighted histogram thus
+// stops serializing all warps of a replica on a few cells (100x100 Cauchy-peaked fill:
+// 9 -> see DESIGN.md), while spread data never enters aggregated mode.
+constexpr int kWC = 16;
+constexpr int kWCBytes = kWC * 4 + kWC * 16;         // tags int32[kWC], then (s1, s2) double2[kWC]
+
 template <bool W, bool ADAPT>
 struct PrivSink {
     uint32_t sm;         // shared-memory address of this warp's replica
     bool agg;            // ADAPT: the warp's previous add collided -> aggregate this one first
+    unsigned char *wc;   // ADAPT && W: this warp's hot-bin cache
     static constexpr int kCell = W ? 16 : 4;
     static __device__ __forceinline__ size_t stride_of(int G) { return ((size_t)G * kCell + 15) & ~size_t(15); }
-    __device__ __forceinline__ void init(unsigned char *s, int G, int R) {
+    __device__ __forceinline__ void init(unsigned char *s, int G, int R, int wc_off = -1) {
         const size_t stride = stride_of(G);
         sm = (uint32_t)__cvta_generic_to_shared(s + (size_t)((threadIdx.x >> 5) % R) * stride);
         agg = false;
+        if (ADAPT && W) {
+            wc = s + wc_off + (size_t)(threadIdx.x >> 5) * kWCBytes;
+            if ((threadIdx.x & 31) < kWC) reinterpret_cast<int32_t *>(wc)[threadIdx.x & 31] = -1;
+        }
         if (W) {
             for (int i = threadIdx.x; i < R * (int)(stride / 16); i += blockDim.x)
                 reinterpret_cast<double2 *>(s)[i] = make_double2(0.0, 0.0);
@@ -398,13 +416,73 @@ struct PrivSink {
             if (agg) {
                 const unsigned peers = __match_any_sync(act, g);
                 agg = __any_sync(act, __popc(peers) >= 4);
-                if (__any_sync(act, __popc(peers) > 1)) add2_shared_grouped(base, g, w, w * w, act);
-                else add2_shared(base + g, w, w * w);
+                add_aggregated(base, g, w, w * w, act, peers);
             } else {
                 agg = __popc(__ballot_sync(act, add2_shared_count(base + g, w, w * w) > 0)) >= 8;
             }
         } else {
             asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(sm + 4u * (uint32_t)g) : "memory");
+        }
+    }
+    // Aggregated add: group sums by a shuffle walk, then per group leader: hit in the
+    // warp's hot-bin cache -> plain add; miss with a group of >= 2 -> claim the entry (one
+    // claimant per entry, the old occupant flushed into the replica); else CAS.
+    __device__ __forceinline__ void add_aggregated(double2 *base, int g, double w, double w2, unsigned act,
+                                                   unsigned peers) {
+        const int lane = (int)(threadIdx.x & 31);
+        const int rounds = __reduce_max_sync(act, (unsigned)__popc(peers));
+        double s1 = 0.0, s2 = 0.0;
+        unsigned m = peers;
+        for (int k = 0; k < rounds; ++k) {
+            const int src = m ? __ffs(m) - 1 : lane;
+            const double v1 = __shfl_sync(act, w, src), v2 = __shfl_sync(act, w2, src);
+            if (m) { s1 += v1; s2 += v2; m &= m - 1; }
+        }
+        const bool leader = lane == __ffs(peers) - 1;
+        int32_t *tags = reinterpret_cast<int32_t *>(wc);
+        double2 *vals = reinterpret_cast<double2 *>(wc + kWC * 4);
+        const int slot = (int)(((uint32_t)g * 2654435761u) >> 28);   // kWC = 16
+        bool done = false;
+        if (leader && tags[slot] == g) {             // at most one leader holds a slot's tag
+            double2 v = vals[slot];
+            v.x += s1;
+            v.y += s2;
+            vals[slot] = v;
+            done = true;
+        }
+        __syncwarp(act);
+        const bool want = leader && !done && __popc(peers) >= 2;
+        const unsigned wm = __ballot_sync(act, want);
+        if (want) {
+            const unsigned sp = __match_any_sync(wm, slot);
+            if (lane == __ffs(sp) - 1) {             // this slot's claimant
+                const int t = tags[slot];
+                if (t >= 0) {
+                    const double2 v = vals[slot];
+                    add2_shared(base + t, v.x, v.y);
+                }
+                tags[slot] = g;
+                vals[slot] = make_double2(s1, s2);
+                done = true;
+            }
+        }
+        if (leader && !done) add2_shared(base + g, s1, s2);
+        __syncwarp(act);
+    }
+    // Before the block barrier of the merge stage: hot-bin caches -> this warp's replica.
+    __device__ __forceinline__ void drain() {
+        if (ADAPT && W) {
+            __syncwarp();
+            const int lane = (int)(threadIdx.x & 31);
+            if (lane < kWC) {
+                int32_t *tags = reinterpret_cast<int32_t *>(wc);
+                const double2 *vals = reinterpret_cast<const double2 *>(wc + kWC * 4);
+                if (tags[lane] >= 0) {
+                    double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
+                    add2_shared(base + tags[lane], vals[lane].x, vals[lane].y);
+                    tags[lane] = -1;
+                }
+            }
         }
     }
     // Merge stage of PAPER.md:162-165: each block adds its local bins (summed over the
@@ -445,6 +523,7 @@ struct GlobalSink {
             atomicAdd(pp->count + g, 1ull);
         }
     }
+    __device__ __forceinline__ void drain() {}
     __device__ __forceinline__ void flush(const FillP &, const unsigned char *) {}
 };
 
@@ -520,6 +599,7 @@ struct CacheSink {
             }
         }
     }
+    __device__ __forceinline__ void drain() {}
     __device__ __forceinline__ void flush(const FillP &p, const unsigned char *) {
         for (int i = threadIdx.x; i < S; i += blockDim.x) {
             const uint32_t k = keys[i];
@@ -583,7 +663,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     if constexpr (SINK == SINK_GLOBAL) sink.pp = &p;
     if constexpr (SINK == SINK_CACHE) sink.pp = &p;
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
-    else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas);
+    else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas, p.wc_off);
     else sink.init(smem, p.G);
     if constexpr (VM == 1) stage_axes<DIM>(p.ax, smem);
     if constexpr (SINK != SINK_GLOBAL || VM == 1) __syncthreads();
@@ -666,6 +746,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     }
 
     if constexpr (SINK != SINK_GLOBAL) {
+        sink.drain();
         __syncthreads();
         sink.flush(p, smem);
     }
@@ -687,7 +768,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     Sink_t sink;
     if constexpr (SINK == SINK_GLOBAL || SINK == SINK_CACHE) sink.pp = &p;
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
-    else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas);
+    else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas, p.wc_off);
     else sink.init(smem, p.G);
     if constexpr (VM == 1) stage_axes<DIM>(p.ax, smem);
     if constexpr (SINK != SINK_GLOBAL || VM == 1) __syncthreads();
@@ -730,6 +811,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
         if (tid < nscalar) one(tid < base ? tid : tail0 + (tid - base));
     }
     if constexpr (SINK != SINK_GLOBAL) {
+        sink.drain();
         __syncthreads();
         sink.flush(p, smem);
     }
@@ -800,7 +882,7 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
     Sink_t sink;
     if constexpr (SINK == SINK_GLOBAL || SINK == SINK_CACHE) sink.pp = &p;
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
-    else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas);
+    else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas, p.wc_off);
     else sink.init(smem, p.G);
     if constexpr (VM == 1) stage_axes<DIM>(p.ax, smem);
     if constexpr (SINK != SINK_GLOBAL || VM == 1) __syncthreads();
@@ -824,6 +906,7 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
     for (int o = 16; o > 0; o >>= 1) passed += __shfl_xor_sync(0xffffffffu, passed, o);
     if ((threadIdx.x & 31) == 0 && passed) atomicAdd(p.entries, (unsigned long long)passed);
     if constexpr (SINK != SINK_GLOBAL) {
+        sink.drain();
         __syncthreads();
         sink.flush(p, smem);
     }

@@ -65,7 +65,7 @@ cudaError_t launch_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
     switch (c.strategy) {
     case BH_STRATEGY_PRIV:
         if constexpr (W) {
-            if (p.replicas > 1) return launch_v<DIM, W, SINK_PRIVA>(p, c, s);
+            if (p.wc_off >= 0) return launch_v<DIM, W, SINK_PRIVA>(p, c, s);
         }
         return launch_v<DIM, W, SINK_PRIV>(p, c, s);
     case BH_STRATEGY_CACHE: return launch_v<DIM, W, SINK_CACHE>(p, c, s);
@@ -108,7 +108,7 @@ cudaError_t launch_f32_w(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
     switch (c.strategy) {
     case BH_STRATEGY_PRIV:
         if constexpr (W) {
-            if (p.replicas > 1) return launch_f32_s<DIM, W, SINK_PRIVA>(p, c, s);
+            if (p.wc_off >= 0) return launch_f32_s<DIM, W, SINK_PRIVA>(p, c, s);
         }
         return launch_f32_s<DIM, W, SINK_PRIV>(p, c, s);
     case BH_STRATEGY_CACHE: return launch_f32_s<DIM, W, SINK_CACHE>(p, c, s);
@@ -130,7 +130,7 @@ cudaError_t launch_expr_w(const FillP &p, const ExprP &e, const LaunchCfg &c, cu
     switch (c.strategy) {
     case BH_STRATEGY_PRIV:
         if constexpr (W) {
-            if (p.replicas > 1) return launch_expr_s<DIM, W, SINK_PRIVA>(p, e, c, s);
+            if (p.wc_off >= 0) return launch_expr_s<DIM, W, SINK_PRIVA>(p, e, c, s);
         }
         return launch_expr_s<DIM, W, SINK_PRIV>(p, e, c, s);
     case BH_STRATEGY_CACHE: return launch_expr_s<DIM, W, SINK_CACHE>(p, e, c, s);

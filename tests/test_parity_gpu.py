@@ -360,6 +360,20 @@ def test_peaked_small_histograms_replicas(nbins, weighted):
         compare(_gpu_fill(axes, [x], w, s), ref, weighted, f"peaked {nbins} strat {s}")
 
 
+@pytest.mark.parametrize("nb", [10, 50, 100])
+def test_peaked_weighted_2d_warp_cache(nb):
+    # weighted 2D fills of C5's peaked columns (Cauchy x, narrow Gaussian y): the
+    # collision-adaptive sink with per-warp hot-bin caches (claims, evictions, drain)
+    rng = np.random.default_rng(7 * nb)
+    n = 3_000_017
+    x = 0.505 + 0.002 * np.tan(np.pi * (rng.random(n) - 0.5))
+    y = rng.normal(0.5, 0.05, n)
+    w = rng.uniform(-0.5, 1.5, n)
+    axes = [(nb, 0.0, 1.0), (nb, 0.0, 1.0)]
+    ref = oracle.OracleHist(axes).fill([x, y], w).read()
+    compare(_gpu_fill(axes, [x, y], w, pkg.BH_STRATEGY_PRIV, splits=2), ref, True, f"peaked 2D {nb}")
+
+
 def test_bench_two_ranks_exchange(tmp_path):
     """bench.py's N>1 path end to end on one GPU: 2 torchrun ranks (gloo backend so both
     may share cuda:0), contiguous shards, pack -> all-reduce -> unpack every step; the

@@ -26,6 +26,27 @@ for name in ("C1", "C2", "C3W", "C4"):
         H.find_bins(cols)
         H.read()
         H.close()
+# SORT strategy: pass 1 (TMA-staged), plan, pass 2; several chunks and a partial last tile
+os.environ["BHIST_SORT_CHUNK"] = "8192"
+for name in ("C3", "C3W", "C4"):
+    wl = bhgen.workload(name, n)
+    h = wl.hists[0]
+    cols = [torch.from_numpy(wl.column(c, 0, n)).to(dev) for c in h.cols]
+    w = torch.from_numpy(wl.column(wl.wcol, 0, n)).to(dev) if h.weighted else None
+    H = pkg.Histogram(h.axes_spec(), strategy=pkg.BH_STRATEGY_SORT)
+    H.fill(cols, w)
+    H.fill([c[1:] for c in cols], None if w is None else w[1:])   # unaligned: thread-loaded tiles
+    H.read()
+    H.close()
+# peaked weighted 2D histograms: per-warp hot-bin caches (1 and several replicas)
+y = torch.from_numpy(rng.normal(0.5, 0.05, n)).to(dev)
+xp = torch.from_numpy(0.505 + 0.002 * np.tan(np.pi * (rng.random(n) - 0.5))).to(dev)
+wp = torch.from_numpy(rng.uniform(0.5, 1.5, n)).to(dev)
+for nb in (10, 100):
+    H = pkg.Histogram([(nb, 0.0, 1.0), (nb, 0.0, 1.0)])
+    H.fill([xp, y], wp)
+    H.read()
+    H.close()
 # peaked weighted small histogram: replicas + collision-adaptive CAS
 x = torch.from_numpy(0.505 + 0.002 * np.tan(np.pi * (rng.random(n) - 0.5))).to(dev)
 w = torch.from_numpy(rng.uniform(0.5, 1.5, n)).to(dev)

@@ -188,6 +188,9 @@ def measure_secondary(name: str, steps: int, warmup: int, local: int) -> dict:
     same protocol as the headline (CUDA events around each bh_fill; inputs >> L2)."""
     import torch
     import paper_2401_13310_b200 as pkg
+    name, _, strat_name = name.partition("+")      # e.g. "C3+sort": opt-in strategy
+    strategy = {"": pkg.BH_STRATEGY_AUTO, "sort": pkg.BH_STRATEGY_SORT, "cache": pkg.BH_STRATEGY_CACHE,
+                "global": pkg.BH_STRATEGY_GLOBAL, "priv": pkg.BH_STRATEGY_PRIV}[strat_name]
     wl = get_workload(name)
     h = wl.hists[0]
     N = wl.n_events
@@ -201,7 +204,7 @@ def measure_secondary(name: str, steps: int, warmup: int, local: int) -> dict:
     cols = [dev_col(c) for c in h.cols]
     w = dev_col(wl.wcol) if h.weighted else None
     del host
-    H = pkg.Histogram(h.axes_spec(), device=local)
+    H = pkg.Histogram(h.axes_spec(), device=local, strategy=strategy)
     st = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for i in range(warmup + steps):
@@ -433,7 +436,7 @@ def main():
     ap.add_argument("--strategy", default="auto", choices=["auto", "priv", "global", "cache", "exact", "sort"])
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend for N>1")
     ap.add_argument("--events", type=int, default=0, help="override events per GPU (tests)")
-    ap.add_argument("--secondary", default="C1S,C1F,C2F",
+    ap.add_argument("--secondary", default="C1S,C1F,C2F,C3+sort",
                     help="comma list of extra configs measured device-resident after the headline ('' = none)")
     ap.add_argument("--cpu-sample", type=int, default=50_000_000)
     ap.add_argument("--ref-sample", type=int, default=1 << 23)

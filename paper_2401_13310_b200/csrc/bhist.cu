@@ -580,7 +580,7 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
             P.e = de;
             P.guide = dg2;
             P.e32 = de32;
-            P.g16 = (A.nbins - 1) < 65536 ? 1 : 0;
+            P.g16 = (A.nbins - 1) < 16384 ? 2 : ((A.nbins - 1) < 65536 ? 1 : 0);
             k_build_guide<<<(gc + 1 + 255) / 256, 256>>>(P, dg2);
             k_edges_f32<<<(A.nbins + 1 + 255) / 256, 256>>>(de, A.nbins + 1, de32);
             if (cudaGetLastError() != cudaSuccess) return cleanup(fail(BH_ECUDA, "guide build launch failed"));

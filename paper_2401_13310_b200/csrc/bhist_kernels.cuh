@@ -37,7 +37,8 @@ struct AxisP {
     double gscale;           // variable: gcells / (e[n] - e[0])
     const float *e32;        // variable: RN-to-float32 copy of the edges (device), staged in smem
     int32_t tab_off;         // variable + VSM: byte offset of [e32 | guide] in dynamic smem
-    int32_t g16;             // variable + VSM: guide staged as uint16 (n-1 < 65536)
+    int32_t g16;             // variable + VSM: guide staged as uint32 (0), uint16 (1, n-1 < 65536) or
+                             // packed uint16 (2, n-1 < 16384): guide[c] << 2 | min(guide[c+1]-guide[c], 3)
 };
 
 struct FillP {
@@ -139,7 +140,7 @@ __device__ __forceinline__ int find_bin_var_global(const AxisP &a, double x) {
 // RN-to-float is monotone, so e32_i < x32 implies e_i < x and e32_i > x32 implies
 // e_i > x; only a float tie needs the exact float64 edge (global, ~1e-3 of events
 // on the C2 axis).  The result is therefore identical to the float64 search.
-template <bool G16>
+template <int GM>   // guide mode: 0 uint32, 1 uint16, 2 packed uint16 (AxisP::g16)
 __device__ __forceinline__ int find_bin_var_smem(const AxisP &a, double x, const unsigned char *tab) {
     if (x < a.xmin) return 0;
     if (!(x < a.xmax)) return a.n + 1;
@@ -147,7 +148,11 @@ __device__ __forceinline__ int find_bin_var_smem(const AxisP &a, double x, const
     const unsigned char *gt = tab + ((4 * (a.n + 1) + 15) & ~15);
     const int c = guide_cell(a, x);
     int lo, hi;
-    if (G16) {
+    if (GM == 2) {                       // one load per event: range start and edge count
+        const uint32_t v = reinterpret_cast<const uint16_t *>(gt)[c];
+        lo = (int)(v >> 2);
+        hi = (v & 3u) < 3u ? lo + (int)(v & 3u) : (int)(reinterpret_cast<const uint16_t *>(gt)[c + 1] >> 2);
+    } else if (GM == 1) {
         lo = reinterpret_cast<const uint16_t *>(gt)[c];
         hi = reinterpret_cast<const uint16_t *>(gt)[c + 1];
     } else {
@@ -164,6 +169,11 @@ __device__ __forceinline__ int find_bin_var_smem(const AxisP &a, double x, const
     return 1 + lo;
 }
 
+__device__ __forceinline__ int find_bin_var_smem_any(const AxisP &a, double x, const unsigned char *tab) {
+    return a.g16 == 2 ? find_bin_var_smem<2>(a, x, tab)
+                      : (a.g16 ? find_bin_var_smem<1>(a, x, tab) : find_bin_var_smem<0>(a, x, tab));
+}
+
 // VM (variable-axis mode, a template constant): 0 = every axis fixed (no variable-axis
 // code at all), 1 = variable-axis tables staged in shared memory, 2 = tables in global.
 template <int VM>
@@ -173,7 +183,7 @@ __device__ __forceinline__ int find_bin(const AxisP &a, double x, const unsigned
 #endif
     if (VM == 0 || !a.var) return find_bin_fixed(a, x);
     if (VM == 1) {
-        return a.g16 ? find_bin_var_smem<true>(a, x, smem + a.tab_off) : find_bin_var_smem<false>(a, x, smem + a.tab_off);
+        return find_bin_var_smem_any(a, x, smem + a.tab_off);
     }
     return find_bin_var_global(a, x);
 }
@@ -197,7 +207,13 @@ __device__ __forceinline__ void stage_axes(const AxisP *ax, unsigned char *smem)
         float *e32 = reinterpret_cast<float *>(smem + ax[a].tab_off);
         for (int i = threadIdx.x; i <= ax[a].n; i += blockDim.x) e32[i] = ax[a].e32[i];
         unsigned char *gt = smem + ax[a].tab_off + ((4 * (ax[a].n + 1) + 15) & ~15);
-        if (ax[a].g16) {
+        if (ax[a].g16 == 2) {            // the last cell's entry (c + 1 = gcells) is read only via cnt 3
+            for (int i = threadIdx.x; i <= ax[a].gcells; i += blockDim.x) {
+                const uint32_t g0 = ax[a].guide[i];
+                const uint32_t d = i < ax[a].gcells ? ax[a].guide[i + 1] - g0 : 0u;
+                reinterpret_cast<uint16_t *>(gt)[i] = (uint16_t)((g0 << 2) | (d < 3u ? d : 3u));
+            }
+        } else if (ax[a].g16) {
             for (int i = threadIdx.x; i <= ax[a].gcells; i += blockDim.x)
                 reinterpret_cast<uint16_t *>(gt)[i] = (uint16_t)ax[a].guide[i];
         } else {
@@ -1150,8 +1166,7 @@ __global__ void __launch_bounds__(1024, 1) k_fill_multi(const __grid_constant__ 
                 int b;
                 if (!A.var) b = find_bin_fixed(A, xa[a]);
                 else if (A.tab_off >= 0)
-                    b = A.g16 ? find_bin_var_smem<true>(A, xa[a], smem + A.tab_off)
-                              : find_bin_var_smem<false>(A, xa[a], smem + A.tab_off);
+                    b = find_bin_var_smem_any(A, xa[a], smem + A.tab_off);
                 else b = find_bin_var_global(A, xa[a]);
                 inr &= (b >= 1) & (b <= A.n);
                 g += b * mul;

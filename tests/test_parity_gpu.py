@@ -360,6 +360,26 @@ def test_peaked_small_histograms_replicas(nbins, weighted):
         compare(_gpu_fill(axes, [x], w, s), ref, weighted, f"peaked {nbins} strat {s}")
 
 
+@pytest.mark.parametrize("nbins", [3, 9_999, 16_384, 16_385, 20_000])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_variable_axis_guide_modes(nbins, weighted):
+    # shared-memory guide tables: packed uint16 (n-1 < 16384, one load per event, cells
+    # with >= 3 edges read the next entry) and plain uint16 above; edges with ties
+    rng = np.random.default_rng(nbins)
+    widths = rng.uniform(0.2, 1.8, nbins) ** 4          # very uneven widths: crowded cells
+    edges = np.concatenate([[0.0], np.cumsum(widths)]) / widths.sum()
+    edges[-1] = 1.0
+    n = 1_000_003
+    x = np.concatenate([rng.normal(0.5, 0.3, n - 4000), rng.choice(edges, 2000),
+                        np.nextafter(rng.choice(edges, 2000), -np.inf)])
+    w = rng.uniform(0.5, 1.5, n) if weighted else None
+    ref = oracle.OracleHist([edges]).fill([x], w).read()
+    compare(_gpu_fill([edges], [x], w), ref, weighted, f"guide modes n={nbins}")
+    h = pkg.Histogram([edges])
+    assert np.array_equal(h.find_bins([_t(x)]).cpu().numpy(), oracle.OracleHist([edges]).find_bins([x]))
+    h.close()
+
+
 @pytest.mark.parametrize("nb", [10, 50, 100])
 def test_peaked_weighted_2d_warp_cache(nb):
     # weighted 2D fills of C5's peaked columns (Cauchy x, narrow Gaussian y): the

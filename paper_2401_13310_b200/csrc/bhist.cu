@@ -182,10 +182,18 @@ struct FillPlan {
     int wc_off = -1;     // weighted PRIV: per-warp hot-bin caches (collision-adaptive sink)
 };
 
-bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl) {
+// Small fills (e.g. the paper's 32768-event bulks) cannot amortize PRIV's
+// per-CTA zeroing and flushing of all G bins: below ~2 G events per SM, AUTO sends them
+// through CACHE (warp-aggregated, hot-bin safe) instead.
+bool small_fill(const bh_hist *h, int64_t n) { return n < 2 * h->G * (int64_t)h->nsm; }
+
+bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n) {
     LaunchCfg &c = pl.c;
     c.weighted = weighted;
     c.strategy = resolve_one_pass(h, c.weighted);
+    if (c.strategy == BH_STRATEGY_PRIV && (h->strategy == BH_STRATEGY_AUTO || h->strategy == BH_STRATEGY_EXACT) &&
+        small_fill(h, n))
+        c.strategy = BH_STRATEGY_CACHE;
     size_t sink = sink_bytes(h, c.strategy, c.weighted);
     // variable-axis tables go to shared memory behind the sink when they fit
     size_t tabs = 0;
@@ -237,7 +245,9 @@ bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl) {
 // to amortize zeroing + flushing its private bins.
 int grid_for(const bh_hist *h, const LaunchCfg &c, int64_t m) {
     const int nt = threads_of(c.strategy, c.weighted);
-    int64_t want_per_block = (int64_t)nt * 8;
+    // small fills are latency-bound: spread them over many SMs (>= 2 events per thread);
+    // PRIV blocks must still amortize zeroing + flushing their G private bins
+    int64_t want_per_block = (int64_t)nt * 2;
     if (c.strategy == BH_STRATEGY_PRIV) want_per_block = std::max<int64_t>(want_per_block, 4 * h->G);
     int64_t grid = (m + want_per_block - 1) / want_per_block;
     return (int)std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)h->nsm * resident_blocks(c.strategy)));
@@ -397,7 +407,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
     if (w && h->strategy == BH_STRATEGY_EXACT) return fill_exact(h, n, coords, w, s);
     if (resolve_strategy(h, w != nullptr) == BH_STRATEGY_SORT) return fill_sort(h, n, coords, w, s);
     FillPlan pl;
-    if (bh_status r = plan_fill(h, w != nullptr, pl)) return r;
+    if (bh_status r = plan_fill(h, w != nullptr, pl, n)) return r;
     LaunchCfg &c = pl.c;
     const int64_t kMaxLaunch = int64_t(1) << 30;   // in-kernel event indices are int32
     for (int64_t off = 0; off < n; off += kMaxLaunch) {
@@ -433,7 +443,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
 // float32 columns (see k_fill_f32); EXACT is not offered for float32 weights (uses AUTO).
 bh_status fill_device_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, cudaStream_t s) {
     FillPlan pl;
-    if (bh_status r = plan_fill(h, w != nullptr, pl)) return r;
+    if (bh_status r = plan_fill(h, w != nullptr, pl, n)) return r;
     LaunchCfg &c = pl.c;
     const int64_t kMaxLaunch = int64_t(1) << 30;
     for (int64_t off = 0; off < n; off += kMaxLaunch) {
@@ -583,6 +593,13 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
             P.g16 = (A.nbins - 1) < 16384 ? 2 : ((A.nbins - 1) < 65536 ? 1 : 0);
             k_build_guide<<<(gc + 1 + 255) / 256, 256>>>(P, dg2);
             k_edges_f32<<<(A.nbins + 1 + 255) / 256, 256>>>(de, A.nbins + 1, de32);
+            unsigned char *img = nullptr;
+            P.tab_bytes = (int32_t)axis_table_bytes(P);
+            ALLOC(img, P.tab_bytes);
+            h->axis_mem.push_back(img);
+            cudaMemset(img, 0, P.tab_bytes);
+            k_table_image<<<(std::max(A.nbins, gc) + 1 + 255) / 256, 256>>>(P, dg2, img);
+            P.tab_img = reinterpret_cast<const uint4 *>(img);
             if (cudaGetLastError() != cudaSuccess) return cleanup(fail(BH_ECUDA, "guide build launch failed"));
         }
     }
@@ -900,7 +917,7 @@ bh_status bh_fill_expr(bh_hist *h, int64_t n, const double *const *cols, int32_t
     if (n == 0) return BH_OK;
     DeviceGuard dg(h->device);
     FillPlan pl;
-    if (bh_status r = plan_fill(h, e.weight_reg >= 0, pl)) return r;
+    if (bh_status r = plan_fill(h, e.weight_reg >= 0, pl, n)) return r;
     LaunchCfg &c = pl.c;
     const int64_t kMaxLaunch = int64_t(1) << 30;
     for (int64_t off = 0; off < n; off += kMaxLaunch) {

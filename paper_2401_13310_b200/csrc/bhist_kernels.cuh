@@ -39,6 +39,8 @@ struct AxisP {
     int32_t tab_off;         // variable + VSM: byte offset of [e32 | guide] in dynamic smem
     int32_t g16;             // variable + VSM: guide staged as uint32 (0), uint16 (1, n-1 < 65536) or
                              // packed uint16 (2, n-1 < 16384): guide[c] << 2 | min(guide[c+1]-guide[c], 3)
+    const uint4 *tab_img;    // variable: the shared-memory image [e32 | guide in mode g16], built at create
+    int32_t tab_bytes;       // its size (multiple of 16)
 };
 
 struct FillP {
@@ -198,27 +200,28 @@ __device__ __forceinline__ int find_bin_deferred(const AxisP &a, double x, const
     return find_bin<VM>(a, x, smem);
 }
 
-// Copy each variable axis' float32 edges and guide table into shared memory.
+// Copy each variable axis' table image (float32 edges + guide, built once at create in
+// the staged layout) into shared memory: 16-byte loads, four per thread in flight.
 template <int DIM>
 __device__ __forceinline__ void stage_axes(const AxisP *ax, unsigned char *smem) {
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
         if (!ax[a].var) continue;
-        float *e32 = reinterpret_cast<float *>(smem + ax[a].tab_off);
-        for (int i = threadIdx.x; i <= ax[a].n; i += blockDim.x) e32[i] = ax[a].e32[i];
-        unsigned char *gt = smem + ax[a].tab_off + ((4 * (ax[a].n + 1) + 15) & ~15);
-        if (ax[a].g16 == 2) {            // the last cell's entry (c + 1 = gcells) is read only via cnt 3
-            for (int i = threadIdx.x; i <= ax[a].gcells; i += blockDim.x) {
-                const uint32_t g0 = ax[a].guide[i];
-                const uint32_t d = i < ax[a].gcells ? ax[a].guide[i + 1] - g0 : 0u;
-                reinterpret_cast<uint16_t *>(gt)[i] = (uint16_t)((g0 << 2) | (d < 3u ? d : 3u));
+        const uint4 *src = ax[a].tab_img;
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + ax[a].tab_off);
+        const int n16 = ax[a].tab_bytes / 16;
+        for (int base = 0; base < n16; base += 4 * (int)blockDim.x) {
+            uint4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = base + k * (int)blockDim.x + (int)threadIdx.x;
+                if (i < n16) v[k] = __ldg(src + i);
             }
-        } else if (ax[a].g16) {
-            for (int i = threadIdx.x; i <= ax[a].gcells; i += blockDim.x)
-                reinterpret_cast<uint16_t *>(gt)[i] = (uint16_t)ax[a].guide[i];
-        } else {
-            for (int i = threadIdx.x; i <= ax[a].gcells; i += blockDim.x)
-                reinterpret_cast<uint32_t *>(gt)[i] = ax[a].guide[i];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = base + k * (int)blockDim.x + (int)threadIdx.x;
+                if (i < n16) dst[i] = v[k];
+            }
         }
     }
 }
@@ -296,10 +299,13 @@ __device__ __forceinline__ void block_stats_finish(const FillP &p, double (&s)[K
     __syncthreads();
     if (!last) return;
     __threadfence();
-    if (threadIdx.x < K) {
+    // warp k sums statistic k over the blocks: lane-strided loads in flight together, then
+    // a fixed butterfly (deterministic for a given grid); small fills are latency-bound
+    if (warp < K) {
         double t = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(p.partials + (size_t)b * K + threadIdx.x);
-        p.stats[threadIdx.x] += t;
+        for (unsigned b = lane; b < gridDim.x; b += 32) t += __ldcg(p.partials + (size_t)b * K + warp);
+        t = warp_sum_fixed(t);
+        if (lane == 0) p.stats[warp] += t;
     }
     if (threadIdx.x == 0) {
         *p.entries += (unsigned long long)p.entries_add;
@@ -506,6 +512,40 @@ struct PrivSink {
     __device__ __forceinline__ void flush(const FillP &p, const unsigned char *s) {
         const int G = p.G, R = p.replicas;
         const size_t stride = stride_of(G);
+        // few bins, many replicas (small fills are latency-bound): S lanes per bin sum
+        // interleaved replicas, then a shuffle tree combines them
+        int S = 1;
+        while (S < 32 && 2 * S <= R && (size_t)2 * S * G <= blockDim.x) S *= 2;
+        if (S > 1) {
+            const int lane = (int)(threadIdx.x & 31), sub = lane & (S - 1);
+            const int bins_per_pass = (int)blockDim.x / S;
+            for (int i0 = 0; i0 < G; i0 += bins_per_pass) {
+                const int i = i0 + (int)threadIdx.x / S;
+                const bool ok = i < G;
+                if (W) {
+                    double a = 0.0, b = 0.0;
+                    for (int r = sub; ok && r < R; r += S) {
+                        const double2 u = reinterpret_cast<const double2 *>(s + r * stride)[i];
+                        a += u.x;
+                        b += u.y;
+                    }
+                    for (int o = S / 2; o > 0; o >>= 1) {
+                        a += __shfl_xor_sync(0xffffffffu, a, o);
+                        b += __shfl_xor_sync(0xffffffffu, b, o);
+                    }
+                    if (ok && sub == 0) {
+                        if (a != 0.0) atomicAdd(p.sumw + i, a);
+                        if (b != 0.0) atomicAdd(p.sumw2 + i, b);
+                    }
+                } else {
+                    uint32_t v = 0;
+                    for (int r = sub; ok && r < R; r += S) v += reinterpret_cast<const uint32_t *>(s + r * stride)[i];
+                    for (int o = S / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    if (ok && sub == 0 && v) atomicAdd(p.count + i, (unsigned long long)v);
+                }
+            }
+            return;
+        }
         if (W) {
             for (int i = threadIdx.x; i < G; i += blockDim.x) {
                 double2 v = reinterpret_cast<const double2 *>(s)[i];
@@ -1262,6 +1302,26 @@ __global__ void k_build_guide(AxisP a, uint32_t *guide) {
 __global__ void k_edges_f32(const double *e, int n, float *e32) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) e32[i] = __double2float_rn(e[i]);
+}
+
+// Shared-memory image of a variable axis: [e32 (n+1 floats, padded to 16 B) | guide in
+// mode a.g16]; the packed mode stores guide[c] << 2 | min(guide[c+1] - guide[c], 3).
+__global__ void k_table_image(AxisP a, const uint32_t *guide, unsigned char *img) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    float *e32 = reinterpret_cast<float *>(img);
+    if (i <= a.n) e32[i] = __double2float_rn(a.e[i]);
+    unsigned char *gt = img + ((4 * (a.n + 1) + 15) & ~15);
+    if (i <= a.gcells) {
+        const uint32_t g0 = guide[i];
+        if (a.g16 == 2) {
+            const uint32_t d = i < a.gcells ? guide[i + 1] - g0 : 0u;
+            reinterpret_cast<uint16_t *>(gt)[i] = (uint16_t)((g0 << 2) | (d < 3u ? d : 3u));
+        } else if (a.g16 == 1) {
+            reinterpret_cast<uint16_t *>(gt)[i] = (uint16_t)g0;
+        } else {
+            reinterpret_cast<uint32_t *>(gt)[i] = g0;
+        }
+    }
 }
 
 #endif  // BH_FILL_TU

@@ -182,6 +182,37 @@ def run_reference(args):
     return 0
 
 
+_PAR = {}
+
+
+def _oracle_shard(args):
+    """Worker of time_oracle_parallel: the oracle on events [a, b) of the forked columns."""
+    import oracle
+    a, b = args
+    wl, cols = _PAR["wl"], _PAR["cols"]
+    for h in wl.hists:
+        o = oracle.OracleHist(oracle.oracle_axes(h))
+        o.fill([cols[c][a:b] for c in h.cols], cols[wl.wcol][a:b] if h.weighted else None)
+    return b - a
+
+
+def time_oracle_parallel(wl, sample_events: int, threads: int) -> float:
+    """Wall time of the same oracle sharded over `threads` forked processes (contiguous
+    event ranges, SURVEY.md §8(d)'s T-thread baseline); the merge of the partial states
+    (one add per bin) is not included."""
+    import multiprocessing as mp
+    need = sorted({c for h in wl.hists for c in h.cols} | ({wl.wcol} if wl.wcol is not None else set()))
+    _PAR["wl"], _PAR["cols"] = wl, {c: wl.column(c, 0, sample_events) for c in need}
+    bounds = [((sample_events * r) // threads, (sample_events * (r + 1)) // threads) for r in range(threads)]
+    with mp.get_context("fork").Pool(threads) as pool:
+        pool.map(_oracle_shard, [(0, 1)] * threads)            # warm the workers
+        t0 = time.perf_counter()
+        pool.map(_oracle_shard, bounds)
+        dt = time.perf_counter() - t0
+    _PAR.clear()
+    return dt
+
+
 # ------------------------------------------------------------------ secondary rows (device-resident only)
 def measure_secondary(name: str, steps: int, warmup: int, local: int) -> dict:
     """Device-resident events/s and roofline fraction of another config's fill kernel,
@@ -271,7 +302,11 @@ def run_gpu(args):
     torch.cuda.synchronize()
 
     strat_code = {"auto": 0, "priv": 1, "global": 2, "cache": 3, "exact": 4, "sort": 5}[args.strategy]
-    Hs = [pkg.Histogram(h.axes_spec(), device=local, strategy=strat_code) for h in hists]
+    per_hist = dict(kv.split("=") for kv in args.hist_strategy.split(",") if kv)   # e.g. "6=sort"
+    Hs = [pkg.Histogram(h.axes_spec(), device=local,
+                        strategy={"auto": 0, "priv": 1, "global": 2, "cache": 3, "exact": 4, "sort": 5}[
+                            per_hist.get(str(i), args.strategy)])
+          for i, h in enumerate(hists)]
     multi = len(Hs) > 1
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -378,11 +413,17 @@ def run_gpu(args):
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
+    cpu_par = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sample = min(N, args.cpu_sample)
         ts = time_oracle(wl, sample, repeats=1)
         cpu = {"value": sample / ts[0], "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"events [0, {sample}) of the {wl.name} stream, single-thread C oracle (Neumaier sums)"}
+        threads = os.cpu_count() or 1
+        if threads > 1:
+            tp = time_oracle_parallel(wl, sample, threads)
+            cpu_par = {"value": sample / tp, "unit": UNIT, "cores": threads, "kind": "oracle",
+                       "sample": f"the same events sharded over {threads} forked processes (all host cores)"}
 
     if rank == 0:
         peak, peak_src = hbm_peak()
@@ -415,6 +456,7 @@ def run_gpu(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "cpu_baseline_all_cores": cpu_par,
             "secondary": secondary or None,
         }
         print(json.dumps(line), flush=True)
@@ -434,6 +476,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--strategy", default="auto", choices=["auto", "priv", "global", "cache", "exact", "sort"])
+    ap.add_argument("--hist-strategy", default="",
+                    help="per-histogram strategies of a multi-histogram config, e.g. '6=sort'")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend for N>1")
     ap.add_argument("--events", type=int, default=0, help="override events per GPU (tests)")
     ap.add_argument("--secondary", default="C1S,C1F,C2F,C3+sort",

@@ -84,9 +84,11 @@ typedef struct {
  *        max|w|.  Unit-weight fills are exact in every mode;
  *        bh_fill_expr uses AUTO.  Slower (six L2 integer atomics per event). */
 #define BH_STRATEGY_EXACT 4
-/* SORT   two-pass partitioned fill for bin spaces too large for PRIV (opt-in: faster
- *        than CACHE on spread-out unit-weight data, slower on peaked or weighted data,
- *        so AUTO uses CACHE there): pass 1 bins each event, accumulates the stats and writes a record
+/* SORT   two-pass partitioned fill for bin spaces too large for PRIV (faster than CACHE
+ *        on spread-out unit-weight data, slower on peaked or weighted data: AUTO uses it
+ *        only for unit-weight fills of >= ~39M events once an asynchronous probe of a
+ *        sample of an earlier such fill found no partition holding > 5% of the events;
+ *        bh_get_strategy then reports SORT for unit weights): pass 1 bins each event, accumulates the stats and writes a record
  *        (bin mod 2^pb, w) into a partition-sorted scratch buffer (p = bin >> pb,
  *        pb = 15 unit / 13 weighted; at most 2048 partitions); pass 2 reduces each
  *        partition in shared memory and adds it to the bins once per CTA.  The

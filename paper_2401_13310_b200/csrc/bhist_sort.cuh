@@ -232,6 +232,44 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_part_scatter(FillP p, PartP
 }
 
 #ifndef BH_FILL_TU
+// ------------------------------------------------------------------ hotness probe (AUTO)
+// One CTA bins an evenly strided sample of a fill's events (global-memory FindBin) and
+// writes the largest partition's count: AUTO uses SORT for later large unit-weight fills
+// only when no partition is hot (a hot partition serializes pass 1's rank atomics).
+constexpr int kProbeHash = 4096;
+
+template <int DIM>
+__global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, int samples, unsigned int *out) {
+    // out[0]: largest partition count; out[1]: largest count of a hashed bin bucket
+    // (4096 buckets: a single hot bin shows up as one large bucket)
+    extern __shared__ unsigned int pc[];
+    unsigned int *hc = pc + P;
+    for (int i = threadIdx.x; i < P + kProbeHash; i += blockDim.x) pc[i] = 0u;
+    __syncthreads();
+    const int64_t stride = p.n / samples;
+    for (int k = threadIdx.x; k < samples; k += blockDim.x) {
+        const int64_t e = (int64_t)k * stride;
+        int g = 0, mul = 1;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            g += find_bin(p.ax[a], p.x[a][e]) * mul;
+            if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
+        }
+        atomicAdd(pc + ((uint32_t)g >> pb), 1u);
+        atomicAdd(hc + (((uint32_t)g * 2654435761u) >> 20), 1u);
+    }
+    __syncthreads();
+    unsigned int m = 0, mh = 0;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) m = max(m, pc[i]);
+    for (int i = threadIdx.x; i < kProbeHash; i += blockDim.x) mh = max(mh, hc[i]);
+    m = __reduce_max_sync(0xffffffffu, m);
+    mh = __reduce_max_sync(0xffffffffu, mh);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, m);
+        atomicMax(out + 1, mh);
+    }
+}
+
 // ------------------------------------------------------------------ plan
 // One warp: cp = exclusive prefix of cnt (records per partition); cnt is zeroed for
 // the next chunk.

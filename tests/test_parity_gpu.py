@@ -643,6 +643,35 @@ def test_sort_pass2_spans_many_tile_batches(name, n):
     compare(_gpu_fill(axes, cols, w, pkg.BH_STRATEGY_SORT), ref, hist.weighted, f"{name} sort n={n}")
 
 
+@pytest.mark.parametrize("peaked", [False, True])
+def test_auto_sort_probe(peaked):
+    # AUTO + large unit-weight fills of a 1M-bin TH2D: the first fill runs CACHE and probes
+    # a sample; later fills use SORT only for spread-out data.  Counts are exact either way.
+    n = 40_000_000
+    g = torch.Generator(device=DEV).manual_seed(5)
+    def col():
+        u = torch.rand(n, dtype=torch.float64, device=DEV, generator=g)
+        return 0.505 + 0.002 * torch.tan(np.pi * (u - 0.5)) if peaked else u
+    x, y = col(), col()                      # peaked: C4's Cauchy shape on both axes
+    axes = [(1000, 0.0, 1.0), (1000, 0.0, 1.0)]
+    h = pkg.Histogram(axes)
+    ref = pkg.Histogram(axes, strategy=pkg.BH_STRATEGY_CACHE)
+    assert h.strategy(False) == pkg.BH_STRATEGY_CACHE
+    for _ in range(3):
+        h.fill([x, y])
+        ref.fill([x, y])
+        torch.cuda.synchronize()
+    assert h.strategy(False) == (pkg.BH_STRATEGY_CACHE if peaked else pkg.BH_STRATEGY_SORT)
+    assert h.strategy(True) == pkg.BH_STRATEGY_CACHE
+    a, b = h.read(), ref.read()
+    assert a["entries"] == b["entries"] == 3 * n
+    assert np.array_equal(a["content"], b["content"])
+    assert a["stats"][0] == b["stats"][0]
+    np.testing.assert_allclose(a["stats"], b["stats"], rtol=1e-12, atol=0)
+    h.close()
+    ref.close()
+
+
 def test_strategy_resolution():
     h = pkg.Histogram([(1000, 0.0, 1.0), (1000, 0.0, 1.0)])
     assert h.strategy(False) == pkg.BH_STRATEGY_CACHE and h.strategy(True) == pkg.BH_STRATEGY_CACHE

@@ -94,6 +94,32 @@ def test_find_bins_random_axes():
         assert np.array_equal(got, ref), (trial, np.flatnonzero(got != ref)[:5])
 
 
+def test_find_bins_fixed_near_integer_quotients():
+    # the fixed-axis FindBin is the exact IEEE expression trunc(RN(RN(n (x - xmin)) / D))
+    # (reading R2); stress it where n (x - xmin) / D lies within a few ulps of an integer,
+    # on axes with awkward ranges (non-dyadic widths, offsets, tiny and huge scales)
+    rng = np.random.default_rng(99)
+    for trial in range(24):
+        n = int(rng.choice([1, 3, 7, 10, 100, 999, 1000, 4096, 10007, 65536, 1_000_003]))
+        lo = float(rng.uniform(-1e3, 1e3)) * float(10 ** rng.uniform(-6, 3))
+        width = float(10 ** rng.uniform(-8, 8)) * float(rng.uniform(1, 10))
+        hi = lo + width
+        k = rng.integers(0, n + 1, 300_000)
+        base = lo + k * ((hi - lo) / n)
+        xs = [base]
+        up = dn = base
+        for _ in range(4):
+            up, dn = np.nextafter(up, np.inf), np.nextafter(dn, -np.inf)
+            xs += [up, dn]
+        x = np.concatenate(xs)
+        ax = (n, lo, hi)
+        ref = oracle.OracleHist([ax]).find_bins([x])
+        h = pkg.Histogram([ax])
+        got = h.find_bins([_t(x)]).cpu().numpy()
+        h.close()
+        assert np.array_equal(got, ref), (trial, ax, np.flatnonzero(got != ref)[:5])
+
+
 # ------------------------------------------------------------------ fills vs oracle
 CASES = [("C1", 1_000_000), ("C2", 2_000_003), ("C3", 2_000_001), ("C3W", 1_000_001), ("C4", 2_000_000),
          ("C4W", 1_000_003)]

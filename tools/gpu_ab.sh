@@ -1,6 +1,5 @@
 #!/bin/bash
-# A/B of two library builds on the default C2 bench (alternating, 2 runs each)
-for i in 1 2; do for lib in paper_2401_13310_b200/libbhist.so build_ab/libbhist_split.so; do
-BHIST_LIBRARY=$PWD/$lib timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print('$lib C2 %.4g ev/s frac %.3f'%(d['value'], d['roofline']['frac']))"; done; done
-BHIST_LIBRARY=$PWD/build_ab/libbhist_split.so timeout 600 python -m pytest tests/test_parity_gpu.py -q -m gpu -x -k "C2 and fill_parity" 2>&1 | tail -1
+# A/B of library builds on the default C2 bench and C3/C4 (alternating)
+for lib in paper_2401_13310_b200/libbhist.so build_ab/libbhist_g.so; do for c in C2 C3 C4 C1S; do
+BHIST_LIBRARY=$PWD/$lib timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.readline()); print('$lib $c %.4g ev/s frac %.3f launch %.3f'%(d['value'], d['roofline']['frac'], d['roofline']['launch_ms']))"; done; done

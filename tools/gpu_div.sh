@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/ -q -m gpu --timeout=600 -x > gpurun_out/pytest_div.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_div.log
+timeout 1200 python -m pytest tests/ -q -m gpu --timeout=600 > gpurun_out/pytest_div.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_div.log; grep -E "^FAILED|^E  " gpurun_out/pytest_div.log | head -10
 run() { timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" "$@" 2>>gpurun_out/d.err | python -c "
 import json,sys
 for l in sys.stdin:

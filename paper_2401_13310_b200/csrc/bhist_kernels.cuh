@@ -396,21 +396,83 @@ __device__ __forceinline__ void add2_shared_grouped(double2 *base, int g, double
 constexpr int kWC = 16;
 constexpr int kWCBytes = kWC * 4 + kWC * 16;         // tags int32[kWC], then (s1, s2) double2[kWC]
 
+// A warp's private direct-mapped cache of hot weighted bins (PRIVA; in front of CACHE's
+// slots it measured slower on C4w, 4.36 vs 3.48 ms, and is not used there).
+// absorb(): called by every lane of `act` after the group sums; if `act` is the full
+// warp, a group leader whose bin is cached adds with a plain read-modify-write (the
+// converged warp is the only writer, and one leader per bin); a leader of a group of
+// >= 2 that misses claims the entry -- one claimant per entry, the previous occupant
+// spilled through `spill(bin, s1, s2)`.  Returns whether this lane's group was absorbed.
+struct WarpHot {
+    unsigned char *wc;
+    __device__ __forceinline__ void init(unsigned char *base) {
+        wc = base + (size_t)(threadIdx.x >> 5) * kWCBytes;
+        if ((threadIdx.x & 31) < kWC) reinterpret_cast<int32_t *>(wc)[threadIdx.x & 31] = -1;
+    }
+    template <typename Spill>
+    __device__ __forceinline__ bool absorb(unsigned act, bool leader, int gsize, int g, double s1, double s2,
+                                           Spill spill) {
+        // Plain read-modify-writes are safe only if no other lanes of this warp can be in
+        // here at the same time: with independent thread scheduling two diverged subsets
+        // of a warp (e.g. the vector loop's last pairs and the scalar tail) may both be
+        // adding.  So only a converged full warp uses the cache; partial masks go to the
+        // caller's atomic path.
+        if (act != 0xffffffffu) return false;
+        const int lane = (int)(threadIdx.x & 31);
+        int32_t *tags = reinterpret_cast<int32_t *>(wc);
+        double2 *vals = reinterpret_cast<double2 *>(wc + kWC * 4);
+        const int slot = (int)(((uint32_t)g * 2654435761u) >> 28);   // kWC = 16
+        bool done = false;
+        __syncwarp();                    // earlier cache writes of every lane are visible
+        if (leader && tags[slot] == g) {
+            double2 v = vals[slot];
+            v.x += s1;
+            v.y += s2;
+            vals[slot] = v;
+            done = true;
+        }
+        __syncwarp(act);
+        const bool want = leader && !done && gsize >= 2;
+        const unsigned wm = __ballot_sync(act, want);
+        if (want) {
+            const unsigned sp = __match_any_sync(wm, slot);
+            if (lane == __ffs(sp) - 1) {
+                const int t = tags[slot];
+                if (t >= 0) spill(t, vals[slot].x, vals[slot].y);
+                tags[slot] = g;
+                vals[slot] = make_double2(s1, s2);
+                done = true;
+            }
+        }
+        __syncwarp(act);
+        return done;
+    }
+    template <typename Spill>
+    __device__ __forceinline__ void drain(Spill spill) {
+        __syncwarp();
+        const int lane = (int)(threadIdx.x & 31);
+        if (lane < kWC) {
+            int32_t *tags = reinterpret_cast<int32_t *>(wc);
+            const double2 *vals = reinterpret_cast<const double2 *>(wc + kWC * 4);
+            if (tags[lane] >= 0) spill(tags[lane], vals[lane].x, vals[lane].y);
+            tags[lane] = -1;
+        }
+        __syncwarp();
+    }
+};
+
 template <bool W, bool ADAPT>
 struct PrivSink {
     uint32_t sm;         // shared-memory address of this warp's replica
     bool agg;            // ADAPT: the warp's previous add collided -> aggregate this one first
-    unsigned char *wc;   // ADAPT && W: this warp's hot-bin cache
+    WarpHot hot;         // ADAPT && W: this warp's hot-bin cache
     static constexpr int kCell = W ? 16 : 4;
     static __device__ __forceinline__ size_t stride_of(int G) { return ((size_t)G * kCell + 15) & ~size_t(15); }
     __device__ __forceinline__ void init(unsigned char *s, int G, int R, int wc_off = -1) {
         const size_t stride = stride_of(G);
         sm = (uint32_t)__cvta_generic_to_shared(s + (size_t)((threadIdx.x >> 5) % R) * stride);
         agg = false;
-        if (ADAPT && W) {
-            wc = s + wc_off + (size_t)(threadIdx.x >> 5) * kWCBytes;
-            if ((threadIdx.x & 31) < kWC) reinterpret_cast<int32_t *>(wc)[threadIdx.x & 31] = -1;
-        }
+        if (ADAPT && W) hot.init(s + wc_off);
         if (W) {
             for (int i = threadIdx.x; i < R * (int)(stride / 16); i += blockDim.x)
                 reinterpret_cast<double2 *>(s)[i] = make_double2(0.0, 0.0);
@@ -461,50 +523,15 @@ struct PrivSink {
             if (m) { s1 += v1; s2 += v2; m &= m - 1; }
         }
         const bool leader = lane == __ffs(peers) - 1;
-        int32_t *tags = reinterpret_cast<int32_t *>(wc);
-        double2 *vals = reinterpret_cast<double2 *>(wc + kWC * 4);
-        const int slot = (int)(((uint32_t)g * 2654435761u) >> 28);   // kWC = 16
-        bool done = false;
-        if (leader && tags[slot] == g) {             // at most one leader holds a slot's tag
-            double2 v = vals[slot];
-            v.x += s1;
-            v.y += s2;
-            vals[slot] = v;
-            done = true;
-        }
-        __syncwarp(act);
-        const bool want = leader && !done && __popc(peers) >= 2;
-        const unsigned wm = __ballot_sync(act, want);
-        if (want) {
-            const unsigned sp = __match_any_sync(wm, slot);
-            if (lane == __ffs(sp) - 1) {             // this slot's claimant
-                const int t = tags[slot];
-                if (t >= 0) {
-                    const double2 v = vals[slot];
-                    add2_shared(base + t, v.x, v.y);
-                }
-                tags[slot] = g;
-                vals[slot] = make_double2(s1, s2);
-                done = true;
-            }
-        }
+        const bool done = hot.absorb(act, leader, __popc(peers), g, s1, s2,
+                                     [&](int t, double a1, double a2) { add2_shared(base + t, a1, a2); });
         if (leader && !done) add2_shared(base + g, s1, s2);
-        __syncwarp(act);
     }
     // Before the block barrier of the merge stage: hot-bin caches -> this warp's replica.
     __device__ __forceinline__ void drain() {
         if (ADAPT && W) {
-            __syncwarp();
-            const int lane = (int)(threadIdx.x & 31);
-            if (lane < kWC) {
-                int32_t *tags = reinterpret_cast<int32_t *>(wc);
-                const double2 *vals = reinterpret_cast<const double2 *>(wc + kWC * 4);
-                if (tags[lane] >= 0) {
-                    double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
-                    add2_shared(base + tags[lane], vals[lane].x, vals[lane].y);
-                    tags[lane] = -1;
-                }
-            }
+            double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
+            hot.drain([&](int t, double a1, double a2) { add2_shared(base + t, a1, a2); });
         }
     }
     // Merge stage of PAPER.md:162-165: each block adds its local bins (summed over the
@@ -635,17 +662,7 @@ struct CacheSink {
                 const double v = __shfl_sync(act, w, src);
                 if (m) { s1 += v; s2 = fma(v, v, s2); m &= m - 1; }
             }
-            if (lane == leader) {
-                const int sl = lookup((uint32_t)g);
-                if (sl >= 0) {
-                    double *d = reinterpret_cast<double *>(vals);
-                    atomicAdd(d + sl, s1);
-                    atomicAdd(d + S + sl, s2);
-                } else {
-                    atomicAdd(pp->sumw + g, s1);
-                    atomicAdd(pp->sumw2 + g, s2);
-                }
-            }
+            if (lane == leader) put(g, s1, s2);
         } else {
             if (lane == leader) {
                 const uint32_t c = (uint32_t)__popc(peers);
@@ -653,6 +670,18 @@ struct CacheSink {
                 if (sl >= 0) atomicAdd(reinterpret_cast<uint32_t *>(vals) + sl, c);
                 else atomicAdd(pp->count + g, (unsigned long long)c);
             }
+        }
+    }
+    // a weighted group sum into its shared-memory slot, or straight to the global bins
+    __device__ __forceinline__ void put(int g, double s1, double s2) {
+        const int sl = lookup((uint32_t)g);
+        if (sl >= 0) {
+            double *d = reinterpret_cast<double *>(vals);
+            atomicAdd(d + sl, s1);
+            atomicAdd(d + S + sl, s2);
+        } else {
+            atomicAdd(pp->sumw + g, s1);
+            atomicAdd(pp->sumw2 + g, s2);
         }
     }
     __device__ __forceinline__ void drain() {}

@@ -415,7 +415,7 @@ bh_status fill_sort(bh_hist *h, int64_t n, const double *const *coords, const do
 // fill reads the result once its event has completed (never waits for it) and from then
 // on uses SORT if the largest partition holds <= 5% of the sample and no hashed bin
 // bucket holds > 1% (a hot bin contends in pass 2).
-constexpr int kProbeSamples = 1 << 16;
+constexpr int kProbeSamples = 1 << 14;     // one CTA: ~40 us, once per histogram
 bool auto_sort(bh_hist *h, int64_t n, const double *const *coords, cudaStream_t s) {
     if (h->strategy != BH_STRATEGY_AUTO || resolve_strategy(h, false) != BH_STRATEGY_CACHE) return false;
     const int P = (int)sort_partitions(h, false);

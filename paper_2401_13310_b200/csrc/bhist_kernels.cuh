@@ -91,23 +91,6 @@ __device__ __forceinline__ int find_bin_fixed(const AxisP &a, double x) {
     return 1 + b;                        // q <= n: bin n+1 is overflow (R4)
 }
 
-// Split form for kernels that defer the rare exact division out of their event loop
-// (a call inside the loop makes the compiler reload every kernel parameter per event):
-// the fast path's bin, with `need` set when only the exact division can decide it.
-__device__ __forceinline__ int find_bin_fixed_fast(const AxisP &a, double x, bool &need) {
-    const bool under = x < a.xmin;
-    const bool over = !(x < a.xmax);
-    const double q = __dmul_rn(__dsub_rn(x, a.xmin), a.inv);
-    const int b = (int)__dmul_rn(q, 1.0 - 0x1p-40);
-    need = b != (int)__dmul_rn(q, 1.0 + 0x1p-40) && !under && !over;
-    return 1 + (under ? -1 : (over ? a.n : b));
-}
-
-// the exact bin of an in-range x whose fast path set `need`
-__device__ __forceinline__ int find_bin_fixed_exact(const AxisP &a, double x) {
-    return 1 + fixed_exact_quotient(a.n, __dsub_rn(x, a.xmin), a.D);
-}
-
 // Guide cell of a coordinate x >= e[0]: monotone non-decreasing in x (RN is
 // monotone, gscale > 0, truncation and min are monotone).  The same function
 // builds the table, so the table is exact for it.
@@ -191,14 +174,6 @@ __device__ __forceinline__ int find_bin(const AxisP &a, double x, const unsigned
 }
 
 __device__ __forceinline__ int find_bin(const AxisP &a, double x) { return find_bin<2>(a, x, nullptr); }
-
-// find_bin with the fixed-axis exact division deferred (see find_bin_fixed_fast)
-template <int VM>
-__device__ __forceinline__ int find_bin_deferred(const AxisP &a, double x, const unsigned char *smem, bool &need) {
-    need = false;
-    if (VM == 0 || !a.var) return find_bin_fixed_fast(a, x, need);
-    return find_bin<VM>(a, x, smem);
-}
 
 // Copy each variable axis' table image (float32 edges + guide, built once at create in
 // the staged layout) into shared memory: 16-byte loads, four per thread in flight.
@@ -359,25 +334,6 @@ __device__ __forceinline__ int add2_shared_count(double2 *cell, double w, double
         ++lost;
         cur = make_double2(__longlong_as_double(ol), __longlong_as_double(oh));
     }
-}
-
-// Warp-aggregated variant for peaked data: the lanes of `act` holding the same cell
-// are grouped with match.any, their (w, w*w) summed over the group by a shuffle walk
-// (lane order), and only the group's leader runs the CAS loop -- one CAS per distinct
-// hot cell instead of a k-way serialized CAS storm (a 32-lane same-address CAS.128
-// costs ~760 cycles, tools/microbench/mb2.cu).
-__device__ __forceinline__ void add2_shared_grouped(double2 *base, int g, double w, double w2, unsigned act) {
-    const unsigned peers = __match_any_sync(act, g);
-    const int lane = (int)(threadIdx.x & 31);
-    const int rounds = __reduce_max_sync(act, (unsigned)__popc(peers));
-    double s1 = 0.0, s2 = 0.0;
-    unsigned m = peers;
-    for (int k = 0; k < rounds; ++k) {
-        const int src = m ? __ffs(m) - 1 : lane;
-        const double v1 = __shfl_sync(act, w, src), v2 = __shfl_sync(act, w2, src);
-        if (m) { s1 += v1; s2 += v2; m &= m - 1; }
-    }
-    if (lane == __ffs(peers) - 1) add2_shared(base + g, s1, s2);
 }
 
 // Shared-memory layout of the PRIV sink: unit -> uint32 count[G];

@@ -21,6 +21,11 @@ template <int SINK> struct ThreadsOf {   // SINK_GLOBAL == 1
     static constexpr int v = SINK == 1 ? kThreadsGlobal : kThreadsSmem;
 };
 
+// Streaming (evict-first) loads of the input columns: each byte is read once.
+__device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }
+__device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
+__device__ __forceinline__ float4 ld_stream(const float4 *p) { return __ldcs(p); }
+
 // Axis as the kernels see it.  Fixed axes use (xmin, xmax, D = xmax-xmin,
 // inv = n/D), all rounded once on the host exactly as the definition rounds them.
 // Variable axes use the edges plus a monotone "guide" table.
@@ -731,8 +736,8 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
                 const int q = q0 + u * nth;
                 if (q < npair) {
 #pragma unroll
-                    for (int a = 0; a < DIM; ++a) bt.x[u][a] = __ldcs(xs[a] + q);
-                    if (W) bt.w[u] = __ldcs(ws + q);
+                    for (int a = 0; a < DIM; ++a) bt.x[u][a] = ld_stream(xs[a] + q);
+                    if (W) bt.w[u] = ld_stream(ws + q);
                 }
             }
         };
@@ -749,22 +754,29 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
             }
         };
         const int step = U * nth;
+        // Warp-uniform trip counts (load/process predicate each lane's pairs) and an explicit
+        // reconvergence per batch: data-dependent branches (the variable-axis search, rare
+        // exact FindBin decisions) must not leave lanes issuing the next batch's loads on
+        // their own -- partial-warp loads of evict-first lines re-read DRAM (measured 2x
+        // traffic and 4.5x time on C2 when the compiler dropped a reconvergence point).
+        const int lane0 = tid & 31;
         if constexpr (B::DB) {
             // register double buffer: load the next batch, then process the current one
             // (a two-buffer ping-pong unroll measured 25% slower on C1S: more live registers)
             B cur, nxt;
             int q0 = tid;
-            if (q0 < npair) load(cur, q0);
-            for (; q0 < npair; q0 += step) {
-                if (q0 + step < npair) load(nxt, q0 + step);
+            load(cur, q0);
+            for (; q0 - lane0 < npair; q0 += step) {
+                load(nxt, q0 + step);
                 process(cur, q0);
                 cur = nxt;
+                __syncwarp();
             }
         } else {
             B cur;
-            for (int q0 = tid; q0 < npair; q0 += step) {
+            for (int q0 = tid; q0 - lane0 < npair; q0 += step) {
                 load(cur, q0);       // 3-4 columns: 48-64 B per thread in flight already
-                process(cur, q0);
+                process(cur, q0);    // (a __syncwarp here measured 2.4% slower on C4)
             }
         }
         // leading peeled events and the odd tail
@@ -781,8 +793,8 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
         for (int i = tid; i < (int)p.n; i += nth) {
             double x[DIM];
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) x[a] = __ldcs(p.x[a] + i);
-            do_event<DIM, W, VM>(p, x, W ? __ldcs(p.w + i) : 1.0, sink, acc, smem);
+            for (int a = 0; a < DIM; ++a) x[a] = ld_stream(p.x[a] + i);
+            do_event<DIM, W, VM>(p, x, W ? ld_stream(p.w + i) : 1.0, sink, acc, smem);
         }
     }
 
@@ -831,11 +843,13 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
         for (int i = tid; i < n; i += nth) one(i);
     } else {
         const int base = p.peel, nq = (n - base) >> 2;
-        for (int q = tid; q < nq; q += nth) {
+        for (int q = tid; q - (tid & 31) < nq; q += nth) {      // warp-uniform trips (see k_fill)
+            __syncwarp();
+            if (q >= nq) continue;
             float4 xv[DIM], wv;
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) xv[a] = __ldcs(reinterpret_cast<const float4 *>(xs[a] + base) + q);
-            if (W) wv = __ldcs(reinterpret_cast<const float4 *>(ws + base) + q);
+            for (int a = 0; a < DIM; ++a) xv[a] = ld_stream(reinterpret_cast<const float4 *>(xs[a] + base) + q);
+            if (W) wv = ld_stream(reinterpret_cast<const float4 *>(ws + base) + q);
             const float *xf[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) xf[a] = reinterpret_cast<const float *>(&xv[a]);
@@ -934,7 +948,7 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += nth) {
         double r[kExprRegs];
 #pragma unroll
-        for (int c = 0; c < kExprRegs; ++c) r[c] = c < e.ncols ? __ldcs(e.cols[c] + i) : 0.0;
+        for (int c = 0; c < kExprRegs; ++c) r[c] = c < e.ncols ? ld_stream(e.cols[c] + i) : 0.0;
         run_expr(e, r);
         if (e.filter_reg >= 0 && !(r[e.filter_reg] != 0.0)) continue;   // Filter
         ++passed;
@@ -1014,13 +1028,13 @@ __global__ void __launch_bounds__(512, 2) k_fill_exact(FillP p, long long *limbs
         bool inr = valid;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
-            x[a] = valid ? __ldcs(p.x[a] + i) : 0.0;
+            x[a] = valid ? ld_stream(p.x[a] + i) : 0.0;
             const int b = find_bin(p.ax[a], x[a]);
             inr &= (b >= 1) & (b <= p.ax[a].n);
             g += b * mul;
             if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
         }
-        const double w = valid ? __ldcs(p.w + i) : 0.0, w2 = w * w;
+        const double w = valid ? ld_stream(p.w + i) : 0.0, w2 = w * w;
         const bool fin = fabs(w) <= 1.7976931348623157e308 && fabs(w2) <= 1.7976931348623157e308;
         if (valid && !fin) {
             atomicAdd(p.sumw + g, w);
@@ -1177,8 +1191,8 @@ __global__ void __launch_bounds__(1024, 1) k_fill_multi(const __grid_constant__ 
         const bool valid = i < p.n;
         double x[kMaxCols];
 #pragma unroll
-        for (int c = 0; c < kMaxCols; ++c) x[c] = (c < p.ncols && valid) ? __ldcs(p.cols[c] + i) : 0.0;
-        const double wv = (valid && p.w) ? __ldcs(p.w + i) : 1.0;
+        for (int c = 0; c < kMaxCols; ++c) x[c] = (c < p.ncols && valid) ? ld_stream(p.cols[c] + i) : 0.0;
+        const double wv = (valid && p.w) ? ld_stream(p.w + i) : 1.0;
         for (int hh = 0; hh < p.nh; ++hh) {
             const MultiH &H = p.h[hh];
             const double w = H.weighted ? wv : 1.0;

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_part_scatter(FillP p, PartP
             double *dx = reinterpret_cast<double *>(smem + st * kStageBytes);
             for (int i = threadIdx.x; i < m; i += kPartThreads)
 #pragma unroll
-                for (int a = 0; a < NCOL; ++a) dx[a * kTile + i] = __ldcs(col[a] + e0 + i);
+                for (int a = 0; a < NCOL; ++a) dx[a * kTile + i] = ld_stream(col[a] + e0 + i);
             __syncthreads();
         }
         // step (1), per axis -> global bin; step (3) stats; rank in partition

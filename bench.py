@@ -402,6 +402,19 @@ def run_gpu(args):
     e2e_value = N * world * e2e_steps / e2e_s
     h2d = 8 * N * len(used)
     d2h = 8 * sum(pkg.bh_packed_size(H.h) for H in Hs)
+    # PCIe roofline of the e2e leg: plain pinned host -> device copy of one input column
+    # (up to 1 GiB), timed with CUDA events on this GPU alone
+    nb = min(N, 1 << 27)
+    dst = torch.empty(nb, dtype=torch.float64, device=dev)
+    dst.copy_(host[0][:nb], non_blocking=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        dst.copy_(host[0][:nb], non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    pcie_peak = 3 * 8 * nb / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    del dst
 
     # ---- secondary rows (rank 0, N=1): e.g. the 1D fixed-bin target of the north star (C1S)
     secondary = {}
@@ -447,11 +460,15 @@ def run_gpu(args):
                        if world > 1 else "single GPU"},
             "pct_hbm_peak": 100.0 * bpe * value / world / 1e9 / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "k_fill_multi" if multi else f"k_fill ({strat})",
+                         "traffic": traffic,
+                         "kernel": "k_fill_multi" if multi else ("k_part_scatter + k_part_reduce (sort)"
+                                                                  if strat == "sort" else f"k_fill ({strat})"),
                          "launch_ms": fill_avg,
                          "algorithmic_bytes_per_launch": bpe * N, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps, "pcie_gbs": h2d * world * e2e_steps / e2e_s / 1e9 / world,
+                    "pcie_peak_gbs": pcie_peak,
+                    "pcie_frac": h2d * e2e_steps / e2e_s / 1e9 / pcie_peak,
                     "clocks": clk2.summary()},
             "gpu_launches": launches,
             "clocks": clocks,

@@ -420,10 +420,14 @@ bool auto_sort(bh_hist *h, int64_t n, const double *const *coords, cudaStream_t 
     if (h->strategy != BH_STRATEGY_AUTO || resolve_strategy(h, false) != BH_STRATEGY_CACHE) return false;
     const int P = (int)sort_partitions(h, false);
     if (P > kPartMaxP || n < 8LL * h->nsm * (1LL << sort_pb(false)) || getenv("BHIST_NO_AUTO_SORT")) return false;
-    if (h->probe_state == 1 && cudaEventQuery(h->probe_done) == cudaSuccess)
-        h->probe_state = ((double)h->probe_host[0] <= 0.05 * kProbeSamples &&
-                          (double)h->probe_host[1] <= 0.01 * kProbeSamples) ? 2 : 3;
-    cudaGetLastError();                              // cudaErrorNotReady is not an error here
+    if (h->probe_state == 1) {
+        const cudaError_t q = cudaEventQuery(h->probe_done);
+        if (q == cudaSuccess)
+            h->probe_state = ((double)h->probe_host[0] <= 0.05 * kProbeSamples &&
+                              (double)h->probe_host[1] <= 0.01 * kProbeSamples) ? 2 : 3;
+        else if (q == cudaErrorNotReady)
+            cudaGetLastError();                      // not an error: the probe is still running
+    }
     if (h->probe_state == 0) {
         if (!h->probe_dev) {
             if (cudaMalloc(reinterpret_cast<void **>(&h->probe_dev), 2 * sizeof(unsigned int)) != cudaSuccess ||

@@ -623,12 +623,12 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
             P.var = 1;
             P.xmin = A.edges[0];
             P.xmax = A.edges[A.nbins];
-            // guide cells: a power of two, up to ~4 per bin (fewer edges per cell for
+            // guide cells: a power of two, up to 64 per bin (fewer edges per cell for
             // non-uniform edges, e.g. log-spaced) while the shared-memory tables (float32
             // edges + uint16 guide) stay <= 56 KB; at least ~n/2 cells
             int gc = 1;
             while (2 * gc < A.nbins && gc < (1 << 22)) gc <<= 1;
-            while (gc < 4 * A.nbins && 4 * (size_t)(A.nbins + 1) + 2 * (size_t)(2 * gc + 1) <= 56 * 1024) gc <<= 1;
+            while (gc < 64 * A.nbins && 4 * (size_t)(A.nbins + 1) + 2 * (size_t)(2 * gc + 1) <= 56 * 1024) gc <<= 1;
             P.gcells = gc;
             P.gscale = (double)gc / (P.xmax - P.xmin);
             if (!std::isfinite(P.gscale) || !(P.gscale > 0)) return cleanup(fail(BH_EINVAL, "axis %d: edge range too small", a));

@@ -29,8 +29,10 @@
  * must stay valid and unmodified until the stream has executed the fill.
  * Streams: `bh_stream` is a cudaStream_t passed as an opaque pointer (NULL = the
  * legacy default stream).  No call synchronizes the device; bh_read synchronizes
- * only its stream; bh_fill_host waits only for its own host->device copies.  A
- * histogram is single-writer: issue its fills on one stream at a time.
+ * only its stream; bh_fill_host waits only for its own host->device copies; a fill
+ * that needs more SORT scratch than the histogram holds (BH_STRATEGY_SORT below)
+ * synchronizes its stream once to grow it.  A histogram is single-writer: issue
+ * its fills on one stream at a time.
  * Errors: every call returns a bh_status; no exception crosses the ABI;
  * bh_last_error() gives a thread-local message for the last failure.  NaN/inf
  * coordinates and any weight value are not errors.  Asynchronous kernel faults

@@ -23,6 +23,8 @@
 // Records cost 2 B (unit) or 10 B (weighted) per event written + read back, instead of
 // one L2 atomic per event; no shared-memory state is bigger than 128 KB.
 #pragma once
+#include <type_traits>
+
 #include "bhist_kernels.cuh"
 
 namespace bh {
@@ -150,30 +152,34 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_part_scatter(FillP p, PartP
         int pp[kEv];
         uint32_t key[kEv];                           // rank << 16 | local bin
         double wk[kEv];                              // the weights again, for the scatter
+        auto bin_rank = [&](auto full) {             // full tiles: no per-event bounds checks
 #pragma unroll
-        for (int u = 0; u < kEv; ++u) {
-            const int i = u * kPartThreads + threadIdx.x;
-            const bool ok = i < m;
-            double x[DIM];
+            for (int u = 0; u < kEv; ++u) {
+                const int i = u * kPartThreads + threadIdx.x;
+                const bool ok = decltype(full)::value || i < m;
+                double x[DIM];
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) x[a] = sx[a * kTile + i];
-            const double w = W ? sx[(NCOL - 1) * kTile + i] : 1.0;
-            wk[u] = w;
-            int g = 0, mul = 1;
-            bool inr = true;
+                for (int a = 0; a < DIM; ++a) x[a] = sx[a * kTile + i];
+                const double w = W ? sx[(NCOL - 1) * kTile + i] : 1.0;
+                wk[u] = w;
+                int g = 0, mul = 1;
+                bool inr = true;
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) {
-                const int b = find_bin<VM>(p.ax[a], x[a], smem);
-                inr &= (b >= 1) & (b <= p.ax[a].n);
-                g += b * mul;
-                if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
+                for (int a = 0; a < DIM; ++a) {
+                    const int b = find_bin<VM>(p.ax[a], x[a], smem);
+                    inr &= (b >= 1) & (b <= p.ax[a].n);
+                    g += b * mul;
+                    if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
+                }
+                if (ok && inr) acc.add(x, w);        // in range only (R6)
+                pp[u] = ok ? (int)((uint32_t)g >> pb) : -1;
+                // the returned old count is the rank (equal addresses of a warp are resolved
+                // by the shared-memory atomic unit)
+                key[u] = ((uint32_t)g & lmask) | (ok ? atomicAdd(cnt + pp[u], 1u) << 16 : 0u);
             }
-            if (ok && inr) acc.add(x, w);            // in range only (R6)
-            pp[u] = ok ? (int)((uint32_t)g >> pb) : -1;
-            // the returned old count is the rank (equal addresses of a warp are resolved
-            // by the shared-memory atomic unit)
-            key[u] = ((uint32_t)g & lmask) | (ok ? atomicAdd(cnt + pp[u], 1u) << 16 : 0u);
-        }
+        };
+        if (m == kTile) bin_rank(std::true_type{});
+        else bin_rank(std::false_type{});
         __syncthreads();                             // (A) stage consumed, counts complete
         if (threadIdx.x == 0) {
             const int tn = t + kPartStages * gridDim.x;

@@ -1,5 +1,5 @@
 #!/bin/bash
-#timeout 1200 python -m pytest tests/ -q -m gpu --timeout=600 -x > gpurun_out/pytest_ab.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_ab.log
-for c in C2 C3 C4 C1S; do for lib in paper_2401_13310_b200/libbhist.so build_ab/libbhist_old.so; do
+for i in 1 2; do for c in C3; do for lib in paper_2401_13310_b200/libbhist.so build_ab/libbhist_old.so; do
 BHIST_LIBRARY=$PWD/$lib timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print('$lib $c %.4g ev/s frac %.3f launch %.3f'%(d['value'], d['roofline']['frac'], d['roofline']['launch_ms']))"; done; done
+import json,sys; d=json.loads(sys.stdin.readline()); print('$lib $c %.4g ev/s frac %.3f launch %.3f'%(d['value'], d['roofline']['frac'], d['roofline']['launch_ms']))"; done; done; done
+timeout 600 python -m pytest tests/test_parity_gpu.py -q -m gpu -x -k "sort" 2>&1 | tail -1

@@ -420,6 +420,35 @@ def test_peaked_weighted_2d_warp_cache(nb):
     compare(_gpu_fill(axes, [x, y], w, pkg.BH_STRATEGY_PRIV, splits=2), ref, True, f"peaked 2D {nb}")
 
 
+def test_bench_json_contract():
+    """bench.py at N=1 on a reduced event count prints one JSON line with every key of
+    the contract: roofline, e2e (incl. PCIe fraction), clocks, launches, CPU baselines."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--steps", "3", "--warmup", "3", "--events", "4000000",
+           "--e2e-steps", "1", "--secondary", "", "--cpu-sample", "200000"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks", "cpu_baseline"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 16 * 4_000_000 and e["d2h_bytes_per_step"] > 0
+    assert 0 < e["pcie_frac"] < 1.5
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert d["config"]["workload"].startswith("C2")
+
+
 def test_bench_two_ranks_exchange(tmp_path):
     """bench.py's N>1 path end to end on one GPU: 2 torchrun ranks (gloo backend so both
     may share cuda:0), contiguous shards, pack -> all-reduce -> unpack every step; the

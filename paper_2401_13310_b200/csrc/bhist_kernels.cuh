@@ -685,6 +685,9 @@ __device__ __forceinline__ void do_event(const FillP &p, const double (&x)[DIM],
     if (inr) acc.add(x, w);                              // step (3): stats, in-range only (R6)
 }
 
+#ifndef BH_DB_MAX_COLS
+#define BH_DB_MAX_COLS 2
+#endif
 template <int DIM, bool W>
 struct Batch {            // U event pairs of every column, held in registers (x2: double-buffered)
     static constexpr int NCOL = DIM + (W ? 1 : 0);
@@ -692,7 +695,7 @@ struct Batch {            // U event pairs of every column, held in registers (x
 #define BH_U_TWO_COLS 1
 #endif
     static constexpr int U = NCOL == 1 ? 2 : NCOL == 2 ? BH_U_TWO_COLS : 1;   // <= 64 registers at 1024 threads
-    static constexpr bool DB = NCOL <= 2;             // prefetch the next batch (register double buffer)
+    static constexpr bool DB = NCOL <= BH_DB_MAX_COLS;   // prefetch the next batch (register double buffer)
     double2 x[U][DIM];
     double2 w[U];
 };

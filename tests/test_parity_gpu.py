@@ -19,6 +19,13 @@ STRATS = {"priv": pkg.BH_STRATEGY_PRIV, "global": pkg.BH_STRATEGY_GLOBAL, "cache
           "sort": pkg.BH_STRATEGY_SORT}
 
 
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def _t(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
 
@@ -459,7 +466,7 @@ def test_bench_two_ranks_exchange(tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"), "--gpus", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"), "--gpus", "2",
            "--steps", "3", "--warmup", "3", "--backend", "gloo", "--events", "2000000", "--e2e-steps", "1"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert out.returncode == 0, out.stderr[-3000:]

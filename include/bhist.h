@@ -131,6 +131,12 @@ bh_status bh_fill(bh_hist *h, int64_t n, const double *const *coords, const doub
  * at half the input bytes.  BH_STRATEGY_EXACT falls back to AUTO here. */
 bh_status bh_fill_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, bh_stream s);
 
+/* Same with int32 coordinate columns (e.g. multiplicities; RDataFrame fills histograms
+ * from integer columns too, "different ... input data types") and
+ * optional float32 weights: each coordinate widens exactly to float64, so the result
+ * equals bh_fill on the widened columns.  DEVICE pointers, 4 B per value. */
+bh_status bh_fill_i32(bh_hist *h, int64_t n, const int32_t *const *coords, const float *w, bh_stream s);
+
 /* Same as bh_fill but coords/w are HOST pointers (pinned: DMA straight from them;
  * pageable: staged by the driver).  Events are copied in chunks into a device
  * double-buffer on an internal copy stream, overlapped with the fills on s.

@@ -22,7 +22,7 @@ BH_DEBUG_SKIP_COPY_WAIT = 1
 
 # every symbol include/bhist.h declares (checked by tests/test_abi.py)
 EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset", "bh_fill", "bh_fill_host",
-            "bh_fill_multi", "bh_fill_expr", "bh_fill_f32", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
+            "bh_fill_multi", "bh_fill_expr", "bh_fill_f32", "bh_fill_i32", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
             "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_launch_count"]
 
 
@@ -79,6 +79,7 @@ def lib(build_if_stale: bool = False):
             "bh_fill_multi": ([_P, _I32, _P, _P, _I64, _P, _I32, _P, _P], _I32),
             "bh_fill_expr": ([_P, _I64, _P, _I32, _P, _I32, _P, _I32, _I32, _P], _I32),
             "bh_fill_f32": ([_P, _I64, _P, _P, _P], _I32),
+            "bh_fill_i32": ([_P, _I64, _P, _P, _P], _I32),
             "bh_info": ([_P, _P, _P, _P], _I32),
             "bh_packed_size": ([_P, _P], _I32),
             "bh_pack": ([_P, _P, _P], _I32),
@@ -150,6 +151,11 @@ def bh_fill(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
 def bh_fill_f32(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
     arr = _ptrs(coord_ptrs)
     _check(lib().bh_fill_f32(h, n, ctypes.addressof(arr), w_ptr, stream))
+
+
+def bh_fill_i32(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
+    arr = _ptrs(coord_ptrs)
+    _check(lib().bh_fill_i32(h, n, ctypes.addressof(arr), w_ptr, stream))
 
 
 def bh_fill_host(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
@@ -346,6 +352,19 @@ class Histogram:
             if not (c.is_cuda and c.dtype == torch.float32 and c.is_contiguous() and c.numel() == n):
                 raise ValueError("columns must be contiguous float32 CUDA tensors of equal length")
         bh_fill_f32(self.h, n, [c.data_ptr() for c in coords], None if w is None else w.data_ptr(),
+                    _stream_handle(stream))
+        return self
+
+    def fill_i32(self, coords, w=None, stream=None):
+        """int32 coordinate CUDA tensors, optional float32 weights (coordinates widened exactly)."""
+        import torch
+        n = coords[0].numel()
+        for c in coords:
+            if not (c.is_cuda and c.dtype == torch.int32 and c.is_contiguous() and c.numel() == n):
+                raise ValueError("coords must be contiguous int32 CUDA tensors of equal length")
+        if w is not None and not (w.is_cuda and w.dtype == torch.float32 and w.is_contiguous() and w.numel() == n):
+            raise ValueError("w must be a contiguous float32 CUDA tensor of the same length")
+        bh_fill_i32(self.h, n, [c.data_ptr() for c in coords], None if w is None else w.data_ptr(),
                     _stream_handle(stream))
         return self
 

@@ -497,7 +497,9 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
 }
 
 // float32 columns (see k_fill_f32); EXACT is not offered for float32 weights (uses AUTO).
-bh_status fill_device_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, cudaStream_t s) {
+// 4-byte columns: float32 or (is_int) int32 coordinates, float32 weights.
+bh_status fill_device_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, cudaStream_t s,
+                          bool is_int = false) {
     FillPlan pl;
     if (bh_status r = plan_fill(h, w != nullptr, pl, n)) return r;
     LaunchCfg &c = pl.c;
@@ -519,10 +521,18 @@ bh_status fill_device_f32(bh_hist *h, int64_t n, const float *const *coords, con
         p.wc_off = pl.wc_off;
         c.grid = grid_for(h, c, m);
         cudaError_t e;
-        switch (h->dim) {
-        case 1: e = c.weighted ? fill_launch_f32<1, true>(p, c, s) : fill_launch_f32<1, false>(p, c, s); break;
-        case 2: e = c.weighted ? fill_launch_f32<2, true>(p, c, s) : fill_launch_f32<2, false>(p, c, s); break;
-        default: e = c.weighted ? fill_launch_f32<3, true>(p, c, s) : fill_launch_f32<3, false>(p, c, s); break;
+        if (is_int) {
+            switch (h->dim) {
+            case 1: e = c.weighted ? fill_launch_i32<1, true>(p, c, s) : fill_launch_i32<1, false>(p, c, s); break;
+            case 2: e = c.weighted ? fill_launch_i32<2, true>(p, c, s) : fill_launch_i32<2, false>(p, c, s); break;
+            default: e = c.weighted ? fill_launch_i32<3, true>(p, c, s) : fill_launch_i32<3, false>(p, c, s); break;
+            }
+        } else {
+            switch (h->dim) {
+            case 1: e = c.weighted ? fill_launch_f32<1, true>(p, c, s) : fill_launch_f32<1, false>(p, c, s); break;
+            case 2: e = c.weighted ? fill_launch_f32<2, true>(p, c, s) : fill_launch_f32<2, false>(p, c, s); break;
+            default: e = c.weighted ? fill_launch_f32<3, true>(p, c, s) : fill_launch_f32<3, false>(p, c, s); break;
+            }
         }
         if (e != cudaSuccess) return fail(BH_ECUDA, "fill_f32 launch: %s", cudaGetErrorString(e));
         ++h->launches;
@@ -738,6 +748,17 @@ bh_status bh_fill_f32(bh_hist *h, int64_t n, const float *const *coords, const f
         if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
     DeviceGuard dg(h->device);
     return fill_device_f32(h, n, coords, w, static_cast<cudaStream_t>(s));
+}
+
+bh_status bh_fill_i32(bh_hist *h, int64_t n, const int32_t *const *coords, const float *w, bh_stream s) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (n < 0) return fail(BH_EINVAL, "n < 0");
+    if (n == 0) return BH_OK;
+    if (!coords) return fail(BH_EINVAL, "coords is NULL");
+    for (int a = 0; a < h->dim; ++a)
+        if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
+    DeviceGuard dg(h->device);
+    return fill_device_f32(h, n, reinterpret_cast<const float *const *>(coords), w, static_cast<cudaStream_t>(s), true);
 }
 
 bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s) {

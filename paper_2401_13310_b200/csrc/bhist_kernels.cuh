@@ -816,8 +816,13 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
 // float64 and the float64 path follows, so the result equals bh_fill on the widened
 // columns; the columns cost 4 B/event instead of 8.  Columns sharing a 16-byte phase are
 // read as float4 (4 events per LDG.128) after `peel` (0-3) leading events; p.peel < 0
-// selects the scalar loop (mixed phases).
-template <int DIM, bool W, int SINK, int VM>
+// selects the scalar loop (mixed phases).  CT = float or int32_t: int32 coordinate columns
+// (e.g. multiplicities) widen exactly to float64 too; weights are float32 in both.
+template <typename CT> struct Vec4Of;
+template <> struct Vec4Of<float> { using T = float4; };
+template <> struct Vec4Of<int32_t> { using T = int4; };
+
+template <int DIM, bool W, int SINK, int VM, typename CT>
 __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill_f32(FillP p) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Sink_t = typename SinkOf<SINK, W>::T;
@@ -830,9 +835,10 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     if constexpr (SINK != SINK_GLOBAL || VM == 1) __syncthreads();
     Acc<DIM, W> acc;
     acc.zero();
-    const float *xs[DIM];
+    using CV = typename Vec4Of<CT>::T;
+    const CT *xs[DIM];
 #pragma unroll
-    for (int a = 0; a < DIM; ++a) xs[a] = reinterpret_cast<const float *>(p.x[a]);
+    for (int a = 0; a < DIM; ++a) xs[a] = reinterpret_cast<const CT *>(p.x[a]);
     const float *ws = reinterpret_cast<const float *>(p.w);
     const int n = (int)p.n;                       // host splits launches at 2^30 events
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
@@ -849,13 +855,14 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
         for (int q = tid; q - (tid & 31) < nq; q += nth) {      // warp-uniform trips (see k_fill)
             __syncwarp();
             if (q >= nq) continue;
-            float4 xv[DIM], wv;
+            CV xv[DIM];
+            float4 wv;
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) xv[a] = ld_stream(reinterpret_cast<const float4 *>(xs[a] + base) + q);
+            for (int a = 0; a < DIM; ++a) xv[a] = __ldcs(reinterpret_cast<const CV *>(xs[a] + base) + q);
             if (W) wv = ld_stream(reinterpret_cast<const float4 *>(ws + base) + q);
-            const float *xf[DIM];
+            const CT *xf[DIM];
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) xf[a] = reinterpret_cast<const float *>(&xv[a]);
+            for (int a = 0; a < DIM; ++a) xf[a] = reinterpret_cast<const CT *>(&xv[a]);
             const float *wf = reinterpret_cast<const float *>(&wv);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {

@@ -95,24 +95,25 @@ cudaError_t launch_part1_v(const FillP &p, const PartP &q, int vm, int rc, int g
     else return launch_part1_r<DIM, W, 8>(p, q, vm, grid, smem, s);
 }
 
-template <int DIM, bool W, int SINK>
+template <int DIM, bool W, int SINK, typename CT>
 cudaError_t launch_f32_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    auto kern = c.vm == 0 ? k_fill_f32<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_f32<DIM, W, SINK, 1> : k_fill_f32<DIM, W, SINK, 2>;
+    auto kern = c.vm == 0 ? k_fill_f32<DIM, W, SINK, 0, CT>
+                          : c.vm == 1 ? k_fill_f32<DIM, W, SINK, 1, CT> : k_fill_f32<DIM, W, SINK, 2, CT>;
     if (cudaError_t r = ensure_smem(reinterpret_cast<const void *>(kern), c.smem)) return r;
     kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
     return cudaGetLastError();
 }
 
-template <int DIM, bool W>
+template <int DIM, bool W, typename CT>
 cudaError_t launch_f32_w(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
     switch (c.strategy) {
     case BH_STRATEGY_PRIV:
         if constexpr (W) {
-            if (p.wc_off >= 0) return launch_f32_s<DIM, W, SINK_PRIVA>(p, c, s);
+            if (p.wc_off >= 0) return launch_f32_s<DIM, W, SINK_PRIVA, CT>(p, c, s);
         }
-        return launch_f32_s<DIM, W, SINK_PRIV>(p, c, s);
-    case BH_STRATEGY_CACHE: return launch_f32_s<DIM, W, SINK_CACHE>(p, c, s);
-    default: return launch_f32_s<DIM, W, SINK_GLOBAL>(p, c, s);
+        return launch_f32_s<DIM, W, SINK_PRIV, CT>(p, c, s);
+    case BH_STRATEGY_CACHE: return launch_f32_s<DIM, W, SINK_CACHE, CT>(p, c, s);
+    default: return launch_f32_s<DIM, W, SINK_GLOBAL, CT>(p, c, s);
     }
 }
 
@@ -143,6 +144,7 @@ cudaError_t launch_expr_w(const FillP &p, const ExprP &e, const LaunchCfg &c, cu
 // one definition per (DIM, W) in bhist_fill_d<DIM><u|w>.cu
 template <int DIM, bool W> cudaError_t fill_launch(const FillP &p, const LaunchCfg &c, cudaStream_t s);
 template <int DIM, bool W> cudaError_t fill_launch_f32(const FillP &p, const LaunchCfg &c, cudaStream_t s);
+template <int DIM, bool W> cudaError_t fill_launch_i32(const FillP &p, const LaunchCfg &c, cudaStream_t s);
 template <int DIM, bool W> cudaError_t fill_launch_expr(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s);
 template <int DIM, bool W> cudaError_t fill_launch_part1(const FillP &p, const PartP &q, int vm, int rc, int grid, size_t smem, cudaStream_t s);
 
@@ -151,7 +153,10 @@ template <int DIM, bool W> cudaError_t fill_launch_part1(const FillP &p, const P
         return launch_s<DIM, W>(p, c, s);                                                                  \
     }                                                                                                      \
     template <> cudaError_t fill_launch_f32<DIM, W>(const FillP &p, const LaunchCfg &c, cudaStream_t s) {  \
-        return launch_f32_w<DIM, W>(p, c, s);                                                              \
+        return launch_f32_w<DIM, W, float>(p, c, s);                                                       \
+    }                                                                                                      \
+    template <> cudaError_t fill_launch_i32<DIM, W>(const FillP &p, const LaunchCfg &c, cudaStream_t s) {  \
+        return launch_f32_w<DIM, W, int32_t>(p, c, s);                                                     \
     }                                                                                                      \
     template <> cudaError_t fill_launch_expr<DIM, W>(const FillP &p, const ExprP &e, const LaunchCfg &c,   \
                                                      cudaStream_t s) {                                     \

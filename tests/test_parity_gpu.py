@@ -748,3 +748,38 @@ def test_strategy_resolution():
     h = pkg.Histogram([(100, 0.0, 1.0)])
     assert h.strategy(False) == pkg.BH_STRATEGY_PRIV
     h.close()
+
+
+# ------------------------------------------------------------------ int32 coordinate columns (NEXT-2)
+@pytest.mark.parametrize("weighted", [False, True])
+@pytest.mark.parametrize("offset", [0, 1, 3])
+def test_fill_i32_equals_widened(weighted, offset):
+    # integer coordinates (e.g. multiplicities) on fixed and variable axes, bins centred
+    # on and between integers, flow on both sides; weights float32
+    rng = np.random.default_rng(77 + offset)
+    n = 1_000_003
+    ax = [(20, -0.5, 19.5), np.array([-3.0, 0.0, 1.0, 2.0, 3.5, 7.0, 12.0, 40.0]), (7, 0.0, 14.0)]
+    ci = [rng.poisson(6.0, n + offset).astype(np.int32) - 1, rng.integers(-5, 60, n + offset).astype(np.int32),
+          rng.integers(-2, 20, n + offset).astype(np.int32)]
+    wf = rng.uniform(-0.5, 1.5, n + offset).astype(np.float32) if weighted else None
+    for dim in (1, 2, 3):
+        axes = ax[:dim]
+        cols = [c[offset:] for c in ci[:dim]]
+        w = None if wf is None else wf[offset:]
+        ref = oracle.OracleHist(axes).fill([c.astype(np.float64) for c in cols],
+                                           None if w is None else w.astype(np.float64)).read()
+        h = pkg.Histogram(axes)
+        # slice on the device: columns start `offset` elements into their allocations
+        h.fill_i32([torch.from_numpy(c).to(DEV)[offset:] for c in ci[:dim]],
+                   None if wf is None else torch.from_numpy(wf).to(DEV)[offset:])
+        compare(h.read(), ref, weighted, f"i32 dim={dim} offset={offset}")
+        h.close()
+
+
+def test_fill_i32_rejects_bad_arguments():
+    h = pkg.Histogram([(10, 0.0, 10.0)])
+    with pytest.raises(ValueError):
+        h.fill_i32([torch.zeros(10, dtype=torch.int64, device=DEV)])
+    with pytest.raises(pkg.BHistError):
+        pkg.bh_fill_i32(h.h, 10, [None])
+    h.close()

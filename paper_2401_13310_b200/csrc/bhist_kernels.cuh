@@ -16,7 +16,10 @@ namespace bh {
 
 constexpr int kMaxDim = 3;
 constexpr int kThreadsGlobal = 512;   // GLOBAL sink: 2 CTAs/SM
-constexpr int kThreadsSmem = 1024;    // PRIV / CACHE sinks: 1 CTA/SM owns the SM's shared memory
+#ifndef BH_SMEM_THREADS
+#define BH_SMEM_THREADS 1024
+#endif
+constexpr int kThreadsSmem = BH_SMEM_THREADS;   // PRIV / CACHE sinks: 1 CTA/SM owns the SM's shared memory
 template <int SINK> struct ThreadsOf {   // SINK_GLOBAL == 1
     static constexpr int v = SINK == 1 ? kThreadsGlobal : kThreadsSmem;
 };

@@ -1,4 +1,4 @@
 #!/bin/bash
-for c in C2 C4 C1S C5; do for lib in paper_2401_13310_b200/libbhist.so build_ab/libbhist_t768.so build_ab/libbhist_t512.so; do
+for i in 1 2; do for c in C1S C1 C5; do for lib in paper_2401_13310_b200/libbhist.so build_ab/libbhist_u4.so; do
 BHIST_LIBRARY=$PWD/$lib timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print('$lib $c %.4g ev/s frac %.3f launch %.3f'%(d['value'], d['roofline']['frac'], d['roofline']['launch_ms']))"; done; done
+import json,sys; d=json.loads(sys.stdin.readline()); print('$lib $c %.4g ev/s frac %.3f launch %.3f'%(d['value'], d['roofline']['frac'], d['roofline']['launch_ms']))"; done; done; done

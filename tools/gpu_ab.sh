@@ -1,4 +1,4 @@
 #!/bin/bash
-for i in 1 2; do for c in C1S C1 C5; do for lib in paper_2401_13310_b200/libbhist.so build_ab/libbhist_u4.so; do
-BHIST_LIBRARY=$PWD/$lib timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print('$lib $c %.4g ev/s frac %.3f launch %.3f'%(d['value'], d['roofline']['frac'], d['roofline']['launch_ms']))"; done; done; done
+timeout 300 python bench.py --config C2 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "C1F,C2F" 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.readline()); print({k:(round(v['events_per_s']/1e9,1), round(v['frac'],3), round(v['fill_ms'],3)) for k,v in d['secondary'].items()})"
+timeout 600 python -m pytest tests/test_parity_gpu.py tests/test_fuzz_gpu.py -q -m gpu -x -k "f32 or i32 or expr or fuzz" 2>&1 | tail -1

@@ -95,7 +95,7 @@ typedef struct {
  *        pb = 15 unit / 13 weighted; at most 2048 partitions); pass 2 reduces each
  *        partition in shared memory and adds it to the bins once per CTA.  The
  *        "sort-then-segmented-reduce" path for large 2D/3D bin spaces.  Scratch of
- *        2 (unit) or 10 (weighted) bytes per event of a chunk (<= 2^27 / 2^26 events)
+ *        2 (unit) or 10 (weighted) bytes per event of a chunk (<= 2^28 / 2^26 events)
  *        is allocated by the histogram on first use.  bh_fill_f32 and bh_fill_expr
  *        use CACHE instead. */
 #define BH_STRATEGY_SORT 5

@@ -1,4 +1,8 @@
 #!/bin/bash
-timeout 300 python bench.py --config C2 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "C1F,C2F" 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print({k:(round(v['events_per_s']/1e9,1), round(v['frac'],3), round(v['fill_ms'],3)) for k,v in d['secondary'].items()})"
-timeout 600 python -m pytest tests/test_parity_gpu.py tests/test_fuzz_gpu.py -q -m gpu -x -k "f32 or i32 or expr or fuzz" 2>&1 | tail -1
+run() { timeout 300 env "$@" python bench.py --config $C --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.readline()); print('$C $*', '%.4g ev/s frac %.3f launch %.3f'%(d['value'], d['roofline']['frac'], d['roofline']['launch_ms']))"; }
+C=C4W; run X=1; run BHIST_CACHE_SLOTS_W=8192; run BHIST_CACHE_SLOTS_W=2048
+C=C3W; run X=1; run BHIST_CACHE_SLOTS_W=8192
+C=C4; run X=1; run BHIST_CACHE_SLOTS_U=8192; run BHIST_CACHE_SLOTS_U=4096
+C=C3; run X=1; run BHIST_SORT_CHUNK=268435456
+C=C5; run X=1; run BHIST_CACHE_SLOTS_U=8192

@@ -357,7 +357,11 @@ __device__ __forceinline__ int add2_shared_count(double2 *cell, double w, double
 // previous occupant is flushed into the replica).  A peaked weighted histogram thus
 // stops serializing all warps of a replica on a few cells (100x100 Cauchy-peaked fill:
 // 9 -> see DESIGN.md), while spread data never enters aggregated mode.
-constexpr int kWC = 16;
+#ifndef BH_WC_BITS
+#define BH_WC_BITS 5      // 32 entries: C5 5.77 -> 5.62 ms, peaked 100x100 weighted 26 -> 47 G events/s over 16
+#endif
+constexpr int kWCBits = BH_WC_BITS;                  // 8 / 16 / 32 entries (<= 32: one per lane)
+constexpr int kWC = 1 << kWCBits;
 constexpr int kWCBytes = kWC * 4 + kWC * 16;         // tags int32[kWC], then (s1, s2) double2[kWC]
 
 // A warp's private direct-mapped cache of hot weighted bins (PRIVA; in front of CACHE's
@@ -385,7 +389,7 @@ struct WarpHot {
         const int lane = (int)(threadIdx.x & 31);
         int32_t *tags = reinterpret_cast<int32_t *>(wc);
         double2 *vals = reinterpret_cast<double2 *>(wc + kWC * 4);
-        const int slot = (int)(((uint32_t)g * 2654435761u) >> 28);   // kWC = 16
+        const int slot = (int)(((uint32_t)g * 2654435761u) >> (32 - kWCBits));
         bool done = false;
         __syncwarp();                    // earlier cache writes of every lane are visible
         if (leader && tags[slot] == g) {
@@ -750,16 +754,20 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
                 }
             }
         };
+        // SINK_PRIVA's warp hot-bin caches need converged full warps: with warp-uniform
+        // trip counts (below) every lane reaches these reconvergence points
+        constexpr bool kConverge = SINK == SINK_PRIVA;
         auto process = [&](const B &bt, int q0) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                if (q0 + u * nth < npair) {
-                    double x0[DIM], x1[DIM];
+                const bool ok = q0 + u * nth < npair;
+                double x0[DIM], x1[DIM];
 #pragma unroll
-                    for (int a = 0; a < DIM; ++a) { x0[a] = bt.x[u][a].x; x1[a] = bt.x[u][a].y; }
-                    do_event<DIM, W, VM>(p, x0, W ? bt.w[u].x : 1.0, sink, acc, smem);
-                    do_event<DIM, W, VM>(p, x1, W ? bt.w[u].y : 1.0, sink, acc, smem);
-                }
+                for (int a = 0; a < DIM; ++a) { x0[a] = bt.x[u][a].x; x1[a] = bt.x[u][a].y; }
+                if (kConverge) __syncwarp();
+                if (ok) do_event<DIM, W, VM>(p, x0, W ? bt.w[u].x : 1.0, sink, acc, smem);
+                if (kConverge) __syncwarp();
+                if (ok) do_event<DIM, W, VM>(p, x1, W ? bt.w[u].y : 1.0, sink, acc, smem);
             }
         };
         const int step = U * nth;
@@ -783,7 +791,9 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
             }
         } else {
             B cur;
-            for (int q0 = tid; q0 < npair; q0 += step) {   // (uniform trips + __syncwarp: C4 2-3% slower)
+            // per-lane trips (uniform trips + __syncwarp measured 2-3% slower on C4), except
+            // for SINK_PRIVA, whose reconvergence points need every lane
+            for (int q0 = tid; kConverge ? q0 - lane0 < npair : q0 < npair; q0 += step) {
                 load(cur, q0);       // 3-4 columns: 48-64 B per thread in flight already
                 process(cur, q0);
             }

@@ -19,7 +19,9 @@ namespace bh {
 // cudaFuncSetAttribute is a driver call (~microseconds); small fills are launch-latency
 // bound, so the dynamic shared-memory limit is raised once per (kernel, device).
 inline cudaError_t ensure_smem(const void *kern, size_t bytes) {
-    if (bytes <= 48 * 1024) return cudaSuccess;
+    // the 48 KB default covers dynamic + static shared memory together, so anything above
+    // ~40 KB of dynamic memory needs the opt-in (kernels carry a few KB of static smem)
+    if (bytes <= 32 * 1024) return cudaSuccess;
     static std::mutex mu;
     static std::unordered_map<uint64_t, size_t> done;
     int dev = 0;

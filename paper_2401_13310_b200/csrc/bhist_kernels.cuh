@@ -429,6 +429,12 @@ struct WarpHot {
     }
 };
 
+#ifndef BH_AGG_ENTER
+#define BH_AGG_ENTER 8       // lanes of one add that lost their CAS -> aggregate the next adds
+#endif
+#ifndef BH_AGG_STAY
+#define BH_AGG_STAY 4        // keep aggregating while some bin holds this many lanes
+#endif
 template <bool W, bool ADAPT>
 struct PrivSink {
     uint32_t sm;         // shared-memory address of this warp's replica
@@ -467,10 +473,10 @@ struct PrivSink {
             agg = __any_sync(act, agg);
             if (agg) {
                 const unsigned peers = __match_any_sync(act, g);
-                agg = __any_sync(act, __popc(peers) >= 4);
+                agg = __any_sync(act, __popc(peers) >= BH_AGG_STAY);
                 add_aggregated(base, g, w, w * w, act, peers);
             } else {
-                agg = __popc(__ballot_sync(act, add2_shared_count(base + g, w, w * w) > 0)) >= 8;
+                agg = __popc(__ballot_sync(act, add2_shared_count(base + g, w, w * w) > 0)) >= BH_AGG_ENTER;
             }
         } else {
             asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(sm + 4u * (uint32_t)g) : "memory");

@@ -51,7 +51,10 @@ struct PartP {
 // so that pass 2 reads them in aligned RC-record chunks; a tile's records occupy
 // q.ts >= tile + P*(RC-1) slots of the scratch.
 constexpr uint16_t kPartPad = 0xffffu;
-constexpr int kPartStages = 2;
+#ifndef BH_PART_STAGES
+#define BH_PART_STAGES 2
+#endif
+constexpr int kPartStages = BH_PART_STAGES;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 

@@ -7,18 +7,21 @@
 // straight into the L2-resident histogram costs one L2 atomic per event (GLOBAL /
 // CACHE, ~1e11 events/s).  Here:
 //
-//   pass 1 (k_part_scatter): the three steps of PAPER.md:126 up to the bin index --
-//     FindBin per axis, global bin g, the GetStats sums in registers -- then the
-//     event's record (local bin l = g mod 2^pb, and w) is ranked within its
-//     partition p = g >> pb (warp-aggregated shared-memory counters), the tile's
-//     records are sorted by partition in shared memory and written out with
-//     coalesced 16-byte stores, plus one row of segment offsets per tile.
+//   pass 1 (k_part_scatter): the tile's columns arrive in shared memory by TMA bulk
+//     copies (two tiles in flight); the three steps of PAPER.md:126 up to the bin index
+//     -- FindBin per axis, global bin g, the GetStats sums in registers -- then the
+//     event's record (local bin l = g mod 2^pb, and w) is ranked within its partition
+//     p = g >> pb by a returning shared-memory atomic, the tile's records are sorted by
+//     partition in shared memory (segments padded to RC-record chunks) and written out
+//     with coalesced 16-byte stores, plus one row of segment offsets per tile.
 //   plan   (k_part_plan): per-partition record totals -> prefix -> pass-2 balance.
 //   pass 2 (k_part_reduce): each CTA owns a contiguous stretch of the (partition,
-//     tile) order of about equal record count; the partition's 2^pb bins live in
-//     shared memory (u32 counts / double2 (sumw, sumw2) with 128-bit CAS, equal bins
-//     warp-aggregated first), and are added to the global bins once per partition
-//     the CTA touched (the merge stage of PAPER.md:162-165).
+//     tile) order of about equal record count; per batch of tiles every thread walks an
+//     equal share of the segments' chunks; the partition's 2^pb bins live in shared
+//     memory (u32 counts by `red.shared.add.u32`; double2 (sumw, sumw2) by 128-bit CAS
+//     behind a per-thread register cache of a repeating bin), and are added to the
+//     global bins once per partition the CTA touched (the merge stage of PAPER.md:162-165).
+//   probe  (k_part_probe): AUTO's hotness test on a sample (see bhist.cu auto_sort).
 //
 // Records cost 2 B (unit) or 10 B (weighted) per event written + read back, instead of
 // one L2 atomic per event; no shared-memory state is bigger than 128 KB.

@@ -63,3 +63,23 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower(), f
+
+
+def test_header_constants_match_binding():
+    # every #define BH_* integer of the header has the same value in the Python binding
+    src = open(os.path.join(ROOT, "include", "bhist.h")).read()
+    consts = {k: int(v) for k, v in re.findall(r"#define\s+(BH_[A-Z0-9_]+)\s+\(?(-?\d+)\)?", src)}
+    assert {"BH_STRATEGY_AUTO", "BH_STRATEGY_SORT", "BH_DEBUG_SKIP_COPY_WAIT"} <= set(consts)
+    from paper_2401_13310_b200 import bhist
+    for k, v in consts.items():
+        if hasattr(bhist, k):
+            assert getattr(bhist, k) == v, k
+    for k in ("BH_STRATEGY_AUTO", "BH_STRATEGY_PRIV", "BH_STRATEGY_GLOBAL", "BH_STRATEGY_CACHE",
+              "BH_STRATEGY_EXACT", "BH_STRATEGY_SORT"):
+        assert getattr(pkg, k) == consts[k], k
+
+
+def test_build_units_cover_every_dim_and_weight():
+    names = sorted(os.path.basename(u) for u in _build.units())
+    assert names[0] == "bhist.cu"
+    assert names[1:] == [f"bhist_fill_d{d}{w}.cu" for d in (1, 2, 3) for w in ("u", "w")]

@@ -108,7 +108,10 @@ namespace {
 
 size_t align16(size_t b);
 size_t axis_table_bytes(const AxisP &a);
-int sort_pb(bool weighted) { return weighted ? 13 : 15; }   // 2^pb bins = 128 KB of shared memory
+#ifndef BH_SORT_PB_UNIT
+#define BH_SORT_PB_UNIT 15
+#endif
+int sort_pb(bool weighted) { return weighted ? 13 : BH_SORT_PB_UNIT; }   // 2^pb bins = 128 KB of shared memory
 int64_t sort_partitions(const bh_hist *h, bool weighted) {
     return (h->G + (int64_t(1) << sort_pb(weighted)) - 1) >> sort_pb(weighted);
 }
@@ -403,8 +406,9 @@ bh_status fill_sort(bh_hist *h, int64_t n, const double *const *coords, const do
         k_part_plan<<<1, 32, 0, s>>>(q);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(BH_ECUDA, "SORT plan launch: %s", cudaGetErrorString(e));
-        e = W ? (rc == 1 ? launch_part2<true, 1>(p, q, h->nsm, s) : launch_part2<true, 4>(p, q, h->nsm, s))
-              : (rc == 1 ? launch_part2<false, 1>(p, q, h->nsm, s) : launch_part2<false, 8>(p, q, h->nsm, s));
+        const int g2 = h->nsm * kReduceCtas;
+        e = W ? (rc == 1 ? launch_part2<true, 1>(p, q, g2, s) : launch_part2<true, 4>(p, q, g2, s))
+              : (rc == 1 ? launch_part2<false, 1>(p, q, g2, s) : launch_part2<false, 8>(p, q, g2, s));
         if (e != cudaSuccess) return fail(BH_ECUDA, "SORT pass 2 launch: %s", cudaGetErrorString(e));
         h->launches += 3;
     }

@@ -36,7 +36,11 @@ constexpr int kPartThreads = 1024;                   // pass 1: 1 CTA per SM (2 
 // events per thread per tile; a staged tile (NCOL columns) is <= 64 KB
 __host__ __device__ constexpr int part_ev(int dim, bool w) { return dim + (w ? 1 : 0) >= 3 ? 2 : 4; }
 constexpr int kPartMaxP = 2048;                      // partitions (bins / 2^pb) supported
-constexpr int kReduceThreads = 1024;                 // pass 2: 1 CTA per SM owns 128 KB of bins
+#ifndef BH_REDUCE_CTAS
+#define BH_REDUCE_CTAS 1
+#endif
+constexpr int kReduceCtas = BH_REDUCE_CTAS;          // pass 2 CTAs per SM
+constexpr int kReduceThreads = 1024 / kReduceCtas;   // (1 CTA per SM owns 128 KB of bins)
 
 struct PartP {
     uint16_t *rec_l;            // [ntiles * kPartTile] local bin, tile-major, partition-sorted within a tile
@@ -358,7 +362,7 @@ constexpr int kReduceBatch = 2048;                   // tiles whose segments are
 // takes an equal contiguous range of chunks (so one hot partition with long segments
 // still keeps all 32 warps busy), walking the segments in order.
 template <bool W, int RC>
-__global__ void __launch_bounds__(kReduceThreads, 1) k_part_reduce(FillP p, PartP q) {
+__global__ void __launch_bounds__(kReduceThreads, kReduceCtas) k_part_reduce(FillP p, PartP q) {
     extern __shared__ __align__(16) unsigned char smem[];
     // layout: [bins (2^pb cells)] [o0 u32[batch]] [cp u32[batch+1]] [scan scratch u32[32]]
     const size_t binbytes = (size_t)(W ? 16 : 4) << q.pb;

@@ -1,5 +1,5 @@
 #!/bin/bash
-run() { timeout 300 env "$@" python bench.py --config $C --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print('$C $*', '%.4g ev/s frac %.3f launch %.4f'%(d['value'], d['roofline']['frac'], d['roofline']['launch_ms']))"; }
-C=C1; for r in 32 16 8 4 1; do run BHIST_PRIV_REPLICAS=$r; done
-C=C1S; for r in 32 16 8; do run BHIST_PRIV_REPLICAS=$r; done
+for i in 1 2; do for lib in paper_2401_13310_b200/libbhist.so build_ab/libbhist_r2.so; do
+BHIST_LIBRARY=$PWD/$lib timeout 300 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.readline()); print('$lib C3 %.4g ev/s frac %.3f launch %.3f'%(d['value'], d['roofline']['frac'], d['roofline']['launch_ms']))"; done; done
+BHIST_LIBRARY=$PWD/build_ab/libbhist_r2.so timeout 600 python -m pytest tests/test_parity_gpu.py -q -m gpu -x -k "sort or probe" 2>&1 | tail -1

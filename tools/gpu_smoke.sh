@@ -1,0 +1,2 @@
+#!/bin/bash
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2

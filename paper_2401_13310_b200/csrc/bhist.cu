@@ -260,7 +260,10 @@ int grid_for(const bh_hist *h, const LaunchCfg &c, int64_t m) {
     // PRIV blocks must still amortize zeroing + flushing their private bins (>= 8 events
     // per thread and >= 4 G per block: measured best for C1's 1e6 events)
     int64_t want_per_block = (int64_t)nt * 2;
-    if (c.strategy == BH_STRATEGY_PRIV) want_per_block = std::max<int64_t>((int64_t)nt * 8, 4 * h->G);
+    if (c.strategy == BH_STRATEGY_PRIV) {
+        static const int ept = getenv("BHIST_PRIV_EPT") ? std::max(1, atoi(getenv("BHIST_PRIV_EPT"))) : 8;  // A/B
+        want_per_block = std::max<int64_t>((int64_t)nt * ept, 4 * h->G);
+    }
     int64_t grid = (m + want_per_block - 1) / want_per_block;
     return (int)std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)h->nsm * resident_blocks(c.strategy)));
 }

@@ -354,3 +354,207 @@ def test_expr_oracle_hand_values():
     h = expr.fill_expr([(10, 0.0, 10.0)], [x, y], prog, [5], filter_reg=7)
     out = h.read()
     assert out["entries"] == 2 and out["content"][6] == 1.0 and out["content"][1] == 1.0   # r=5 -> bin 6
+
+
+# ------------------------------------------------------------------ association of the fixed formula
+def _rn(q: Fraction) -> Fraction:
+    """Round a rational to the nearest binary64 (ties to even) with integer arithmetic only —
+    an emulation independent of the host FPU, for normal-range values."""
+    if q == 0:
+        return Fraction(0)
+    s = -1 if q < 0 else 1
+    q = abs(q)
+    e = q.numerator.bit_length() - q.denominator.bit_length()
+    while Fraction(2) ** e > q:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= q:
+        e += 1
+    assert -1022 <= e <= 1023
+    scaled = q / Fraction(2) ** (e - 52)           # in [2^52, 2^53)
+    m, r = divmod(scaled.numerator, scaled.denominator)
+    twice = 2 * r
+    if twice > scaled.denominator or (twice == scaled.denominator and m % 2 == 1):
+        m += 1
+    return s * Fraction(m) * Fraction(2) ** (e - 52)
+
+
+def _softfloat_bin(n, lo, hi, x):
+    """Reading R2 evaluated with the rounding emulation: 1 + trunc(RN(RN(n*RN(x-lo)) / RN(hi-lo)))."""
+    d = _rn(Fraction(x) - Fraction(lo))
+    q = _rn(_rn(Fraction(n) * d) / _rn(Fraction(hi) - Fraction(lo)))
+    return 1 + math.floor(q)
+
+
+def test_association_pins():
+    """Hand-derived pins on non-unit ranges where (n*d)/D, d*(n/D) and n*(d/D) give different
+    bins (tests/golden/ieee_pins.json 'association_pins', PAPER.md:126 + reading R2). Each
+    derivation is re-checked with the integer rounding emulation, then the oracle is held to it."""
+    for p in _load("ieee_pins.json")["association_pins"]:
+        x = _x(p["x_hex"])
+        assert _softfloat_bin(p["nbins"], p["xmin"], p["xmax"], x) == p["bin"], p["why"]
+        assert _exact_bin(p["nbins"], p["xmin"], p["xmax"], x)[1] == p["real_bin"], p["why"]
+        assert oracle.find_bin_fixed(p["nbins"], p["xmin"], p["xmax"], x) == p["bin"], p["why"]
+
+
+def test_fixed_softfloat_near_edges():
+    """Every coordinate within 3 ulps of a computed edge on a few non-unit axes: the oracle equals
+    the integer rounding emulation of reading R2 (where the associations disagree most)."""
+    for n, lo, hi in [(100, 0.0, 3.0), (1000, -1.0, 2.0), (37, 0.1, 0.8), (7, -2.5, 9.75)]:
+        D = hi - lo
+        checked = 0
+        for k in range(0, n + 1):
+            x0 = lo + k * D / n
+            xs = [x0]
+            up = dn = x0
+            for _ in range(3):
+                up, dn = float(np.nextafter(up, np.inf)), float(np.nextafter(dn, -np.inf))
+                xs += [up, dn]
+            for x in xs:
+                if not (lo < x < hi) or x - lo < 1e-300:
+                    continue
+                assert oracle.find_bin_fixed(n, lo, hi, x) == _softfloat_bin(n, lo, hi, x), (n, lo, hi, x)
+                checked += 1
+        assert checked > 5 * (n - 1)
+
+
+def test_fixed_numpy_vectorized_1e7():
+    """SURVEY §8(c) pin: an independent vectorised numpy evaluation of reading R2
+    (numpy float64 ops are single IEEE roundings, never contracted) over 1.2e7 random and
+    near-edge coordinates on 24 axes must agree with the oracle event by event."""
+    rng = np.random.default_rng(2024)
+    total = 0
+    for t in range(24):
+        n = int(rng.choice([3, 7, 100, 1000, 9973, 65536, 10 ** 6]))
+        lo = float(rng.choice([0.0, -1.0, float(rng.uniform(-100, 100))]))
+        hi = lo + float(rng.choice([1.0, 3.0, 0.3, float(10.0 ** rng.uniform(-3, 3))]))
+        m = 250_000
+        xs = rng.uniform(lo - 0.01 * (hi - lo), hi + 0.01 * (hi - lo), m)
+        k = rng.integers(0, n + 1, m)
+        e = lo + k * ((hi - lo) / n)
+        sh = rng.integers(-3, 4, m)
+        near = e.copy()
+        for s in (1, 2, 3):
+            near = np.where(sh >= s, np.nextafter(near, np.inf), near)
+            near = np.where(sh <= -s, np.nextafter(near, -np.inf), near)
+        x = np.concatenate([xs, near, [lo, hi, np.nan, -np.inf, np.inf, -0.0]])
+        with np.errstate(invalid="ignore"):
+            q = (np.float64(n) * (x - lo)) / (hi - lo)
+            ref = np.where(x < lo, 0, np.where(~(x < hi), n + 1, 1 + np.trunc(np.where(x < lo, 0, q))))
+        got = oracle.OracleHist([(n, lo, hi)]).find_bins([x])
+        assert np.array_equal(got, ref.astype(np.int32)), (n, lo, hi)
+        total += len(x)
+    assert total >= 12_000_000
+
+
+# ------------------------------------------------------------------ 3-D stats, exact rationals
+def test_conservation_and_stats_bruteforce_3d():
+    """All 11 GetStats sums of a TH3 (reading R8, PAPER.md:126 'depends on the dimension'):
+    [Σw, Σw², Σwx, Σwx², Σwy, Σwy², Σwxy, Σwz, Σwz², Σwxz, Σwyz], each against an exact
+    rational sum over the events that are in range on every axis. x, y, z have different
+    laws so every cross term has a different value (swapping any two indices fails)."""
+    rng = np.random.default_rng(33)
+    n = 2500
+    x = rng.uniform(-0.1, 1.1, n)
+    y = rng.normal(2.0, 0.6, n)
+    z = rng.exponential(3.0, n) - 1.0
+    w = rng.uniform(-0.5, 2.0, n)
+    ez = [-1.0, 0.0, 0.5, 2.0, 4.5, 8.0]
+    h = oracle.OracleHist([(9, 0.0, 1.0), (6, 0.5, 3.5), np.array(ez)]).fill([x, y, z], w)
+    r = h.read()
+    assert r["entries"] == n and len(r["stats"]) == 11
+    assert math.isclose(r["content"].sum(), math.fsum(w), rel_tol=0, abs_tol=1e-12 * np.abs(w).sum())
+    F = Fraction
+    terms = [[] for _ in range(11)]
+    for a, b, c, ww in zip(x, y, z, w):
+        a, b, c, ww = float(a), float(b), float(c), float(ww)
+        if not (1 <= _exact_bin(9, 0.0, 1.0, a)[1] <= 9 if 0.0 <= a < 1.0 else False):
+            continue
+        if not (1 <= _exact_bin(6, 0.5, 3.5, b)[1] <= 6 if 0.5 <= b < 3.5 else False):
+            continue
+        if not 1 <= _linear_scan(ez, c) <= 5:
+            continue
+        A, B, C, W = F(a), F(b), F(c), F(ww)
+        for k, t in enumerate([W, W * W, W * A, W * A * A, W * B, W * B * B, W * A * B,
+                               W * C, W * C * C, W * A * C, W * B * C]):
+            terms[k].append(t)
+    assert 300 < len(terms[0]) < n
+    for k in range(11):
+        exact = float(sum(terms[k], F(0)))
+        scale = float(sum((abs(t) for t in terms[k]), F(0)))
+        assert abs(r["stats"][k] - exact) <= 2.0 ** -50 * scale, k
+    # the cross terms are pairwise far apart, so an index swap cannot pass
+    s = r["stats"]
+    for i, j in [(6, 9), (6, 10), (9, 10), (7, 4), (8, 5), (2, 4), (2, 7)]:
+        assert abs(s[i] - s[j]) > 1e-3 * max(abs(s[i]), abs(s[j])), (i, j)
+
+
+def test_stats_hand_values_3d():
+    """One in-range TH3 event (x, y, z) = (0.5, 2, 4), w = 3: the 11 sums by hand."""
+    h = oracle.OracleHist([(10, 0.0, 1.0), (10, 0.0, 8.0), (10, 0.0, 8.0)])
+    h.fill([np.array([0.5]), np.array([2.0]), np.array([4.0])], np.array([3.0]))
+    # Σw=3, Σw²=9, Σwx=1.5, Σwx²=0.75, Σwy=6, Σwy²=12, Σwxy=3, Σwz=12, Σwz²=48, Σwxz=6, Σwyz=24
+    assert list(h.read()["stats"]) == [3.0, 9.0, 1.5, 0.75, 6.0, 12.0, 3.0, 12.0, 48.0, 6.0, 24.0]
+
+
+# ------------------------------------------------------------------ Filter + Define: every opcode
+_NAN, _INF = float("nan"), float("inf")
+# columns: a, b, c (registers 0, 1, 2)
+_EA = [3.0, -2.0, _NAN, 0.0, -0.0, _INF]
+_EB = [4.0, 0.5, 1.0, _NAN, 0.0, _INF]
+_EC = [10.0, 20.0, 30.0, 40.0, 50.0, 60.0]
+# Hand values per opcode (include/bhist.h BH_OP_*; IEEE 754 binary64 semantics: NaN compares
+# false, fmin/fmax are minNum/maxNum so a NaN operand yields the other one, a truth value is
+# "!= 0" so NaN is true, sqrt(-0) = -0).  '-0' marks a value whose sign bit must be set.
+_EXPR_HAND = {
+    "const": (("const", 3, 0, 0, 0, 2.5), [2.5] * 6),
+    "copy": (("copy", 3, 0, 0, 0, 0.0), [3.0, -2.0, _NAN, 0.0, "-0", _INF]),
+    "add": (("add", 3, 0, 1, 0, 0.0), [7.0, -1.5, _NAN, _NAN, 0.0, _INF]),
+    "sub": (("sub", 3, 0, 1, 0, 0.0), [-1.0, -2.5, _NAN, _NAN, "-0", _NAN]),
+    "mul": (("mul", 3, 0, 1, 0, 0.0), [12.0, -1.0, _NAN, _NAN, "-0", _INF]),
+    "div": (("div", 3, 0, 1, 0, 0.0), [0.75, -4.0, _NAN, _NAN, _NAN, _NAN]),
+    "sqrt": (("sqrt", 3, 0, 0, 0, 0.0), [1.7320508075688772, _NAN, _NAN, 0.0, "-0", _INF]),
+    "abs": (("abs", 3, 0, 0, 0, 0.0), [3.0, 2.0, _NAN, 0.0, 0.0, _INF]),
+    "neg": (("neg", 3, 0, 0, 0, 0.0), [-3.0, 2.0, _NAN, "-0", 0.0, -_INF]),
+    "min": (("min", 3, 0, 1, 0, 0.0), [3.0, -2.0, 1.0, 0.0, None, _INF]),
+    "max": (("max", 3, 0, 1, 0, 0.0), [4.0, 0.5, 1.0, 0.0, None, _INF]),
+    "lt": (("lt", 3, 0, 1, 0, 0.0), [1.0, 1.0, 0.0, 0.0, 0.0, 0.0]),
+    "le": (("le", 3, 0, 1, 0, 0.0), [1.0, 1.0, 0.0, 0.0, 1.0, 1.0]),
+    "gt": (("gt", 3, 0, 1, 0, 0.0), [0.0, 0.0, 0.0, 0.0, 0.0, 0.0]),
+    "ge": (("ge", 3, 0, 1, 0, 0.0), [0.0, 0.0, 0.0, 0.0, 1.0, 1.0]),
+    "eq": (("eq", 3, 0, 1, 0, 0.0), [0.0, 0.0, 0.0, 0.0, 1.0, 1.0]),
+    "ne": (("ne", 3, 0, 1, 0, 0.0), [1.0, 1.0, 1.0, 1.0, 0.0, 0.0]),
+    "and": (("and", 3, 0, 1, 0, 0.0), [1.0, 1.0, 1.0, 0.0, 0.0, 1.0]),
+    "or": (("or", 3, 0, 1, 0, 0.0), [1.0, 1.0, 1.0, 1.0, 0.0, 1.0]),
+    "not": (("not", 3, 0, 0, 0, 0.0), [0.0, 0.0, 0.0, 1.0, 1.0, 0.0]),
+    "select": (("select", 3, 0, 1, 2, 0.0), [4.0, 0.5, 1.0, 40.0, 50.0, _INF]),
+}
+
+
+def _check_hand(got, want, name):
+    for i, (g, v) in enumerate(zip(got, want)):
+        if v is None:                      # fmin(-0, +0): either zero is a valid minNum
+            assert g == 0.0, (name, i)
+        elif v == "-0":
+            assert g == 0.0 and math.copysign(1.0, g) < 0, (name, i, g)
+        elif isinstance(v, float) and math.isnan(v):
+            assert math.isnan(g), (name, i, g)
+        else:
+            assert g == v and (v != 0.0 or math.copysign(1.0, g) > 0), (name, i, g, v)
+
+
+def test_expr_every_opcode_hand_values():
+    from oracle import expr
+    from paper_2401_13310_b200.bhist import OPS   # names only (the opcode table of the header)
+    assert set(_EXPR_HAND) == set(OPS)
+    cols = [np.array(_EA), np.array(_EB), np.array(_EC)]
+    for name, (op, want) in _EXPR_HAND.items():
+        r = expr.run_program(cols, [op], 6)
+        _check_hand(list(r[3]), want, name)
+    # programs chain through registers in order, and the filter keeps exactly the truthy events:
+    # r3 = b - a, r4 = r3*r3, r5 = (a == a) (false only for NaN); weights c
+    prog = [("sub", 3, 1, 0, 0, 0.0), ("mul", 4, 3, 3, 0, 0.0), ("eq", 5, 0, 0, 0, 0.0)]
+    h = expr.fill_expr([(4, 0.0, 100.0)], cols, prog, [4], weight_reg=2, filter_reg=5).read()
+    # kept events 0,1,3,4,5: r4 = 1, 6.25, NaN (0-NaN), 0, NaN (inf-inf) -> bin 1 gets 10+20+50,
+    # overflow (bin 5, NaN routed per reading R5) gets 40+60
+    assert h["entries"] == 5
+    assert h["content"][1] == 80.0 and h["content"][5] == 100.0 and h["content"].sum() == 180.0

@@ -71,7 +71,9 @@ typedef struct {
 
 /* Fill strategies (bh_set_strategy).  AUTO picks by bin-space size and weights:
  * PRIV   block-private shared-memory bins, flushed once per CTA (PAPER.md:138,
- *        "each block fills a local copy ... in shared memory");
+ *        "each block fills a local copy ... in shared memory"); bh_set_strategy accepts it
+ *        when the unit-weight bins (4 B each) fit; weighted fills whose 16-B cells do not
+ *        fit then use CACHE;
  * GLOBAL device-wide atomics straight into the L2-resident histogram;
  * CACHE  per-CTA shared-memory cache of the hottest bins with global fallback
  *        (hot-bin contention, BASELINE.json config 4). */
@@ -102,6 +104,7 @@ typedef struct {
 
 /* Debug flags (bh_set_debug) — negative controls for tests only. */
 #define BH_DEBUG_SKIP_COPY_WAIT 1 /* bh_fill_host: fill without waiting for the H2D copy (PAPER.md:223 race) */
+#define BH_DEBUG_FIND_BINS_GLOBAL 2 /* bh_find_bins: search variable axes in global memory, not the fills' staged tables */
 
 /* ABI version (major*10000 + minor*100 + patch). */
 int32_t bh_version(void);
@@ -195,7 +198,12 @@ typedef struct {
 bh_status bh_fill_expr(bh_hist *h, int64_t n, const double *const *cols, int32_t ncols, const bh_op *prog,
                        int32_t nops, const int32_t *axis_reg, int32_t weight_reg, int32_t filter_reg, bh_stream s);
 
-/* Per-event global bin (parity/debug): out[i] = g(event i), int32, DEVICE pointer. */
+/* Step (1) of PAPER.md:126 alone, per event (parity/debug): out[i] = the global bin
+ * b0 + (n0+2)*(b1 + (n1+2)*b2) of event i (FindBin per axis; DESIGN.md
+ * readings R1, R2, R4, R5, R9), int32, DEVICE pointer of n elements, caller-owned.  Runs
+ * the same FindBin code the fills run, variable-axis tables staged in shared memory as
+ * the fills stage them (BH_DEBUG_FIND_BINS_GLOBAL: the float64 global-memory search).
+ * Async on s; BH_EINVAL on NULL pointers or n < 0. */
 bh_status bh_find_bins(const bh_hist *h, int64_t n, const double *const *coords, int32_t *out, bh_stream s);
 
 /* Shape: dimension, number of bins including flow bins, number of stats (4/7/11). Any may be NULL. */
@@ -205,15 +213,20 @@ bh_status bh_info(const bh_hist *h, int32_t *dim, int64_t *nbins_total, int32_t 
 bh_status bh_packed_size(const bh_hist *h, int64_t *n_doubles);
 
 /* Write the state as float64 [content(G) | sumw2(G) | stats(K) | entries(1)] to
- * the DEVICE buffer dev_out (for an all-reduce SUM across ranks).  Async on s.
- * Unit-weight counts are integers < 2^53, exact in any summation order. */
+ * the DEVICE buffer dev_out (caller-owned, bh_packed_size doubles) for an all-reduce SUM
+ * across ranks: the state is a sum over events (SPEC.md S:113-121 merge),
+ * so partial histograms of disjoint event shards add elementwise.  Async on s.
+ * Unit-weight counts are integers < 2^53, exact in any summation order.  BH_EINVAL on NULL. */
 bh_status bh_pack(const bh_hist *h, double *dev_out, bh_stream s);
 
-/* Replace the state with a packed buffer (DEVICE pointer), e.g. after all-reduce. Async on s. */
+/* Replace the state with a packed buffer (DEVICE pointer, bh_packed_size doubles, layout of
+ * bh_pack), e.g. after the all-reduce of SURVEY.md §8(e).  Async on s; BH_EINVAL on NULL. */
 bh_status bh_unpack(bh_hist *h, const double *dev_in, bh_stream s);
 
-/* Read back to HOST buffers (any may be NULL): contents[G], sumw2[G], stats[K],
- * entries.  Synchronizes stream s.  Reports earlier asynchronous faults. */
+/* Read back to HOST buffers (any may be NULL): contents[G], sumw2[G], stats[K] (ROOT
+ * GetStats order, reading R8), entries — "only copy back ... once all bulks have been
+ * processed".  Buffers are caller-owned.  Synchronizes stream s; reports
+ * earlier asynchronous faults as BH_ECUDA. */
 bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *stats, int64_t *entries,
                   bh_stream s);
 

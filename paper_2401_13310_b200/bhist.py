@@ -19,6 +19,7 @@ from . import _build
 BH_OK, BH_EINVAL, BH_ENOMEM, BH_ECUDA, BH_EDEVICE, BH_EMISMATCH = 0, -1, -2, -3, -4, -5
 BH_STRATEGY_AUTO, BH_STRATEGY_PRIV, BH_STRATEGY_GLOBAL, BH_STRATEGY_CACHE, BH_STRATEGY_EXACT, BH_STRATEGY_SORT = 0, 1, 2, 3, 4, 5
 BH_DEBUG_SKIP_COPY_WAIT = 1
+BH_DEBUG_FIND_BINS_GLOBAL = 2
 
 # every symbol include/bhist.h declares (checked by tests/test_abi.py)
 EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset", "bh_fill", "bh_fill_host",
@@ -226,16 +227,20 @@ class Program:
 
 def fill_expr(hist, cols, prog: "Program", axis_regs, weight_reg: int = -1, filter_reg: int = -1, stream=None):
     """Filter + Define + fill in one kernel: cols are contiguous float64 CUDA tensors."""
+    import torch
     n = cols[0].numel() if cols else 0
+    _check_cols(cols, (torch.float64,), n, hist.device, "cols")
     bh_fill_expr(hist.h, n, [c.data_ptr() for c in cols], prog.ops, axis_regs, weight_reg, filter_reg,
-                 _stream_handle(stream))
+                 _stream_handle(stream, hist.device))
 
 
 def fill_multi(hists, col_of_axis, weighted, cols, w=None, stream=None) -> None:
     """Histogram-level wrapper: cols are contiguous float64 CUDA tensors of equal length."""
+    import torch
     n = cols[0].numel()
+    _check_cols(cols + ([w] if w is not None else []), (torch.float64,), n, hists[0].device, "cols / w")
     bh_fill_multi([h.h for h in hists], col_of_axis, weighted, n, [c.data_ptr() for c in cols],
-                  None if w is None else w.data_ptr(), _stream_handle(stream))
+                  None if w is None else w.data_ptr(), _stream_handle(stream, hists[0].device))
 
 
 def bh_find_bins(h, n: int, coord_ptrs, out_ptr, stream=None) -> None:
@@ -298,11 +303,35 @@ def bh_launch_count(h) -> int:
 
 
 # ---------------------------------------------------------------- torch convenience
-def _stream_handle(stream):
+def _stream_handle(stream, device=None):
+    """None -> the current torch stream of `device` (the histogram's device, not the
+    caller's current device); torch.cuda.Stream or a raw cudaStream_t int otherwise."""
     import torch
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _check_cols(cols, dtypes, n, device, what):
+    """Every column: a contiguous CUDA tensor of an allowed dtype, `n` elements, on `device`."""
+    for c in cols:
+        if not (c.is_cuda and c.dtype in dtypes and c.is_contiguous() and c.numel() == n):
+            raise ValueError(f"{what} must be contiguous CUDA tensors of dtype {dtypes} and length {n}")
+        if c.device.index != device:
+            raise ValueError(f"{what} live on cuda:{c.device.index}, the histogram on cuda:{device}")
+
+
+def _host_col(a, n, what):
+    """A host float64 column for bh_fill_host: contiguous, `n` elements, not on a GPU."""
+    import torch
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda or a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != n:
+            raise ValueError(f"{what} must be a contiguous float64 host tensor of length {n}")
+        return a.data_ptr()
+    a_np = a
+    if not (isinstance(a_np, np.ndarray) and a_np.dtype == np.float64 and a_np.flags.c_contiguous and a_np.size == n):
+        raise ValueError(f"{what} must be a contiguous float64 numpy array of length {n}")
+    return a_np.ctypes.data
 
 
 class Histogram:
@@ -326,61 +355,59 @@ class Histogram:
         except Exception:
             pass
 
+    def _s(self, stream):
+        return _stream_handle(stream, self.device)
+
+    def _coords(self, coords):
+        if len(coords) != self.dim:
+            raise ValueError(f"need {self.dim} coordinate columns, got {len(coords)}")
+        return coords[0].numel()
+
     def reset(self, stream=None):
-        bh_reset(self.h, _stream_handle(stream))
+        bh_reset(self.h, self._s(stream))
         return self
 
     def fill(self, coords, w=None, stream=None):
         """coords: list of `dim` contiguous float64 CUDA tensors; w: float64 CUDA tensor or None."""
         import torch
-        assert len(coords) == self.dim
-        n = coords[0].numel()
-        for c in coords:
-            if not (c.is_cuda and c.dtype == torch.float64 and c.is_contiguous() and c.numel() == n):
-                raise ValueError("coords must be contiguous float64 CUDA tensors of equal length")
-        if w is not None and not (w.is_cuda and w.dtype == torch.float64 and w.is_contiguous() and w.numel() == n):
-            raise ValueError("w must be a contiguous float64 CUDA tensor of the same length")
-        bh_fill(self.h, n, [c.data_ptr() for c in coords], None if w is None else w.data_ptr(),
-                _stream_handle(stream))
+        n = self._coords(coords)
+        _check_cols(coords + ([w] if w is not None else []), (torch.float64,), n, self.device, "coords / w")
+        bh_fill(self.h, n, [c.data_ptr() for c in coords], None if w is None else w.data_ptr(), self._s(stream))
         return self
 
     def fill_f32(self, coords, w=None, stream=None):
         """float32 CUDA tensors (widened exactly to float64 inside the kernel)."""
         import torch
-        n = coords[0].numel()
-        for c in coords + ([w] if w is not None else []):
-            if not (c.is_cuda and c.dtype == torch.float32 and c.is_contiguous() and c.numel() == n):
-                raise ValueError("columns must be contiguous float32 CUDA tensors of equal length")
-        bh_fill_f32(self.h, n, [c.data_ptr() for c in coords], None if w is None else w.data_ptr(),
-                    _stream_handle(stream))
+        n = self._coords(coords)
+        _check_cols(coords + ([w] if w is not None else []), (torch.float32,), n, self.device, "coords / w")
+        bh_fill_f32(self.h, n, [c.data_ptr() for c in coords], None if w is None else w.data_ptr(), self._s(stream))
         return self
 
     def fill_i32(self, coords, w=None, stream=None):
         """int32 coordinate CUDA tensors, optional float32 weights (coordinates widened exactly)."""
         import torch
-        n = coords[0].numel()
-        for c in coords:
-            if not (c.is_cuda and c.dtype == torch.int32 and c.is_contiguous() and c.numel() == n):
-                raise ValueError("coords must be contiguous int32 CUDA tensors of equal length")
-        if w is not None and not (w.is_cuda and w.dtype == torch.float32 and w.is_contiguous() and w.numel() == n):
-            raise ValueError("w must be a contiguous float32 CUDA tensor of the same length")
-        bh_fill_i32(self.h, n, [c.data_ptr() for c in coords], None if w is None else w.data_ptr(),
-                    _stream_handle(stream))
+        n = self._coords(coords)
+        _check_cols(coords, (torch.int32,), n, self.device, "coords")
+        if w is not None:
+            _check_cols([w], (torch.float32,), n, self.device, "w")
+        bh_fill_i32(self.h, n, [c.data_ptr() for c in coords], None if w is None else w.data_ptr(), self._s(stream))
         return self
 
     def fill_host(self, coords, w=None, stream=None):
-        """coords / w: host (preferably pinned) float64 torch tensors or numpy arrays."""
-        def ptr(a):
-            return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+        """coords / w: host (preferably pinned) contiguous float64 torch tensors or numpy arrays."""
+        if len(coords) != self.dim:
+            raise ValueError(f"need {self.dim} coordinate columns, got {len(coords)}")
         n = len(coords[0])
-        bh_fill_host(self.h, n, [ptr(c) for c in coords], None if w is None else ptr(w), _stream_handle(stream))
+        ptrs = [_host_col(c, n, "coords") for c in coords]
+        bh_fill_host(self.h, n, ptrs, None if w is None else _host_col(w, n, "w"), self._s(stream))
         return self
 
     def find_bins(self, coords, stream=None):
         import torch
-        n = coords[0].numel()
+        n = self._coords(coords)
+        _check_cols(coords, (torch.float64,), n, self.device, "coords")
         out = torch.empty(n, dtype=torch.int32, device=coords[0].device)
-        bh_find_bins(self.h, n, [c.data_ptr() for c in coords], out.data_ptr(), _stream_handle(stream))
+        bh_find_bins(self.h, n, [c.data_ptr() for c in coords], out.data_ptr(), self._s(stream))
         return out
 
     def pack(self, out=None, stream=None):
@@ -388,15 +415,18 @@ class Histogram:
         n = bh_packed_size(self.h)
         if out is None:
             out = torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
-        bh_pack(self.h, out.data_ptr(), _stream_handle(stream))
+        _check_cols([out], (torch.float64,), n, self.device, "out")
+        bh_pack(self.h, out.data_ptr(), self._s(stream))
         return out
 
     def unpack(self, buf, stream=None):
-        bh_unpack(self.h, buf.data_ptr(), _stream_handle(stream))
+        import torch
+        _check_cols([buf], (torch.float64,), bh_packed_size(self.h), self.device, "buf")
+        bh_unpack(self.h, buf.data_ptr(), self._s(stream))
         return self
 
     def read(self, stream=None) -> dict:
-        return bh_read(self.h, _stream_handle(stream))
+        return bh_read(self.h, self._s(stream))
 
     def strategy(self, weighted: bool) -> int:
         return bh_get_strategy(self.h, weighted)

@@ -102,6 +102,8 @@ struct bh_hist {
     double *stage[kStageSlots] = {};  // each slot: (dim+1) columns of `chunk` doubles
     int64_t stage_chunk = 0;
     cudaEvent_t copied[kStageSlots] = {}, consumed[kStageSlots] = {};
+    bool slot_used[kStageSlots] = {};  // consumed[slot] recorded at least once (persists across calls)
+    int next_slot = 0;                 // ring position (persists across calls)
 };
 
 namespace {
@@ -123,8 +125,11 @@ int resolve_strategy(const bh_hist *h, bool weighted) {
     // EXACT only changes weighted fills of bh_fill / bh_fill_host (fill_exact below)
     if (h->strategy == BH_STRATEGY_SORT)     // weighted partitions are 4x smaller
         return sort_partitions(h, weighted) <= kPartMaxP ? BH_STRATEGY_SORT : BH_STRATEGY_CACHE;
-    if (h->strategy != BH_STRATEGY_AUTO && h->strategy != BH_STRATEGY_EXACT) return h->strategy;
     const size_t priv = (weighted ? 16 : 4) * (size_t)h->G;
+    // forced PRIV is accepted when the unit-weight bins fit (bh_set_strategy); weighted
+    // cells are 4x larger, so a weighted fill that cannot hold them uses CACHE instead
+    if (h->strategy == BH_STRATEGY_PRIV && priv + kStaticSmemReserve > h->smem_optin) return BH_STRATEGY_CACHE;
+    if (h->strategy != BH_STRATEGY_AUTO && h->strategy != BH_STRATEGY_EXACT) return h->strategy;
     if (priv + kStaticSmemReserve <= h->smem_optin) return BH_STRATEGY_PRIV;
     // large bin spaces: shared-memory cache of the hottest bins in front of L2 atomics
     // (as fast as plain GLOBAL on uniform data, 30x faster on the peaked C4 shape).
@@ -157,6 +162,7 @@ size_t sink_bytes(const bh_hist *h, int strategy, bool weighted) {
 // Bytes of shared memory the variable-axis tables take (float32 edges + guide).
 size_t axis_table_bytes(const AxisP &a) {
     if (!a.var) return 0;
+    if (a.g16 == 3) return align16(4 * (size_t)(a.gcells + 1));
     return align16(4 * (size_t)(a.n + 1)) + align16((a.g16 ? 2 : 4) * (size_t)(a.gcells + 1));
 }
 
@@ -217,6 +223,11 @@ bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n) {
     }
     c.vsm = tabs > 0 && sink + tabs + kStaticSmemReserve <= h->smem_optin;
     c.vm = tabs == 0 ? 0 : (c.vsm ? 1 : 2);
+    if (c.vm == 1) {                     // every variable axis compact: the specialized search
+        bool all3 = true;
+        for (int a = 0; a < h->dim; ++a) all3 &= !h->ax[a].var || h->ax[a].g16 == 3;
+        if (all3) c.vm = 3;
+    }
     // PRIV: replicate the private bins into the spare shared memory (up to one copy
     // per warp) so hot bins are not contended across warps
     pl.replicas = 1;
@@ -649,6 +660,27 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
             int gc = 1;
             while (2 * gc < A.nbins && gc < (1 << 22)) gc <<= 1;
             while (gc < 64 * A.nbins && 4 * (size_t)(A.nbins + 1) + 2 * (size_t)(2 * gc + 1) <= 56 * 1024) gc <<= 1;
+            // compact mode (g16 == 3): one 32-bit word per cell, no float32 edges, as many cells
+            // as fit in 56 KB (<= 64 per bin); taken when <= 2% of the interior edges share a
+            // cell with two others (those cells search the float64 edges), e.g. C2's 10,000
+            // near-uniform bins: 8192 cells, 0.3% of the edges
+            int gc3 = 1;
+            while (2 * gc3 <= 64 * A.nbins && 4 * (size_t)(2 * gc3 + 1) <= 56 * 1024) gc3 <<= 1;
+            bool compact = (A.nbins - 1) < 16384 && 2 * gc3 >= A.nbins && !getenv("BHIST_NO_COMPACT");
+            if (compact) {
+                const double sc = (double)gc3 / (A.edges[A.nbins] - A.edges[0]);
+                std::vector<int> cnt(gc3, 0);
+                std::vector<int> cell(A.nbins + 1, 0);
+                for (int i = 1; i < A.nbins; ++i) {
+                    const double t = (A.edges[i] - A.edges[0]) * sc;
+                    cell[i] = std::min((int)t, gc3 - 1);
+                    ++cnt[cell[i]];
+                }
+                int crowded = 0;
+                for (int i = 1; i < A.nbins; ++i) crowded += cnt[cell[i]] >= 3;
+                compact = crowded <= 0.02 * std::max(1, A.nbins - 1);
+            }
+            if (compact) gc = gc3;
             P.gcells = gc;
             P.gscale = (double)gc / (P.xmax - P.xmin);
             if (!std::isfinite(P.gscale) || !(P.gscale > 0)) return cleanup(fail(BH_EINVAL, "axis %d: edge range too small", a));
@@ -666,7 +698,7 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
             P.e = de;
             P.guide = dg2;
             P.e32 = de32;
-            P.g16 = (A.nbins - 1) < 16384 ? 2 : ((A.nbins - 1) < 65536 ? 1 : 0);
+            P.g16 = compact ? 3 : (A.nbins - 1) < 16384 ? 2 : ((A.nbins - 1) < 65536 ? 1 : 0);
             k_build_guide<<<(gc + 1 + 255) / 256, 256>>>(P, dg2);
             k_edges_f32<<<(A.nbins + 1 + 255) / 256, 256>>>(de, A.nbins + 1, de32);
             unsigned char *img = nullptr;
@@ -795,17 +827,20 @@ bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const
             }
             if (!h->copied[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->copied[i], cudaEventDisableTiming));
             if (!h->consumed[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->consumed[i], cudaEventDisableTiming));
+            h->slot_used[i] = false;       // fresh buffer: nothing reads it yet
         }
         h->stage_chunk = h->chunk;
     }
     const int64_t C = h->stage_chunk;
-    int k = 0;
-    for (int64_t off = 0; off < n; off += C, ++k) {
-        const int slot = k % kStageSlots;
+    for (int64_t off = 0; off < n; off += C) {
+        const int slot = h->next_slot;
+        h->next_slot = (slot + 1) % kStageSlots;
         const int64_t m = std::min(C, n - off);
         double *buf = h->stage[slot];
-        // the slot may be overwritten only after the fill that read it has run
-        if (k >= kStageSlots) CUDA_TRY(cudaStreamWaitEvent(h->copy_stream, h->consumed[slot], 0));
+        // the slot may be overwritten only after the fill that read it has run:
+        // that fill may belong to an earlier bh_fill_host call whose kernels are still queued
+        // on a stream (this function returns once the HOST bytes are consumed, not the slots)
+        if (h->slot_used[slot]) CUDA_TRY(cudaStreamWaitEvent(h->copy_stream, h->consumed[slot], 0));
         const double *dcols[kMaxDim] = {};
         for (int a = 0; a < h->dim; ++a) {
             CUDA_TRY(cudaMemcpyAsync(buf + a * C, coords[a] + off, sizeof(double) * m, cudaMemcpyHostToDevice, h->copy_stream));
@@ -821,6 +856,7 @@ bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const
         bh_status r = fill_device(h, m, dcols, dw, st);
         if (r != BH_OK) return r;
         CUDA_TRY(cudaEventRecord(h->consumed[slot], st));
+        h->slot_used[slot] = true;
     }
     // every host byte has been read once the last copy has completed
     CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
@@ -1045,14 +1081,36 @@ bh_status bh_find_bins(const bh_hist *h, int64_t n, const double *const *coords,
         if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
     DeviceGuard dg(h->device);
     FillP p = make_params(h, n, coords, nullptr);
-    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)h->nsm * 16);
-    cudaStream_t st = static_cast<cudaStream_t>(s);
-    switch (h->dim) {
-    case 1: k_find_bins<1><<<grid, 256, 0, st>>>(p, out); break;
-    case 2: k_find_bins<2><<<grid, 256, 0, st>>>(p, out); break;
-    default: k_find_bins<3><<<grid, 256, 0, st>>>(p, out); break;
+    // the variable-axis search the fills use: tables in shared memory when they fit
+    // (BH_DEBUG_FIND_BINS_GLOBAL forces the float64 global-memory search instead)
+    size_t tabs = 0;
+    bool all3 = true;
+    for (int a = 0; a < h->dim; ++a) {
+        if (!h->ax[a].var) continue;
+        p.ax[a].tab_off = (int32_t)tabs;
+        tabs += axis_table_bytes(h->ax[a]);
+        all3 &= h->ax[a].g16 == 3;
     }
-    CUDA_TRY(cudaGetLastError());
+    int vm = tabs == 0 ? 0 : (tabs + kStaticSmemReserve <= h->smem_optin ? (all3 ? 3 : 1) : 2);
+    if (vm && (h->debug & BH_DEBUG_FIND_BINS_GLOBAL)) vm = 2;
+    const size_t smem = (vm == 1 || vm == 3) ? tabs : 0;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)h->nsm * (smem ? 2 : 16));
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    auto launch = [&](auto kern) -> cudaError_t {
+        if (cudaError_t e = ensure_smem(reinterpret_cast<const void *>(kern), smem)) return e;
+        kern<<<grid, 256, smem, st>>>(p, out);
+        return cudaGetLastError();
+    };
+    cudaError_t e;
+#define BH_FB(D) (vm == 0 ? launch(k_find_bins<D, 0>) : vm == 1 ? launch(k_find_bins<D, 1>) \
+                  : vm == 3 ? launch(k_find_bins<D, 3>) : launch(k_find_bins<D, 2>))
+    switch (h->dim) {
+    case 1: e = BH_FB(1); break;
+    case 2: e = BH_FB(2); break;
+    default: e = BH_FB(3); break;
+    }
+#undef BH_FB
+    if (e != cudaSuccess) return fail(BH_ECUDA, "find_bins launch: %s", cudaGetErrorString(e));
     const_cast<bh_hist *>(h)->launches++;
     return BH_OK;
 }

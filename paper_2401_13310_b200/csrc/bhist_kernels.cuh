@@ -46,8 +46,10 @@ struct AxisP {
     const float *e32;        // variable: RN-to-float32 copy of the edges (device), staged in smem
     int32_t tab_off;         // variable + VSM: byte offset of [e32 | guide] in dynamic smem
     int32_t g16;             // variable + VSM: guide staged as uint32 (0), uint16 (1, n-1 < 65536) or
-                             // packed uint16 (2, n-1 < 16384): guide[c] << 2 | min(guide[c+1]-guide[c], 3)
-    const uint4 *tab_img;    // variable: the shared-memory image [e32 | guide in mode g16], built at create
+                             // packed uint16 (2, n-1 < 16384): guide[c] << 2 | min(guide[c+1]-guide[c], 3);
+                             // 3: compact table, no float32 edges (see find_bin_var_compact)
+    const uint4 *tab_img;    // variable: the shared-memory image [e32 | guide in mode g16] (mode 3: the
+                             // compact table alone), built at create
     int32_t tab_bytes;       // its size (multiple of 16)
 };
 
@@ -162,19 +164,67 @@ __device__ __forceinline__ int find_bin_var_smem(const AxisP &a, double x, const
     return 1 + lo;
 }
 
+// Compact mode (g16 == 3, n-1 < 16384): one 32-bit shared-memory word per guide cell and
+// no float32 edge array.  With t = RN(RN(x-e0)*gscale) (guide_cell's monotone t) and
+// Q(x) = floor(256 t) (exact scaling), the cell is c = Q >> 8 and the quantized position
+// inside it q = Q & 255 (clamped to the last cell as guide_cell clamps, with q = 255 there).
+// Word c = lo | min(cnt,3) << 14 | q(e_{lo+1}) << 16 | q(e_{lo+2}) << 24, where lo = guide[c]
+// and cnt = guide[c+1] - guide[c] interior edges lie in cell c.  (c, q) is monotone in x, so
+// q(x) > q(e_i) implies x > e_i and q(x) < q(e_i) implies x < e_i; only an equal q (a tie,
+// ~cnt/256 of the events) or a cell of >= 3 edges reads the float64 edges (global, L1/L2
+// resident).  One LDS.32 per event instead of the guide load plus the float32 edge search.
+__device__ __forceinline__ int compact_cell(const AxisP &a, double x, int &q) {
+    const double t = __dmul_rn(__dsub_rn(x, a.xmin), a.gscale);
+    const int qf = (int)__dmul_rn(t, 256.0);         // floor(256 t); t >= 0 and < ~gcells
+    int c = qf >> 8;
+    q = qf & 255;
+    if (c > a.gcells - 1) { c = a.gcells - 1; q = 255; }
+    return c;
+}
+
+static __device__ __noinline__ int compact_slow(const AxisP &a, double x, const uint32_t *tab, int c, int lo, int cnt) {
+    // count the cell's interior edges e[lo+1 .. hi] <= x exactly (ties / >= 3 edges)
+    int hi = cnt < 3 ? lo + cnt : (int)(tab[c + 1] & 0x3fffu);
+    int l = lo;                                      // largest l in [lo, hi] with l == lo or e[l] <= x
+    while (l < hi) {
+        const int m = (l + hi + 1) >> 1;
+        if (__ldg(a.e + m) <= x) l = m; else hi = m - 1;
+    }
+    return 1 + l;
+}
+
+template <bool CHECK_RANGE = true>
+__device__ __forceinline__ int find_bin_var_compact(const AxisP &a, double x, const unsigned char *tabc) {
+    if (x < a.xmin) return 0;
+    if (!(x < a.xmax)) return a.n + 1;
+    const uint32_t *tab = reinterpret_cast<const uint32_t *>(tabc);
+    int q;
+    const int c = compact_cell(a, x, q);
+    const uint32_t v = tab[c];
+    const int lo = (int)(v & 0x3fffu), cnt = (int)((v >> 14) & 3u);
+    const int p1 = (int)((v >> 16) & 255u), p2 = (int)(v >> 24);
+    const bool tie = (cnt >= 1 && q == p1) || (cnt >= 2 && q == p2);
+    if (tie || cnt == 3) return compact_slow(a, x, tab, c, lo, cnt);
+    return 1 + lo + (int)(cnt >= 1 && q > p1) + (int)(cnt >= 2 && q > p2);
+}
+
 __device__ __forceinline__ int find_bin_var_smem_any(const AxisP &a, double x, const unsigned char *tab) {
+    if (a.g16 == 3) return find_bin_var_compact(a, x, tab);
     return a.g16 == 2 ? find_bin_var_smem<2>(a, x, tab)
                       : (a.g16 ? find_bin_var_smem<1>(a, x, tab) : find_bin_var_smem<0>(a, x, tab));
 }
 
 // VM (variable-axis mode, a template constant): 0 = every axis fixed (no variable-axis
-// code at all), 1 = variable-axis tables staged in shared memory, 2 = tables in global.
-template <int VM>
+// code at all), 1 = variable-axis tables staged in shared memory, 2 = tables in global,
+// 3 = tables in shared memory and every variable axis in the compact mode (g16 == 3).
+// VAR1: the axis is known to be variable (1-D histograms with VM != 0).
+template <int VM, bool VAR1 = false>
 __device__ __forceinline__ int find_bin(const AxisP &a, double x, const unsigned char *smem) {
 #ifdef BH_EXP_NOSEARCH   // experiment only (wrong results): bin from the guide cell alone
     if (a.var) return x < a.xmin ? 0 : (!(x < a.xmax) ? a.n + 1 : 1 + (int)((long long)guide_cell(a, x) * a.n / a.gcells));
 #endif
-    if (VM == 0 || !a.var) return find_bin_fixed(a, x);
+    if (VM == 0 || (!VAR1 && !a.var)) return find_bin_fixed(a, x);
+    if (VM == 3) return find_bin_var_compact(a, x, smem + a.tab_off);
     if (VM == 1) {
         return find_bin_var_smem_any(a, x, smem + a.tab_off);
     }
@@ -284,11 +334,11 @@ __device__ __forceinline__ void block_stats_finish(const FillP &p, double (&s)[K
     __threadfence();
     // warp k sums statistic k over the blocks: lane-strided loads in flight together, then
     // a fixed butterfly (deterministic for a given grid); small fills are latency-bound
-    if (warp < K) {
+    for (int k = warp; k < K; k += (int)(blockDim.x >> 5)) {   // any blockDim >= 32
         double t = 0.0;
-        for (unsigned b = lane; b < gridDim.x; b += 32) t += __ldcg(p.partials + (size_t)b * K + warp);
+        for (unsigned b = lane; b < gridDim.x; b += 32) t += __ldcg(p.partials + (size_t)b * K + k);
         t = warp_sum_fixed(t);
-        if (lane == 0) p.stats[warp] += t;
+        if (lane == 0) p.stats[k] += t;
     }
     if (threadIdx.x == 0) {
         *p.entries += (unsigned long long)p.entries_add;
@@ -689,7 +739,7 @@ __device__ __forceinline__ void do_event(const FillP &p, const double (&x)[DIM],
     bool inr = true;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
-        const int b = find_bin<VM>(p.ax[a], x[a], smem);   // step (1), per axis
+        const int b = find_bin<VM, DIM == 1 && VM != 0>(p.ax[a], x[a], smem);   // step (1), per axis
         inr &= (b >= 1) & (b <= p.ax[a].n);
         g += b * mul;
         if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
@@ -730,8 +780,8 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
     else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas, p.wc_off);
     else sink.init(smem, p.G);
-    if constexpr (VM == 1) stage_axes<DIM>(p.ax, smem);
-    if constexpr (SINK != SINK_GLOBAL || VM == 1) __syncthreads();
+    if constexpr (VM == 1 || VM == 3) stage_axes<DIM>(p.ax, smem);
+    if constexpr (SINK != SINK_GLOBAL || VM == 1 || VM == 3) __syncthreads();
 
     Acc<DIM, W> acc;
     acc.zero();
@@ -1355,6 +1405,18 @@ __global__ void k_edges_f32(const double *e, int n, float *e32) {
 // mode a.g16]; the packed mode stores guide[c] << 2 | min(guide[c+1] - guide[c], 3).
 __global__ void k_table_image(AxisP a, const uint32_t *guide, unsigned char *img) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a.g16 == 3) {                    // compact: one word per cell, no float32 edges
+        if (i <= a.gcells) {
+            const uint32_t lo = guide[i];
+            const uint32_t cnt = i < a.gcells ? guide[i + 1] - lo : 0u;
+            uint32_t v = lo | (cnt < 3u ? cnt : 3u) << 14;
+            int q;
+            if (cnt >= 1) { compact_cell(a, a.e[lo + 1], q); v |= (uint32_t)q << 16; }
+            if (cnt >= 2) { compact_cell(a, a.e[lo + 2], q); v |= (uint32_t)q << 24; }
+            reinterpret_cast<uint32_t *>(img)[i] = v;
+        }
+        return;
+    }
     float *e32 = reinterpret_cast<float *>(img);
     if (i <= a.n) e32[i] = __double2float_rn(a.e[i]);
     unsigned char *gt = img + ((4 * (a.n + 1) + 15) & ~15);
@@ -1373,13 +1435,21 @@ __global__ void k_table_image(AxisP a, const uint32_t *guide, unsigned char *img
 
 #endif  // BH_FILL_TU
 
-template <int DIM>
+// Per-event global bins through the same FindBin code the fills run: VM 1 / 3 stage the
+// variable-axis tables in shared memory exactly as k_fill does (float32-edge or compact
+// search), VM 2 searches the float64 edges in global memory, VM 0 has fixed axes only.
+template <int DIM, int VM>
 __global__ void k_find_bins(FillP p, int32_t *out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if constexpr (VM == 1 || VM == 3) {
+        stage_axes<DIM>(p.ax, smem);
+        __syncthreads();
+    }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
         int g = 0, mul = 1;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
-            g += find_bin(p.ax[a], p.x[a][i]) * mul;
+            g += find_bin<VM, DIM == 1 && VM != 0>(p.ax[a], p.x[a][i], smem) * mul;
             if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
         }
         out[i] = g;

@@ -38,7 +38,8 @@ inline cudaError_t ensure_smem(const void *kern, size_t bytes) {
 struct LaunchCfg {
     int strategy;
     bool weighted, vec, vsm;
-    int vm;                      // 0 fixed axes only, 1 variable tables in smem, 2 in global
+    int vm;                      // 0 fixed axes only, 1 variable tables in smem, 2 in global, 3 smem + all
+                                 // variable axes compact (k_fill only; the other kernels take 1)
     int grid;
     size_t smem;
 };
@@ -53,8 +54,12 @@ cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
 
 template <int DIM, bool W, int SINK, bool VEC>
 cudaError_t launch_m(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
-    return c.vm == 0 ? launch_t<DIM, W, SINK, VEC, 0>(p, c, s)
-                     : c.vm == 1 ? launch_t<DIM, W, SINK, VEC, 1>(p, c, s) : launch_t<DIM, W, SINK, VEC, 2>(p, c, s);
+    switch (c.vm) {
+    case 0: return launch_t<DIM, W, SINK, VEC, 0>(p, c, s);
+    case 1: return launch_t<DIM, W, SINK, VEC, 1>(p, c, s);
+    case 3: return launch_t<DIM, W, SINK, VEC, 3>(p, c, s);
+    default: return launch_t<DIM, W, SINK, VEC, 2>(p, c, s);
+    }
 }
 
 template <int DIM, bool W, int SINK>
@@ -100,7 +105,7 @@ cudaError_t launch_part1_v(const FillP &p, const PartP &q, int vm, int rc, int g
 template <int DIM, bool W, int SINK, typename CT>
 cudaError_t launch_f32_s(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
     auto kern = c.vm == 0 ? k_fill_f32<DIM, W, SINK, 0, CT>
-                          : c.vm == 1 ? k_fill_f32<DIM, W, SINK, 1, CT> : k_fill_f32<DIM, W, SINK, 2, CT>;
+                          : (c.vm == 1 || c.vm == 3) ? k_fill_f32<DIM, W, SINK, 1, CT> : k_fill_f32<DIM, W, SINK, 2, CT>;
     if (cudaError_t r = ensure_smem(reinterpret_cast<const void *>(kern), c.smem)) return r;
     kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
     return cudaGetLastError();
@@ -122,7 +127,8 @@ cudaError_t launch_f32_w(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
 
 template <int DIM, bool W, int SINK>
 cudaError_t launch_expr_s(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s) {
-    auto kern = c.vm == 0 ? k_fill_expr<DIM, W, SINK, 0> : c.vm == 1 ? k_fill_expr<DIM, W, SINK, 1> : k_fill_expr<DIM, W, SINK, 2>;
+    auto kern = c.vm == 0 ? k_fill_expr<DIM, W, SINK, 0>
+                          : (c.vm == 1 || c.vm == 3) ? k_fill_expr<DIM, W, SINK, 1> : k_fill_expr<DIM, W, SINK, 2>;
     if (cudaError_t r = ensure_smem(reinterpret_cast<const void *>(kern), c.smem)) return r;
     kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p, e);
     return cudaGetLastError();

@@ -1,0 +1,241 @@
+"""GPU parity, round 2: per-event FindBin through every variable-axis search path, every
+Filter+Define opcode, C5 at bench size, back-to-back host fills, and wrapper argument checks.
+Bin indices bit-exact; weighted sums within 1e-12 of sum|term| (BASELINE.json north star)."""
+import os
+
+import numpy as np
+import pytest
+
+import bhgen
+import oracle
+import paper_2401_13310_b200 as pkg
+from _helpers import compare, gen_columns, oracle_parallel
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _near(vals, k=3):
+    """vals and +-1..k ulps around each."""
+    out = [vals]
+    up = dn = vals
+    for _ in range(k):
+        up, dn = np.nextafter(up, np.inf), np.nextafter(dn, -np.inf)
+        out += [up, dn]
+    return np.concatenate(out)
+
+
+def _axes_under_test():
+    wl = bhgen.workload("C2", 1000)
+    c5 = bhgen.workload("C5", 1000)
+    rng = np.random.default_rng(77)
+    return {
+        "C2 edges": wl.hists[0].axes[0].edges,                     # compact mode (8192 cells)
+        "C5 H3 log": c5.hists[3].axes[0].edges,                     # crowded cells: packed guide
+        "random 3000": np.cumsum(rng.uniform(1e-3, 1.0, 3001) ** 3) - 2.0,
+        "uniform 16383": np.linspace(-1.0, 3.0, 16384),            # largest compact n
+        "uniform 20000": np.linspace(0.0, 1.0, 20001),             # too many bins for compact
+        "two bins": np.array([0.0, 0.25, 1.0]),
+    }
+
+
+def _coords_for(edges, rng, m=200_000):
+    lo, hi = edges[0], edges[-1]
+    # random, every edge +-3 ulps, the guide-cell and quantized sub-cell (1/256) boundaries
+    # +-2 ulps (where the compact search switches decisions), flow and special values
+    sub = lo + (hi - lo) * (np.arange(0, 2 ** 15 * 256 + 1, 97) / (2 ** 15 * 256))
+    xs = [rng.uniform(lo - 0.05 * (hi - lo), hi + 0.05 * (hi - lo), m), _near(edges), _near(sub, 2),
+          np.array([np.nan, np.inf, -np.inf, -0.0, 0.0, 1e308, -1e308])]
+    return np.concatenate(xs)
+
+
+@pytest.mark.parametrize("compact", [True, False])
+@pytest.mark.parametrize("search", ["staged", "global"])
+def test_find_bins_every_search_path(compact, search, monkeypatch):
+    """The per-event bin of the fills' own search (tables staged in shared memory: compact
+    32-bit cells or float32 edges + guide) and of the float64 global search equals the
+    oracle's binary search (reading R1) on random, edge, sub-cell-boundary and NaN/inf inputs."""
+    if not compact:
+        monkeypatch.setenv("BHIST_NO_COMPACT", "1")
+    rng = np.random.default_rng(5 + compact)
+    for name, edges in _axes_under_test().items():
+        x = _coords_for(edges, rng)
+        ref = oracle.OracleHist([edges]).find_bins([x])
+        h = pkg.Histogram([edges])
+        if search == "global":
+            pkg.bh_set_debug(h.h, pkg.BH_DEBUG_FIND_BINS_GLOBAL)
+        got = h.find_bins([_t(x)]).cpu().numpy()
+        # the same events through a weighted fill (bins must match the per-event answer)
+        w = rng.uniform(0.5, 1.5, len(x))
+        h.fill([_t(x)], _t(w))
+        compare(h.read(), oracle.OracleHist([edges]).fill([x], w).read(), True, name)
+        h.close()
+        bad = np.flatnonzero(got != ref)
+        assert bad.size == 0, (name, compact, search, x[bad[:5]], got[bad[:5]], ref[bad[:5]])
+
+
+def test_find_bins_mixed_axes_2d_3d():
+    """2-D/3-D histograms mixing fixed and compact/packed variable axes (runtime per-axis
+    dispatch in the staged search)."""
+    rng = np.random.default_rng(9)
+    ax = _axes_under_test()
+    for axes in ([ax["C2 edges"], (100, 0.0, 1.0)], [(7, -1.0, 2.0), ax["C5 H3 log"], ax["two bins"]]):
+        cols = []
+        for a in axes:
+            e = a if isinstance(a, np.ndarray) else np.linspace(a[1], a[2], a[0] + 1)
+            c = _coords_for(e, rng, 100_000)
+            cols.append(c)
+        m = min(len(c) for c in cols)
+        cols = [rng.permutation(c)[:m] for c in cols]
+        ref = oracle.OracleHist(axes).find_bins(cols)
+        h = pkg.Histogram(axes)
+        got = h.find_bins([_t(c) for c in cols]).cpu().numpy()
+        h.close()
+        assert np.array_equal(got, ref), np.flatnonzero(got != ref)[:5]
+
+
+# ------------------------------------------------------------------ Filter + Define: every opcode
+def _expr_inputs(n, rng):
+    a = rng.normal(0, 2, n)
+    b = rng.normal(0.5, 1, n)
+    c = rng.uniform(-3, 3, n)
+    for arr in (a, b):
+        arr[rng.integers(0, n, n // 50)] = np.nan
+        arr[rng.integers(0, n, n // 200)] = np.inf
+        arr[rng.integers(0, n, n // 200)] = -np.inf
+        arr[rng.integers(0, n, n // 100)] = 0.0
+        arr[rng.integers(0, n, n // 100)] = -0.0
+    b[rng.integers(0, n, n // 20)] = a[rng.integers(0, n, n // 20)]        # equal operands for eq/ne/le/ge
+    c[rng.integers(0, n, n // 10)] = 0.0                                  # select/logic on zero
+    return a, b, c
+
+
+@pytest.mark.parametrize("op", list(pkg.OPS))
+def test_fill_expr_every_opcode(op):
+    """Each of the 21 opcodes on the GPU against the numpy oracle (oracle/expr.py), its
+    result used as the coordinate AND (for a second histogram) as the filter, so a wrong
+    value or a wrong truth value both break parity.  Inputs carry NaN, +-inf, +-0."""
+    from oracle import expr
+    rng = np.random.default_rng(abs(hash(op)) % 2 ** 32)
+    n = 300_001
+    a, b, c = _expr_inputs(n, rng)
+    prog = [(op, 3, 0, 1, 2, 1.25)]
+    cols = [_t(a), _t(b), _t(c)]
+    for axes, filt, wreg in (([(64, -6.0, 6.0)], -1, -1), ([(16, -3.0, 3.0)], 3, 2)):
+        coord = 3 if filt < 0 else 2
+        h = pkg.Histogram(axes)
+        pkg.bh_fill_expr(h.h, n, [t.data_ptr() for t in cols], prog, [coord], wreg, filt,
+                         torch.cuda.current_stream().cuda_stream)
+        ref = expr.fill_expr(axes, [a, b, c], prog, [coord], wreg, filt).read()
+        compare(h.read(), ref, wreg >= 0, f"{op} filter={filt}")
+        h.close()
+
+
+def test_fill_expr_long_program_all_registers():
+    """A 32-op program touching all 16 registers (chained selects, divisions, sqrt of
+    negatives) through a weighted 2-D fill."""
+    from oracle import expr
+    rng = np.random.default_rng(3)
+    n = 200_003
+    a, b, c = _expr_inputs(n, rng)
+    names = list(pkg.OPS)
+    prog = []
+    for k in range(32):
+        op = names[k % len(names)]
+        dst = 3 + (k % 13)
+        prog.append((op, dst, (k * 5) % 16, (k * 7 + 1) % 16, (k * 11 + 2) % 16, 0.5 + k))
+    cols = [_t(a), _t(b), _t(c)]
+    axes = [(20, -2.0, 2.0), (10, 0.0, 40.0)]
+    h = pkg.Histogram(axes)
+    pkg.bh_fill_expr(h.h, n, [t.data_ptr() for t in cols], prog, [15, 14], 2, 13,
+                     torch.cuda.current_stream().cuda_stream)
+    ref = expr.fill_expr(axes, [a, b, c], prog, [15, 14], 2, 13).read()
+    compare(h.read(), ref, True, "32 ops")
+    h.close()
+
+
+# ------------------------------------------------------------------ C5 at the bench's size
+@pytest.mark.slow
+def test_c5_bench_size_against_sharded_oracle():
+    """C5 as bench.py runs it at N=1 (1.25e8 device-resident events per GPU at 8 GPUs; the
+    large-fill sinks the planner picks only at this size) against the oracle per histogram."""
+    n = 125_000_000
+    wl = bhgen.workload("C5", n)
+    cols = [_t(wl.column(c, 0, n)) for c in range(len(wl.columns))]
+    w = _t(wl.column(wl.wcol, 0, n))
+    hs = [pkg.Histogram(oracle.oracle_axes(hist)) for hist in wl.hists]
+    pkg.fill_multi(hs, [hist.cols for hist in wl.hists], [hist.weighted for hist in wl.hists], cols, w)
+    got = [h.read() for h in hs]
+    for h in hs:
+        h.close()
+    del cols, w
+    torch.cuda.empty_cache()
+    for i, hist in enumerate(wl.hists):
+        ref = oracle_parallel("C5", n, hidx=i)
+        compare(got[i], ref, hist.weighted, f"C5 H{i}")
+
+
+# ------------------------------------------------------------------ host -> device path
+def test_fill_host_back_to_back_calls_while_stream_busy():
+    """bh_fill_host returns once the HOST bytes are consumed; its fills may
+    still be queued.  A second call made at once must not overwrite a staging slot those
+    queued fills still read: keep the stream busy, fill twice, compare."""
+    rng = np.random.default_rng(12)
+    axes = [(1000, 0.0, 1.0)]
+    n = 1 << 16
+    x1, x2 = rng.uniform(0, 0.5, n), rng.uniform(0.5, 1.0, n)
+    h = pkg.Histogram(axes)
+    pkg.bh_set_chunk(h.h, 1 << 14)                       # 4 chunks per call through 2 slots
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(200_000_000)                   # ~0.1 s of GPU time queued on s
+        h.fill_host([x1], stream=s)
+        h.fill_host([x2], stream=s)
+    s.synchronize()
+    ref = oracle.OracleHist(axes).fill([x1]).fill([x2]).read()
+    compare(h.read(), ref, False, "back-to-back fill_host")
+    h.close()
+
+
+def test_wrapper_rejects_wrong_columns():
+    """dtype / length / contiguity / device checks before any pointer
+    reaches the C ABI."""
+    h = pkg.Histogram([(10, 0.0, 1.0)])
+    with pytest.raises(ValueError):
+        h.fill_host([np.zeros(10, dtype=np.float32)])
+    with pytest.raises(ValueError):
+        h.fill_host([np.zeros(10)], w=np.zeros(9))
+    with pytest.raises(ValueError):
+        h.fill_host([np.zeros(20)[::2]])
+    with pytest.raises(ValueError):
+        h.fill_host([torch.zeros(10, device=DEV)])
+    with pytest.raises(ValueError):
+        h.fill([torch.zeros(10, device=DEV, dtype=torch.float32)])
+    with pytest.raises(ValueError):
+        h.fill([torch.zeros(10, device=DEV)], torch.zeros(9, device=DEV, dtype=torch.float64))
+    with pytest.raises(ValueError):
+        h.fill([torch.zeros(10, dtype=torch.float64)])          # host tensor to a device fill
+    with pytest.raises(ValueError):
+        h.fill([torch.zeros(10, device=DEV, dtype=torch.float64), torch.zeros(10, device=DEV, dtype=torch.float64)])
+    if torch.cuda.device_count() > 1:
+        with pytest.raises(ValueError):
+            h.fill([torch.zeros(10, device="cuda:1", dtype=torch.float64)])
+    h.close()
+
+
+def test_forced_priv_weighted_falls_back_when_cells_do_not_fit():
+    """PRIV is accepted for a bin space whose unit-weight counters fit but
+    whose 16-byte weighted cells do not; weighted fills then take CACHE and stay correct."""
+    axes = [(150, 0.0, 1.0), (150, 0.0, 1.0)]        # 23,104 bins: 92 KB unit, 370 KB weighted
+    h = pkg.Histogram(axes, strategy=pkg.BH_STRATEGY_PRIV)
+    assert h.strategy(False) == pkg.BH_STRATEGY_PRIV and h.strategy(True) == pkg.BH_STRATEGY_CACHE
+    rng = np.random.default_rng(4)
+    x, y, w = rng.uniform(0, 1, 500_000), rng.normal(0.5, 0.2, 500_000), rng.uniform(0.5, 1.5, 500_000)
+    h.fill([_t(x), _t(y)], _t(w))
+    compare(h.read(), oracle.OracleHist(axes).fill([x, y], w).read(), True, "forced PRIV weighted")
+    h.close()

@@ -250,6 +250,21 @@ def measure_secondary(name: str, steps: int, warmup: int, local: int) -> dict:
             ev[i - warmup][1].record(st)
     torch.cuda.synchronize()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    e2e = None
+    if f32:    # end to end through bh_fill_host_f32: pinned host float32 columns, H2D inside
+        hc = [c.cpu().pin_memory() for c in cols]
+        hw = w.cpu().pin_memory() if w is not None else None
+        H.fill_host_f32(hc, hw)
+        H.reset()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        H.fill_host_f32(hc, hw)
+        r = H.read()
+        dt = time.perf_counter() - t0
+        assert r["entries"] == N
+        e2e = {"events_per_s": N / dt, "h2d_bytes_per_event": 4 * (len(hc) + (hw is not None)),
+               "api": "bh_fill_host_f32"}
+        del hc, hw
     peak, _ = hbm_peak()
     bpe = wl.bytes_per_event // (2 if f32 else 1)
     gbs = bpe * N / (ms * 1e-3) / 1e9
@@ -259,7 +274,49 @@ def measure_secondary(name: str, steps: int, warmup: int, local: int) -> dict:
     torch.cuda.empty_cache()
     return {"workload": workload_desc(wl), "events": N, "bytes_per_event": bpe, "events_per_s": N / (ms * 1e-3),
             "fill_ms": ms,
-            "achieved_gbs": gbs, "frac": gbs / peak, "fill_strategy": strat}
+            "achieved_gbs": gbs, "frac": gbs / peak, "fill_strategy": strat, "e2e": e2e}
+
+
+def measure_bulk_regime(local: int, total: int = 1 << 25, bulk: int = 32768) -> dict:
+    """The paper's own benchmark regime: TH1D with 1000 variable bins on
+    [0,1] (random widths), uniform float64 events handed over in bulks of 32768 from host
+    memory, end to end (H2D inside, steady clock, result read back once at the end,
+    PAPER.md:129).  Rows: one bh_fill_host call per bulk from pinned bulk buffers (the
+    RDataFrame pattern), and one call over the whole array with the library's staging
+    chunk swept (32768 ... 2^22 events)."""
+    import torch
+    import paper_2401_13310_b200 as pkg
+    edges = bhgen.edges_random_widths(bhgen.seed_of(6, 15), 1000)
+    host = torch.empty(total, dtype=torch.float64).pin_memory()
+    bhgen.fill_ptr(bhgen.UNIFORM, bhgen.seed_of(6, 0), 0, total, 0.0, 1.0, host.data_ptr())
+    bulks = [host[i:i + bulk] for i in range(0, total, bulk)]
+    H = pkg.Histogram([edges], device=local)
+    out = {"workload": f"TH1D 1000 variable bins, {total} uniform float64 events from pinned host memory, "
+                       f"bulks of {bulk} (PAPER.md:241)", "events": total}
+
+    def run(fn):
+        fn()                                              # warm-up (staging buffers, tables)
+        H.reset()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        r = H.read()
+        dt = time.perf_counter() - t0
+        assert r["entries"] == total
+        return total / dt
+
+    def per_bulk():
+        for b in bulks:
+            H.fill_host([b])
+    pkg.bh_set_chunk(H.h, bulk)
+    out["per_bulk_calls_events_per_s"] = run(per_bulk)
+    sweep = {}
+    for chunk in (bulk, 1 << 18, 1 << 20, 1 << 22):
+        pkg.bh_set_chunk(H.h, chunk)
+        sweep[str(chunk)] = run(lambda: H.fill_host([host]))
+    out["one_call_chunk_sweep_events_per_s"] = sweep
+    H.close()
+    return out
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -268,7 +325,7 @@ def run_gpu(args):
     import torch.distributed as dist
 
     import paper_2401_13310_b200 as pkg
-    from paper_2401_13310_b200.dist import allreduce_state
+    from paper_2401_13310_b200.dist import Exchange
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -310,7 +367,10 @@ def run_gpu(args):
     multi = len(Hs) > 1
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
-    packed = [torch.empty(pkg.bh_packed_size(H.h), dtype=torch.float64, device=dev) for H in Hs]
+    # the exchange step (N>1): ONE collective per step over the packed state of every histogram,
+    # unit-weight histograms without their sum of w^2; reduce-to-root by default (only rank 0
+    # reads the result), --exchange allreduce leaves the total on every rank
+    xchg = Exchange(Hs, unit=[not h.weighted for h in hists], op=args.exchange) if world > 1 else None
     fill_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
 
     def do_fill(cols):
@@ -330,9 +390,8 @@ def run_gpu(args):
         do_fill(devc)
         if i is not None:
             fill_ev[i][1].record(stream)
-        if world > 1:
-            for H, buf in zip(Hs, packed):
-                allreduce_state(H, buf)
+        if xchg is not None:
+            xchg(stream)
 
     for _ in range(args.warmup):
         step()
@@ -354,8 +413,8 @@ def run_gpu(args):
     clk.stop()
     dl = [pkg.bh_launch_count(H.h) - a for H, a in zip(Hs, l0)]
     launches = sum(dl)        # the library counts each kernel launch once (fused passes on their first histogram)
-    if world > 1:
-        launches += len(Hs) * 2 * args.steps     # pack + unpack kernels per histogram per step
+    if world > 1:        # one pack (+ one unpack where the sum lands) per step, counted by the library
+        pass
     ms = t0.elapsed_time(t1)
     fill_ms = [a.elapsed_time(b) for a, b in fill_ev]
     if world > 1:
@@ -378,9 +437,8 @@ def run_gpu(args):
         else:
             h = hists[0]
             Hs[0].fill_host([host[slot[c]] for c in h.cols], host[slot[wl.wcol]] if h.weighted else None)
-        if world > 1:
-            for H, buf in zip(Hs, packed):
-                allreduce_state(H, buf)
+        if xchg is not None:
+            xchg(stream)
         return [H.read() for H in Hs]
 
     e2e_step()   # warm-up (staging buffers, copy stream)
@@ -398,10 +456,14 @@ def run_gpu(args):
         m = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         e2e_s = float(m.item())
-    assert all(r["entries"] == N * world for r in res), [r["entries"] for r in res]
+    if rank == 0 or args.exchange == "allreduce":
+        assert all(r["entries"] == N * world for r in res), [r["entries"] for r in res]
+    if args.dump and rank == 0:          # the reduced states (tests compare them with the oracle)
+        np.savez(args.dump, **{f"{k}{i}": r[k] for i, r in enumerate(res) for k in ("content", "sumw2", "stats")},
+                 **{f"entries{i}": np.array(r["entries"]) for i, r in enumerate(res)})
     e2e_value = N * world * e2e_steps / e2e_s
     h2d = 8 * N * len(used)
-    d2h = 8 * sum(pkg.bh_packed_size(H.h) for H in Hs)
+    d2h = 8 * sum(pkg.bh_packed_size(H.h) for H in Hs)      # bh_read of every histogram
     # PCIe roofline of the e2e leg: plain pinned host -> device copy of one input column
     # (up to 1 GiB), timed with CUDA events on this GPU alone
     nb = min(N, 1 << 27)
@@ -422,7 +484,10 @@ def run_gpu(args):
         del devc
         torch.cuda.empty_cache()
         for name in [x for x in args.secondary.split(",") if x]:
-            secondary[name] = measure_secondary(name, max(3, min(args.steps, 10)), 3, local)
+            if name == "P32K":
+                secondary[name] = measure_bulk_regime(local)
+            else:
+                secondary[name] = measure_secondary(name, max(3, min(args.steps, 10)), 3, local)
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
@@ -456,7 +521,8 @@ def run_gpu(args):
                        "total_bins": sum(H.nbins_total for H in Hs), "histograms": len(Hs),
                        "weighted": any(h.weighted for h in hists), "fill_strategy": strat,
                        "l2": f"inputs {bpe * N / 2**30:.1f} GiB/GPU >> 126 MB L2 (no flush needed)",
-                       "parallelism": f"dp{world}: events sharded, NCCL all-reduce of packed bins+stats"
+                       "parallelism": f"dp{world}: events sharded, one NCCL {args.exchange} per step of the "
+                                      f"packed bins+stats of all histograms ({xchg.nbytes} B)"
                        if world > 1 else "single GPU"},
             "pct_hbm_peak": 100.0 * bpe * value / world / 1e9 / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -496,8 +562,11 @@ def main():
     ap.add_argument("--hist-strategy", default="",
                     help="per-histogram strategies of a multi-histogram config, e.g. '6=sort'")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend for N>1")
+    ap.add_argument("--exchange", default="reduce", choices=["reduce", "allreduce"],
+                    help="N>1: sum the partial states on rank 0 only (reduce) or on every rank")
+    ap.add_argument("--dump", default="", help="rank 0 writes the final (reduced) states to this .npz (tests)")
     ap.add_argument("--events", type=int, default=0, help="override events per GPU (tests)")
-    ap.add_argument("--secondary", default="C1S,C1F,C2F,C3+sort",
+    ap.add_argument("--secondary", default="C1S,C1F,C2F,C3+sort,P32K",
                     help="comma list of extra configs measured device-resident after the headline ('' = none)")
     ap.add_argument("--cpu-sample", type=int, default=50_000_000)
     ap.add_argument("--ref-sample", type=int, default=1 << 23)

@@ -147,6 +147,15 @@ bh_status bh_fill_i32(bh_hist *h, int64_t n, const int32_t *const *coords, const
  * buffers — the fix of PAPER.md:223); kernels may still be in flight on s. */
 bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s);
 
+/* bh_fill_host with float32 coordinate/weight columns (bh_fill_f32 semantics: exact
+ * widening): HOST pointers, 4 B per value, so half the PCIe bytes of bh_fill_host.  Same
+ * staging, overlap and return rule. */
+bh_status bh_fill_host_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, bh_stream s);
+
+/* bh_fill_host with int32 coordinate columns and optional float32 weights (bh_fill_i32
+ * semantics), HOST pointers. */
+bh_status bh_fill_host_i32(bh_hist *h, int64_t n, const int32_t *const *coords, const float *w, bh_stream s);
+
 /* Fused multi-histogram fill (one pass over the columns; PAPER.md:470 future work,
  * BASELINE.json config 5).  hs[nh] (1 <= nh <= 8, distinct, same device);
  * col_of_axis[3*i + a] = index into cols[] of the column feeding axis a of
@@ -222,6 +231,19 @@ bh_status bh_pack(const bh_hist *h, double *dev_out, bh_stream s);
 /* Replace the state with a packed buffer (DEVICE pointer, bh_packed_size doubles, layout of
  * bh_pack), e.g. after the all-reduce of SURVEY.md §8(e).  Async on s; BH_EINVAL on NULL. */
 bh_status bh_unpack(bh_hist *h, const double *dev_in, bh_stream s);
+
+/* The multi-GPU exchange of SURVEY.md §8(e) for several histograms in ONE collective:
+ * hs[nh] (1 <= nh <= 8, same device) are packed one after the other into one DEVICE
+ * buffer of bh_packed_size_multi doubles (caller-owned).  unit (may be NULL): unit[i] != 0
+ * packs histogram i as [content(G) | stats(K) | entries] without its sum of w^2, which for
+ * unit weights equals the content (reading R12), halving the payload; bh_pack_multi
+ * refuses (BH_EINVAL) a unit entry for a histogram that received a weighted fill (or a
+ * full unpack) since its create/reset.  bh_unpack_multi replaces the states from such a
+ * buffer (sum of w^2 := content for unit entries).  Async on s.  The buffer is a sum over
+ * events, so ranks holding disjoint shards reduce it elementwise (SUM). */
+bh_status bh_packed_size_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, int64_t *n_doubles);
+bh_status bh_pack_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, double *dev_out, bh_stream s);
+bh_status bh_unpack_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, const double *dev_in, bh_stream s);
 
 /* Read back to HOST buffers (any may be NULL): contents[G], sumw2[G], stats[K] (ROOT
  * GetStats order, reading R8), entries — "only copy back ... once all bulks have been

@@ -24,6 +24,7 @@ BH_DEBUG_FIND_BINS_GLOBAL = 2
 # every symbol include/bhist.h declares (checked by tests/test_abi.py)
 EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset", "bh_fill", "bh_fill_host",
             "bh_fill_multi", "bh_fill_expr", "bh_fill_f32", "bh_fill_i32", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
+            "bh_fill_host_f32", "bh_fill_host_i32", "bh_packed_size_multi", "bh_pack_multi", "bh_unpack_multi",
             "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_launch_count"]
 
 
@@ -76,6 +77,11 @@ def lib(build_if_stale: bool = False):
             "bh_reset": ([_P, _P], _I32),
             "bh_fill": ([_P, _I64, _P, _P, _P], _I32),
             "bh_fill_host": ([_P, _I64, _P, _P, _P], _I32),
+            "bh_fill_host_f32": ([_P, _I64, _P, _P, _P], _I32),
+            "bh_fill_host_i32": ([_P, _I64, _P, _P, _P], _I32),
+            "bh_packed_size_multi": ([_P, _I32, _P, _P], _I32),
+            "bh_pack_multi": ([_P, _I32, _P, _P, _P], _I32),
+            "bh_unpack_multi": ([_P, _I32, _P, _P, _P], _I32),
             "bh_find_bins": ([_P, _I64, _P, _P, _P], _I32),
             "bh_fill_multi": ([_P, _I32, _P, _P, _I64, _P, _I32, _P, _P], _I32),
             "bh_fill_expr": ([_P, _I64, _P, _I32, _P, _I32, _P, _I32, _I32, _P], _I32),
@@ -162,6 +168,43 @@ def bh_fill_i32(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
 def bh_fill_host(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
     arr = _ptrs(coord_ptrs)
     _check(lib().bh_fill_host(h, n, ctypes.addressof(arr), w_ptr, stream))
+
+
+def bh_fill_host_f32(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
+    arr = _ptrs(coord_ptrs)
+    _check(lib().bh_fill_host_f32(h, n, ctypes.addressof(arr), w_ptr, stream))
+
+
+def bh_fill_host_i32(h, n: int, coord_ptrs, w_ptr=None, stream=None) -> None:
+    arr = _ptrs(coord_ptrs)
+    _check(lib().bh_fill_host_i32(h, n, ctypes.addressof(arr), w_ptr, stream))
+
+
+def _multi_args(handles, unit):
+    nh = len(handles)
+    hs = (ctypes.c_void_p * nh)(*handles)
+    u = None if unit is None else (ctypes.c_uint8 * nh)(*[1 if x else 0 for x in unit])
+    return nh, hs, u
+
+
+def bh_packed_size_multi(handles, unit=None) -> int:
+    nh, hs, u = _multi_args(handles, unit)
+    n = _I64()
+    _check(lib().bh_packed_size_multi(ctypes.addressof(hs), nh, None if u is None else ctypes.addressof(u),
+                                      ctypes.byref(n)))
+    return n.value
+
+
+def bh_pack_multi(handles, unit, dev_out_ptr, stream=None) -> None:
+    nh, hs, u = _multi_args(handles, unit)
+    _check(lib().bh_pack_multi(ctypes.addressof(hs), nh, None if u is None else ctypes.addressof(u), dev_out_ptr,
+                               stream))
+
+
+def bh_unpack_multi(handles, unit, dev_in_ptr, stream=None) -> None:
+    nh, hs, u = _multi_args(handles, unit)
+    _check(lib().bh_unpack_multi(ctypes.addressof(hs), nh, None if u is None else ctypes.addressof(u), dev_in_ptr,
+                                 stream))
 
 
 def bh_fill_multi(handles, col_of_axis, weighted, n: int, col_ptrs, w_ptr=None, stream=None) -> None:
@@ -321,17 +364,17 @@ def _check_cols(cols, dtypes, n, device, what):
             raise ValueError(f"{what} live on cuda:{c.device.index}, the histogram on cuda:{device}")
 
 
-def _host_col(a, n, what):
-    """A host float64 column for bh_fill_host: contiguous, `n` elements, not on a GPU."""
+def _host_col(a, n, what, dtype=np.float64):
+    """A host column for the bh_fill_host* calls: contiguous, `n` elements of `dtype`, not on a GPU."""
     import torch
+    tdt = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32}[dtype]
     if isinstance(a, torch.Tensor):
-        if a.is_cuda or a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != n:
-            raise ValueError(f"{what} must be a contiguous float64 host tensor of length {n}")
+        if a.is_cuda or a.dtype != tdt or not a.is_contiguous() or a.numel() != n:
+            raise ValueError(f"{what} must be a contiguous {tdt} host tensor of length {n}")
         return a.data_ptr()
-    a_np = a
-    if not (isinstance(a_np, np.ndarray) and a_np.dtype == np.float64 and a_np.flags.c_contiguous and a_np.size == n):
-        raise ValueError(f"{what} must be a contiguous float64 numpy array of length {n}")
-    return a_np.ctypes.data
+    if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous and a.size == n):
+        raise ValueError(f"{what} must be a contiguous {np.dtype(dtype).name} numpy array of length {n}")
+    return a.ctypes.data
 
 
 class Histogram:
@@ -401,6 +444,23 @@ class Histogram:
         ptrs = [_host_col(c, n, "coords") for c in coords]
         bh_fill_host(self.h, n, ptrs, None if w is None else _host_col(w, n, "w"), self._s(stream))
         return self
+
+    def fill_host_f32(self, coords, w=None, stream=None):
+        """Host float32 columns (pinned preferably): half the PCIe bytes of fill_host."""
+        self._fill_host_4(coords, w, np.float32, bh_fill_host_f32, stream)
+        return self
+
+    def fill_host_i32(self, coords, w=None, stream=None):
+        """Host int32 coordinate columns, optional host float32 weights."""
+        self._fill_host_4(coords, w, np.int32, bh_fill_host_i32, stream)
+        return self
+
+    def _fill_host_4(self, coords, w, cdt, fn, stream):
+        if len(coords) != self.dim:
+            raise ValueError(f"need {self.dim} coordinate columns, got {len(coords)}")
+        n = len(coords[0])
+        ptrs = [_host_col(c, n, "coords", cdt) for c in coords]
+        fn(self.h, n, ptrs, None if w is None else _host_col(w, n, "w", np.float32), self._s(stream))
 
     def find_bins(self, coords, stream=None):
         import torch

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/bhist.h"
@@ -102,6 +103,7 @@ struct bh_hist {
     double *stage[kStageSlots] = {};  // each slot: (dim+1) columns of `chunk` doubles
     int64_t stage_chunk = 0;
     cudaEvent_t copied[kStageSlots] = {}, consumed[kStageSlots] = {};
+    bool weighted_content = false;     // a weighted fill (or a full unpack) since create/reset
     bool slot_used[kStageSlots] = {};  // consumed[slot] recorded at least once (persists across calls)
     int next_slot = 0;                 // ring position (persists across calls)
 };
@@ -480,6 +482,7 @@ bool auto_sort(bh_hist *h, int64_t n, const double *const *coords, cudaStream_t 
 
 // One fill over device-resident columns, split into launches of <= 2^30 events.
 bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
+    if (w) h->weighted_content = true;
     if (w && h->strategy == BH_STRATEGY_EXACT) return fill_exact(h, n, coords, w, s);
     if (resolve_strategy(h, w != nullptr) == BH_STRATEGY_SORT) return fill_sort(h, n, coords, w, s);
     if (!w && auto_sort(h, n, coords, s)) return fill_sort(h, n, coords, w, s);
@@ -521,6 +524,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
 // 4-byte columns: float32 or (is_int) int32 coordinates, float32 weights.
 bh_status fill_device_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, cudaStream_t s,
                           bool is_int = false) {
+    if (w) h->weighted_content = true;
     FillPlan pl;
     if (bh_status r = plan_fill(h, w != nullptr, pl, n)) return r;
     LaunchCfg &c = pl.c;
@@ -767,6 +771,7 @@ bh_status bh_reset(bh_hist *h, bh_stream s) {
     CUDA_TRY(cudaMemsetAsync(h->sumw2, 0, sizeof(double) * h->G, st));
     CUDA_TRY(cudaMemsetAsync(h->stats, 0, sizeof(double) * 16, st));
     CUDA_TRY(cudaMemsetAsync(h->entries, 0, sizeof(unsigned long long), st));
+    h->weighted_content = false;
     return BH_OK;
 }
 
@@ -803,7 +808,13 @@ bh_status bh_fill_i32(bh_hist *h, int64_t n, const int32_t *const *coords, const
     return fill_device_f32(h, n, reinterpret_cast<const float *const *>(coords), w, static_cast<cudaStream_t>(s), true);
 }
 
-bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s) {
+}  // extern "C"
+
+namespace {
+// Host columns -> device staging ring (copy stream) -> the device fill of column type CT
+// (double: bh_fill path; float / int32_t: the 4-byte path with float32 weights).
+template <typename CT, typename WT>
+bh_status fill_host_impl(bh_hist *h, int64_t n, const CT *const *coords, const WT *w, bh_stream s) {
     if (check_hist(h)) return BH_EINVAL;
     if (n < 0) return fail(BH_EINVAL, "n < 0");
     if (n == 0) return BH_OK;
@@ -831,29 +842,34 @@ bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const
         }
         h->stage_chunk = h->chunk;
     }
-    const int64_t C = h->stage_chunk;
+    // a slot holds (dim + 1) columns of `chunk` float64 values: 2x `chunk` 4-byte values
+    const int64_t C = h->stage_chunk * (int64_t)(sizeof(double) / sizeof(CT));
     for (int64_t off = 0; off < n; off += C) {
         const int slot = h->next_slot;
         h->next_slot = (slot + 1) % kStageSlots;
         const int64_t m = std::min(C, n - off);
-        double *buf = h->stage[slot];
+        CT *buf = reinterpret_cast<CT *>(h->stage[slot]);
         // the slot may be overwritten only after the fill that read it has run:
         // that fill may belong to an earlier bh_fill_host call whose kernels are still queued
         // on a stream (this function returns once the HOST bytes are consumed, not the slots)
         if (h->slot_used[slot]) CUDA_TRY(cudaStreamWaitEvent(h->copy_stream, h->consumed[slot], 0));
-        const double *dcols[kMaxDim] = {};
+        const CT *dcols[kMaxDim] = {};
         for (int a = 0; a < h->dim; ++a) {
-            CUDA_TRY(cudaMemcpyAsync(buf + a * C, coords[a] + off, sizeof(double) * m, cudaMemcpyHostToDevice, h->copy_stream));
+            CUDA_TRY(cudaMemcpyAsync(buf + a * C, coords[a] + off, sizeof(CT) * m, cudaMemcpyHostToDevice, h->copy_stream));
             dcols[a] = buf + a * C;
         }
-        const double *dw = nullptr;
+        const WT *dw = nullptr;
         if (w) {
-            CUDA_TRY(cudaMemcpyAsync(buf + h->dim * C, w + off, sizeof(double) * m, cudaMemcpyHostToDevice, h->copy_stream));
-            dw = buf + h->dim * C;
+            WT *wb = reinterpret_cast<WT *>(buf + h->dim * C);
+            CUDA_TRY(cudaMemcpyAsync(wb, w + off, sizeof(WT) * m, cudaMemcpyHostToDevice, h->copy_stream));
+            dw = wb;
         }
         CUDA_TRY(cudaEventRecord(h->copied[slot], h->copy_stream));
         if (!(h->debug & BH_DEBUG_SKIP_COPY_WAIT)) CUDA_TRY(cudaStreamWaitEvent(st, h->copied[slot], 0));
-        bh_status r = fill_device(h, m, dcols, dw, st);
+        bh_status r;
+        if constexpr (sizeof(CT) == 8) r = fill_device(h, m, dcols, dw, st);
+        else r = fill_device_f32(h, m, reinterpret_cast<const float *const *>(dcols), dw, st,
+                                 std::is_same<CT, int32_t>::value);
         if (r != BH_OK) return r;
         CUDA_TRY(cudaEventRecord(h->consumed[slot], st));
         h->slot_used[slot] = true;
@@ -861,6 +877,21 @@ bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const
     // every host byte has been read once the last copy has completed
     CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
     return BH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+bh_status bh_fill_host(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s) {
+    return fill_host_impl<double, double>(h, n, coords, w, s);
+}
+
+bh_status bh_fill_host_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, bh_stream s) {
+    return fill_host_impl<float, float>(h, n, coords, w, s);
+}
+
+bh_status bh_fill_host_i32(bh_hist *h, int64_t n, const int32_t *const *coords, const float *w, bh_stream s) {
+    return fill_host_impl<int32_t, float>(h, n, coords, w, s);
 }
 
 bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_axis, const uint8_t *weighted,
@@ -885,6 +916,8 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
         nstats += hs[i]->K;
     }
     if (n == 0) return BH_OK;
+    for (int i = 0; i < nh; ++i)
+        if (weighted[i]) hs[i]->weighted_content = true;
     DeviceGuard dg(hs[0]->device);
     cudaStream_t st = static_cast<cudaStream_t>(s);
     // ---- plan.  The single-histogram kernel (k_fill, fully templated) is faster per
@@ -1039,6 +1072,7 @@ bh_status bh_fill_expr(bh_hist *h, int64_t n, const double *const *cols, int32_t
     }
     if (weight_reg >= kExprRegs || filter_reg >= kExprRegs) return fail(BH_EINVAL, "register out of range");
     e.weight_reg = weight_reg < 0 ? -1 : weight_reg;
+    if (e.weight_reg >= 0 && n > 0) h->weighted_content = true;
     e.filter_reg = filter_reg < 0 ? -1 : filter_reg;
     if (n == 0) return BH_OK;
     DeviceGuard dg(h->device);
@@ -1153,6 +1187,75 @@ bh_status bh_unpack(bh_hist *h, const double *dev_in, bh_stream s) {
                                                               h->entries, dev_in);
     CUDA_TRY(cudaGetLastError());
     h->launches++;
+    h->weighted_content = true;          // sumw2 now comes from the buffer
+    return BH_OK;
+}
+
+}  // extern "C"
+
+namespace {
+bh_status pack_plan(bh_hist *const *hs, int32_t nh, const uint8_t *unit, PackMultiP &p, bool packing) {
+    if (!hs || nh < 1 || nh > kMaxPack) return fail(BH_EINVAL, "need 1..%d histograms", kMaxPack);
+    p = PackMultiP{};
+    p.nh = nh;
+    int64_t off = 0;
+    for (int i = 0; i < nh; ++i) {
+        bh_hist *h = hs[i];
+        if (!h) return fail(BH_EINVAL, "histogram %d is NULL", i);
+        if (h->device != hs[0]->device) return fail(BH_EMISMATCH, "histograms live on different devices");
+        const bool u = unit && unit[i];
+        if (u && packing && h->weighted_content)
+            return fail(BH_EINVAL, "histogram %d holds weighted fills: it cannot be packed without sumw2", i);
+        PackDesc &D = p.d[i];
+        D.off = off;
+        D.G = (int32_t)h->G;
+        D.K = h->K;
+        D.unit = u ? 1 : 0;
+        D.count = h->count;
+        D.sumw = h->sumw;
+        D.sumw2 = h->sumw2;
+        D.stats = h->stats;
+        D.entries = h->entries;
+        off += (u ? 1 : 2) * h->G + h->K + 1;
+    }
+    p.total = off;
+    return BH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+bh_status bh_packed_size_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, int64_t *n_doubles) {
+    if (!n_doubles) return fail(BH_EINVAL, "NULL output");
+    PackMultiP p;
+    if (bh_status r = pack_plan(hs, nh, unit, p, false)) return r;
+    *n_doubles = p.total;
+    return BH_OK;
+}
+
+bh_status bh_pack_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, double *dev_out, bh_stream s) {
+    if (!dev_out) return fail(BH_EINVAL, "NULL output");
+    PackMultiP p;
+    if (bh_status r = pack_plan(hs, nh, unit, p, true)) return r;
+    DeviceGuard dg(hs[0]->device);
+    const int grid = (int)std::min<int64_t>((p.total + 255) / 256, (int64_t)hs[0]->nsm * 8);
+    k_pack_multi<<<grid, 256, 0, static_cast<cudaStream_t>(s)>>>(p, dev_out);
+    CUDA_TRY(cudaGetLastError());
+    hs[0]->launches++;
+    return BH_OK;
+}
+
+bh_status bh_unpack_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, const double *dev_in, bh_stream s) {
+    if (!dev_in) return fail(BH_EINVAL, "NULL input");
+    PackMultiP p;
+    if (bh_status r = pack_plan(hs, nh, unit, p, false)) return r;
+    DeviceGuard dg(hs[0]->device);
+    const int grid = (int)std::min<int64_t>((p.total + 255) / 256, (int64_t)hs[0]->nsm * 8);
+    k_unpack_multi<<<grid, 256, 0, static_cast<cudaStream_t>(s)>>>(p, dev_in);
+    CUDA_TRY(cudaGetLastError());
+    hs[0]->launches++;
+    for (int i = 0; i < nh; ++i)
+        if (!(unit && unit[i])) hs[i]->weighted_content = true;
     return BH_OK;
 }
 

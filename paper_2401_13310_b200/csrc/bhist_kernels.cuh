@@ -1483,6 +1483,59 @@ __global__ void k_unpack(int G, int K, unsigned long long *count, double *sumw, 
     }
 }
 
+// Several histograms packed into one buffer for ONE collective per step:
+// histogram i occupies [off_i, off_i + len_i) with the bh_pack layout, or, when unit_i is
+// set (a unit-weight-only state: sumw2 == content), [content(G) | stats(K) | entries].
+struct PackDesc {
+    int64_t off;
+    int32_t G, K, unit;
+    unsigned long long *count;
+    double *sumw, *sumw2, *stats;
+    unsigned long long *entries;
+};
+constexpr int kMaxPack = 8;
+struct PackMultiP {
+    int32_t nh;
+    int64_t total;
+    PackDesc d[kMaxPack];
+};
+
+__device__ __forceinline__ int pack_find(const PackMultiP &p, int64_t i) {
+    int k = 0;
+    while (k + 1 < p.nh && p.d[k + 1].off <= i) ++k;
+    return k;
+}
+
+__global__ void k_pack_multi(const __grid_constant__ PackMultiP p, double *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.total; i += (int64_t)gridDim.x * blockDim.x) {
+        const PackDesc &D = p.d[pack_find(p, i)];
+        const int64_t j = i - D.off, G = D.G;
+        const int64_t s2 = D.unit ? 0 : G;           // length of the sumw2 section
+        double v;
+        if (j < G) v = (double)D.count[j] + D.sumw[j];
+        else if (j < G + s2) v = (double)D.count[j - G] + D.sumw2[j - G];
+        else if (j < G + s2 + D.K) v = D.stats[j - G - s2];
+        else v = (double)*D.entries;
+        out[i] = v;
+    }
+}
+
+__global__ void k_unpack_multi(const __grid_constant__ PackMultiP p, const double *in) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.total; i += (int64_t)gridDim.x * blockDim.x) {
+        const PackDesc &D = p.d[pack_find(p, i)];
+        const int64_t j = i - D.off, G = D.G;
+        const int64_t s2 = D.unit ? 0 : G;
+        const double v = in[i];
+        if (j < G) {
+            D.count[j] = 0ull;
+            D.sumw[j] = v;
+            if (D.unit) D.sumw2[j] = v;              // unit weights: sum w^2 == count
+        } else if (j < G + s2) D.sumw2[j - G] = v;
+        else if (j < G + s2 + D.K) D.stats[j - G - s2] = v;
+        else *D.entries = (unsigned long long)v;
+    }
+}
+
 #endif  // BH_FILL_TU
 
 }  // namespace bh

@@ -239,3 +239,129 @@ def test_forced_priv_weighted_falls_back_when_cells_do_not_fit():
     h.fill([_t(x), _t(y)], _t(w))
     compare(h.read(), oracle.OracleHist(axes).fill([x, y], w).read(), True, "forced PRIV weighted")
     h.close()
+
+
+# ------------------------------------------------------------------ host float32 / int32 columns (NEXT-2)
+@pytest.mark.parametrize("kind", ["f32", "i32"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_fill_host_4byte_columns(kind, weighted):
+    """bh_fill_host_f32 / _i32: host 4-byte columns through the staging ring (chunks of
+    2x the float64 chunk), equal to the oracle on the exactly widened columns."""
+    rng = np.random.default_rng(31)
+    n = 1_000_003
+    if kind == "f32":
+        x = rng.normal(0.5, 0.2, n).astype(np.float32)
+        y = rng.uniform(-0.1, 1.1, n).astype(np.float32)
+        axes = [bhgen.workload("C2", 10).hists[0].axes[0].edges, (50, 0.0, 1.0)]
+    else:
+        x = rng.integers(-5, 120, n).astype(np.int32)
+        y = rng.poisson(7.0, n).astype(np.int32)
+        axes = [(100, 0.0, 100.0), np.array([0.0, 2.0, 5.0, 6.0, 7.0, 8.0, 12.0, 30.0])]
+    w = rng.uniform(0.5, 1.5, n).astype(np.float32) if weighted else None
+    h = pkg.Histogram(axes)
+    pkg.bh_set_chunk(h.h, 100_000)
+    xs = [torch.from_numpy(x).pin_memory(), torch.from_numpy(y)]       # pinned and pageable
+    tw = None if w is None else torch.from_numpy(w).pin_memory()
+    (h.fill_host_f32 if kind == "f32" else h.fill_host_i32)(xs, tw)
+    ref = oracle.OracleHist(axes).fill([x.astype(np.float64), y.astype(np.float64)],
+                                       None if w is None else w.astype(np.float64)).read()
+    compare(h.read(), ref, weighted, f"fill_host_{kind}")
+    h.close()
+
+
+# ------------------------------------------------------------------ multi-histogram exchange (SURVEY §8(e))
+def test_pack_multi_layout_and_roundtrip():
+    """bh_pack_multi: histograms back to back, unit ones without sumw2; unpack restores
+    every state (unit: sumw2 := content); a unit entry for a weighted histogram is refused."""
+    wl = bhgen.workload("C5", 300_001)
+    n = wl.n_events
+    cols = [_t(wl.column(c, 0, n)) for c in range(len(wl.columns))]
+    w = _t(wl.column(wl.wcol, 0, n))
+    hs = [pkg.Histogram(oracle.oracle_axes(hist)) for hist in wl.hists]
+    pkg.fill_multi(hs, [hist.cols for hist in wl.hists], [hist.weighted for hist in wl.hists], cols, w)
+    before = [h.read() for h in hs]
+    unit = [not hist.weighted for hist in wl.hists]
+    handles = [h.h for h in hs]
+    size = pkg.bh_packed_size_multi(handles, unit)
+    assert size == sum((1 if u else 2) * h.nbins_total + h.nstats + 1 for h, u in zip(hs, unit))
+    buf = torch.empty(size, dtype=torch.float64, device=DEV)
+    pkg.bh_pack_multi(handles, unit, buf.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    b = buf.cpu().numpy()
+    off = 0
+    for r, u, h in zip(before, unit, hs):
+        assert np.array_equal(b[off:off + h.nbins_total], r["content"])
+        off += h.nbins_total
+        if not u:
+            assert np.array_equal(b[off:off + h.nbins_total], r["sumw2"])
+            off += h.nbins_total
+        assert np.array_equal(b[off:off + h.nstats], r["stats"])
+        off += h.nstats
+        assert b[off] == r["entries"]
+        off += 1
+    for h in hs:
+        h.reset()
+    pkg.bh_unpack_multi(handles, unit, buf.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    for h, r in zip(hs, before):
+        a = h.read()
+        for k in ("content", "sumw2", "stats"):
+            assert np.array_equal(a[k], r[k]), k
+        assert a["entries"] == r["entries"]
+    with pytest.raises(pkg.BHistError):       # histogram 1 is weighted: no unit packing
+        hs[1].fill([cols[1]], w)
+        pkg.bh_pack_multi(handles, [True] * len(hs), buf.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    for h in hs:
+        h.close()
+
+
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _bench_ranks(tmp_path, world, backend, config, events, exchange):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dump = str(tmp_path / f"dump_{config}_{exchange}.npz")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--gpus", str(world), "--steps", "3", "--warmup", "3", "--backend", backend, "--events", str(events),
+           "--e2e-steps", "1", "--config", config, "--exchange", exchange, "--dump", dump]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    return json.loads(lines[0]), np.load(dump)
+
+
+@pytest.mark.parametrize("config,exchange", [("C2", "reduce"), ("C5", "allreduce"), ("C3", "reduce")])
+def test_bench_two_ranks_reduced_state_matches_oracle(tmp_path, config, exchange):
+    """bench.py --gpus 2 (two gloo ranks sharing cuda:0): each rank fills its contiguous
+    shard [r N, (r+1) N), one collective per step sums all histograms; the state rank 0
+    ends with equals the oracle over all 2N events."""
+    events = 400_003
+    d, z = _bench_ranks(tmp_path, 2, "gloo", config, events, exchange)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    wl = bhgen.workload(config, 2 * events)
+    for i, hist in enumerate(wl.hists):
+        ref = oracle_parallel(config, 2 * events, hidx=i, nproc=4)
+        got = {"content": z[f"content{i}"], "sumw2": z[f"sumw2{i}"], "stats": z[f"stats{i}"],
+               "entries": int(z[f"entries{i}"])}
+        compare(got, ref, hist.weighted, f"{config} H{i} {exchange}")
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("exchange", ["reduce", "allreduce"])
+def test_nccl_two_gpus_reduced_state_matches_oracle(tmp_path, exchange):
+    """The same over NCCL on two GPUs (skipped on one-GPU boxes)."""
+    events = 2_000_003
+    d, z = _bench_ranks(tmp_path, 2, "nccl", "C5", events, exchange)
+    wl = bhgen.workload("C5", 2 * events)
+    for i, hist in enumerate(wl.hists):
+        ref = oracle_parallel("C5", 2 * events, hidx=i)
+        got = {"content": z[f"content{i}"], "sumw2": z[f"sumw2{i}"], "stats": z[f"stats{i}"],
+               "entries": int(z[f"entries{i}"])}
+        compare(got, ref, hist.weighted, f"nccl C5 H{i}")

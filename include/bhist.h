@@ -105,6 +105,8 @@ typedef struct {
 /* Debug flags (bh_set_debug) — negative controls for tests only. */
 #define BH_DEBUG_SKIP_COPY_WAIT 1 /* bh_fill_host: fill without waiting for the H2D copy (PAPER.md:223 race) */
 #define BH_DEBUG_FIND_BINS_GLOBAL 2 /* bh_find_bins: search variable axes in global memory, not the fills' staged tables */
+#define BH_DEBUG_REQUIRE_JIT 4      /* bh_fill_multi (flag on hs[0]): fail instead of falling back when the
+                                       run-time compiled one-pass kernel is unavailable */
 
 /* ABI version (major*10000 + minor*100 + patch). */
 int32_t bh_version(void);
@@ -244,6 +246,13 @@ bh_status bh_unpack(bh_hist *h, const double *dev_in, bh_stream s);
 bh_status bh_packed_size_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, int64_t *n_doubles);
 bh_status bh_pack_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, double *dev_out, bh_stream s);
 bh_status bh_unpack_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, const double *dev_in, bh_stream s);
+
+/* Diagnostics (no GPU needed): compile the one-pass fused kernel of bh_fill_multi for the
+ * histogram-set instantiation `kernel_expr` (e.g. "bh::k_fused<bh::Role<...>>", the form the
+ * planner generates) with NVRTC for sm_100a, `threads` per CTA and `ept` events per thread
+ * per tile.  Writes a NUL-terminated message (the NVRTC log on failure) to log[log_size].
+ * BH_OK, BH_EINVAL, or BH_ECUDA when NVRTC is unavailable or the compile fails. */
+bh_status bh_jit_compile_check(const char *kernel_expr, int32_t threads, int32_t ept, char *log, int64_t log_size);
 
 /* Read back to HOST buffers (any may be NULL): contents[G], sumw2[G], stats[K] (ROOT
  * GetStats order, reading R8), entries — "only copy back ... once all bulks have been

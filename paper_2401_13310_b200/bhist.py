@@ -20,11 +20,13 @@ BH_OK, BH_EINVAL, BH_ENOMEM, BH_ECUDA, BH_EDEVICE, BH_EMISMATCH = 0, -1, -2, -3,
 BH_STRATEGY_AUTO, BH_STRATEGY_PRIV, BH_STRATEGY_GLOBAL, BH_STRATEGY_CACHE, BH_STRATEGY_EXACT, BH_STRATEGY_SORT = 0, 1, 2, 3, 4, 5
 BH_DEBUG_SKIP_COPY_WAIT = 1
 BH_DEBUG_FIND_BINS_GLOBAL = 2
+BH_DEBUG_REQUIRE_JIT = 4
 
 # every symbol include/bhist.h declares (checked by tests/test_abi.py)
 EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset", "bh_fill", "bh_fill_host",
             "bh_fill_multi", "bh_fill_expr", "bh_fill_f32", "bh_fill_i32", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
             "bh_fill_host_f32", "bh_fill_host_i32", "bh_packed_size_multi", "bh_pack_multi", "bh_unpack_multi",
+            "bh_jit_compile_check",
             "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_launch_count"]
 
 
@@ -82,6 +84,7 @@ def lib(build_if_stale: bool = False):
             "bh_packed_size_multi": ([_P, _I32, _P, _P], _I32),
             "bh_pack_multi": ([_P, _I32, _P, _P, _P], _I32),
             "bh_unpack_multi": ([_P, _I32, _P, _P, _P], _I32),
+            "bh_jit_compile_check": ([ctypes.c_char_p, _I32, _I32, ctypes.c_char_p, _I64], _I32),
             "bh_find_bins": ([_P, _I64, _P, _P, _P], _I32),
             "bh_fill_multi": ([_P, _I32, _P, _P, _I64, _P, _I32, _P, _P], _I32),
             "bh_fill_expr": ([_P, _I64, _P, _I32, _P, _I32, _P, _I32, _I32, _P], _I32),
@@ -205,6 +208,13 @@ def bh_unpack_multi(handles, unit, dev_in_ptr, stream=None) -> None:
     nh, hs, u = _multi_args(handles, unit)
     _check(lib().bh_unpack_multi(ctypes.addressof(hs), nh, None if u is None else ctypes.addressof(u), dev_in_ptr,
                                  stream))
+
+
+def bh_jit_compile_check(kernel_expr: str, threads: int = 512, ept: int = 2) -> str:
+    """NVRTC-compile a fused-kernel instantiation for sm_100a (no GPU needed); returns the message."""
+    buf = ctypes.create_string_buffer(4096)
+    _check(lib().bh_jit_compile_check(kernel_expr.encode(), threads, ept, buf, len(buf)))
+    return buf.value.decode()
 
 
 def bh_fill_multi(handles, col_of_axis, weighted, n: int, col_ptrs, w_ptr=None, stream=None) -> None:

@@ -19,6 +19,7 @@
 
 #include "../../include/bhist.h"
 #include "bhist_launch.cuh"
+#include "bhist_state.h"
 
 using namespace bh;
 
@@ -56,57 +57,9 @@ struct DeviceGuard {
     }
 };
 
-constexpr int kStageSlots = 2;
-
 }  // namespace
 
-struct bh_hist {
-    int device = 0;
-    int dim = 0;
-    int nsm = 148;
-    int K = 0;
-    int64_t G = 0;
-    AxisP ax[kMaxDim] = {};
-    int32_t st1 = 1, st2 = 1;
-    int strategy = BH_STRATEGY_AUTO;
-    int debug = 0;
-    int64_t chunk = 1 << 22;
-    int64_t launches = 0;
-    size_t smem_optin = 0;
-    int max_grid = 0;
-    // device state
-    unsigned long long *count = nullptr;
-    double *sumw = nullptr, *sumw2 = nullptr;
-    double *stats = nullptr;
-    unsigned long long *entries = nullptr;
-    double *partials = nullptr;
-    unsigned int *counter = nullptr;
-    long long *limbs = nullptr;       // EXACT: per bin 2 x kLimbs int64 limbs (sumw, sumw2), zero between fills
-    unsigned long long *maxbits = nullptr;   // EXACT: bit pattern of max|w| of the current launch
-    double *pack_buf = nullptr;       // device buffer for bh_read
-    double *pack_host = nullptr;      // pinned host buffer for bh_read
-    // SORT strategy scratch (grown on demand): records, segment offsets, partition totals
-    uint16_t *part_l = nullptr;
-    double *part_w = nullptr;
-    uint32_t *part_offs = nullptr;
-    unsigned long long *part_cnt = nullptr, *part_cp = nullptr;
-    int64_t part_cap_l = 0, part_cap_w = 0, part_cap_offs = 0;
-    int part_P = 0;
-    // AUTO's SORT decision for large unit-weight fills: 0 unknown, 1 probe in flight,
-    // 2 spread-out data (SORT), 3 a hot partition (CACHE)
-    int probe_state = 0;
-    unsigned int *probe_dev = nullptr, *probe_host = nullptr;
-    cudaEvent_t probe_done = nullptr;
-    std::vector<void *> axis_mem;     // edges and guide tables
-    // host->device double buffer
-    cudaStream_t copy_stream = nullptr;
-    double *stage[kStageSlots] = {};  // each slot: (dim+1) columns of `chunk` doubles
-    int64_t stage_chunk = 0;
-    cudaEvent_t copied[kStageSlots] = {}, consumed[kStageSlots] = {};
-    bool weighted_content = false;     // a weighted fill (or a full unpack) since create/reset
-    bool slot_used[kStageSlots] = {};  // consumed[slot] recorded at least once (persists across calls)
-    int next_slot = 0;                 // ring position (persists across calls)
-};
+
 
 namespace {
 
@@ -572,6 +525,11 @@ bh_status check_hist(const bh_hist *h) {
 
 }  // namespace
 
+namespace bh {
+bh_status set_error(bh_status st, const char *msg) { return fail(st, "%s", msg); }
+size_t axis_table_bytes_of(const AxisP &a) { return axis_table_bytes(a); }
+}  // namespace bh
+
 extern "C" {
 
 int32_t bh_version(void) { return 10000; }
@@ -920,7 +878,31 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
         if (weighted[i]) hs[i]->weighted_content = true;
     DeviceGuard dg(hs[0]->device);
     cudaStream_t st = static_cast<cudaStream_t>(s);
-    // ---- plan.  The single-histogram kernel (k_fill, fully templated) is faster per
+    // ---- one pass for every histogram (bhist_jit.cu): a kernel specialized to this set,
+    // compiled at run time; EXACT / forced-SORT histograms keep passes of their own
+    std::vector<int> jit_idx, rest_idx;
+    for (int i = 0; i < nh; ++i) {
+        const int st = hs[i]->strategy;
+        if ((st == BH_STRATEGY_EXACT && weighted[i]) || st == BH_STRATEGY_SORT) rest_idx.push_back(i);
+        else jit_idx.push_back(i);
+    }
+    if (jit_idx.size() >= 2) {
+        bool done = false;
+        if (bh_status r = fused_fill(hs, jit_idx.data(), (int)jit_idx.size(), col_of_axis, weighted, n, cols, ncols, w,
+                                     st, &done))
+            return r;
+        if (done) {
+            for (int i : rest_idx) {
+                const double *cs[kMaxDim] = {};
+                for (int a = 0; a < hs[i]->dim; ++a) cs[a] = cols[col_of_axis[3 * i + a]];
+                if (bh_status r = fill_device(hs[i], n, cs, weighted[i] ? w : nullptr, st)) return r;
+            }
+            return BH_OK;
+        }
+        if (hs[0]->debug & BH_DEBUG_REQUIRE_JIT)
+            return fail(BH_ECUDA, "fused one-pass fill unavailable: %s", g_err.c_str());
+    }
+    // ---- fallback plan.  The single-histogram kernel (k_fill, fully templated) is faster per
     // histogram than the generic fused kernel, and the fill is bound by the bin updates,
     // not by HBM; so fusing only pays when histograms read the SAME columns (e.g. one
     // variable with several binnings): then the fused pass reads them once.  Histograms

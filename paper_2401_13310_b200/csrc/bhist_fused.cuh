@@ -1,0 +1,316 @@
+// bhist_fused.cuh — one-pass fill of several histograms from shared columns (bh_fill_multi).
+//
+// The paper's future work "compute multiple histograms using data in different (parts of
+// the) columns" in one pass; RDataFrame runs every action of a dataframe in
+// one event loop.  Each histogram runs the same three steps as k_fill
+// (PAPER.md:126): FindBin per axis, bin += w with sum w^2, the GetStats sums.
+//
+// The kernel is a template over the histogram set, instantiated at run time with NVRTC
+// (bhist_jit.cu) for the exact set a bh_fill_multi call names, so every histogram's shape
+// (dimension, weights, axis kinds, sink, columns) is a compile-time constant and its
+// statistics live in registers.  Histograms whose private state does not fit one SM's
+// shared memory together are split over the CTAs of a thread-block CLUSTER ("roles"):
+// the R CTAs of a cluster walk the same event tiles, each role reading the columns its
+// histograms need; a column several roles read is fetched from DRAM once and served to
+// the other roles from L2, kept there by a cluster barrier every few tiles (the roles stay
+// within sync_tiles tiles of each other, so the re-read lines are still resident).
+#pragma once
+#include "bhist_kernels.cuh"
+
+#ifndef BH_FUSED_THREADS
+#define BH_FUSED_THREADS 512
+#endif
+#ifndef BH_FUSED_EPT
+#define BH_FUSED_EPT 2       // events per thread per tile (loads in flight before processing)
+#endif
+
+namespace bh {
+
+constexpr int kFusedMaxHist = 8;
+constexpr int kFusedMaxCols = 8;
+
+struct FusedH {
+    AxisP ax[kMaxDim];            // tab_off: byte offset of the staged tables (VM 1 / 3 axes)
+    int32_t st1, st2, G, K;
+    int32_t smem_off;             // PRIV sinks: byte offset of the private bins
+    unsigned long long *count;    // unit-weight counts [G]
+    double *sumw, *sumw2;         // weighted sums [G]
+    double *stats, *partials;     // running stats [K]; per-cluster partials [nclusters * K]
+    unsigned long long *entries;
+    unsigned int *counter;        // last-CTA ticket of this histogram
+};
+
+struct FusedP {
+    int64_t n;
+    const double *cols[kFusedMaxCols];
+    const double *w;
+    int32_t nclusters;            // clusters in the grid (= CTAs per role)
+    int32_t sync_tiles;           // cluster barrier every sync_tiles tiles
+    FusedH h[kFusedMaxHist];
+};
+
+// Sinks: block-private bins in shared memory (plain: one ATOMS / 128-bit CAS per event;
+// AGG: lanes of a warp on the same bin first combine, one update per distinct bin -- hot
+// bins of small or peaked histograms), or warp-aggregated atomics straight into the
+// L2-resident global bins (bin spaces too large for shared memory).
+enum FusedSink { FS_PRIV = 0, FS_PRIV_AGG = 1, FS_GLOBAL_AGG = 2 };
+
+// One histogram of a role.  VMa per axis: 0 fixed, 1 variable with tables staged in shared
+// memory (guide mode at run time), 2 variable searched in global memory, 3 variable compact.
+template <int ID_, int DIM_, bool W_, int SINK_, int C0, int C1, int C2, int VM0, int VM1, int VM2>
+struct HS {
+    static_assert(ID_ >= 0 && ID_ < 8 && DIM_ >= 1 && DIM_ <= 3 && SINK_ >= 0 && SINK_ <= 2, "bad histogram spec");
+    static_assert(C0 >= 0 && C0 < 8 && C1 >= 0 && C1 < 8 && C2 >= 0 && C2 < 8, "column index out of range");
+    static_assert(VM0 >= 0 && VM0 <= 3 && VM1 >= 0 && VM1 <= 3 && VM2 >= 0 && VM2 <= 3, "bad axis mode");
+    static constexpr int ID = ID_, DIM = DIM_, SINK = SINK_;
+    static constexpr bool W = W_;
+    static constexpr unsigned colmask = (1u << C0) | (DIM_ > 1 ? 1u << C1 : 0u) | (DIM_ > 2 ? 1u << C2 : 0u);
+    static constexpr int col[3] = {C0, C1, C2};
+    static constexpr int vm[3] = {VM0, VM1, VM2};
+};
+
+// A role: the histograms one CTA of the cluster owns.  SHARED: columns other roles read too
+// (loaded with the default L2 policy; the others stream with evict-first).
+template <unsigned SHARED, class... Hs>
+struct Role {};
+
+template <int VM>
+__device__ __forceinline__ int fused_find_bin(const AxisP &a, double x, const unsigned char *smem) {
+    if (VM == 0) return find_bin_fixed(a, x);
+    if (VM == 3) return find_bin_var_compact(a, x, smem + a.tab_off);
+    if (VM == 1) return find_bin_var_smem_any(a, x, smem + a.tab_off);
+    return find_bin_var_global(a, x);
+}
+
+// registers: one Acc per histogram of the role
+template <class... Hs> struct AccT;
+template <> struct AccT<> {
+    __device__ __forceinline__ void zero() {}
+};
+template <class H, class... Rest> struct AccT<H, Rest...> {
+    Acc<H::DIM, H::W> a;
+    AccT<Rest...> rest;
+    __device__ __forceinline__ void zero() { a.zero(); rest.zero(); }
+};
+
+// warp-aggregated add: lanes of `act` holding the same bin g combine (count by popc, sums
+// of w and w*w by a shuffle walk over the peer mask); the group leader gets the totals
+template <bool W>
+__device__ __forceinline__ bool agg_group(unsigned act, int g, double w, double &s1, double &s2, unsigned &cnt) {
+    const unsigned peers = __match_any_sync(act, g);
+    const int lane = (int)(threadIdx.x & 31);
+    cnt = (unsigned)__popc(peers);
+    if (W) {
+        const int rounds = __reduce_max_sync(act, cnt);
+        s1 = 0.0;
+        s2 = 0.0;
+        unsigned m = peers;
+        for (int k = 0; k < rounds; ++k) {
+            const int src = m ? __ffs(m) - 1 : lane;
+            const double v = __shfl_sync(act, w, src);
+            if (m) { s1 += v; s2 = fma(v, v, s2); m &= m - 1; }
+        }
+    }
+    return lane == __ffs(peers) - 1;
+}
+
+template <class H>
+__device__ __forceinline__ void fused_sink(const FusedH &F, int g, double w, bool valid, unsigned char *smem) {
+    if constexpr (H::SINK == FS_PRIV) {
+        if (!valid) return;
+        if constexpr (H::W) add2_shared(reinterpret_cast<double2 *>(smem + F.smem_off) + g, w, w * w);
+        else asm volatile("red.shared.add.u32 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(smem + F.smem_off) + 4u * (uint32_t)g)
+                          : "memory");
+    } else {
+        __syncwarp();
+        const unsigned act = __ballot_sync(0xffffffffu, valid);
+        if (!valid) return;
+        double s1, s2;
+        unsigned cnt;
+        if (!agg_group<H::W>(act, g, w, s1, s2, cnt)) return;
+        if constexpr (H::SINK == FS_PRIV_AGG) {
+            if constexpr (H::W) add2_shared(reinterpret_cast<double2 *>(smem + F.smem_off) + g, s1, s2);
+            else atomicAdd(reinterpret_cast<uint32_t *>(smem + F.smem_off) + g, cnt);
+        } else {
+            if constexpr (H::W) {
+                atomicAdd(F.sumw + g, s1);
+                atomicAdd(F.sumw2 + g, s2);
+            } else {
+                atomicAdd(F.count + g, (unsigned long long)cnt);
+            }
+        }
+    }
+}
+
+template <class... Hs> struct Proc;
+template <> struct Proc<> {
+    template <class X>
+    static __device__ __forceinline__ void event(const FusedP &, const X &, double, bool, unsigned char *, AccT<> &) {}
+    static __device__ __forceinline__ void init(const FusedP &, unsigned char *) {}
+    static __device__ __forceinline__ void flush(const FusedP &, unsigned char *) {}
+    static __device__ __forceinline__ void finish(const FusedP &, unsigned char *, AccT<> &, int) {}
+};
+
+template <class H, class... Rest> struct Proc<H, Rest...> {
+    // FindBin on axis A (step (1), per axis) and its term of the global bin
+    template <int A, class X>
+    static __device__ __forceinline__ void axis_step(const FusedH &F, const X &x, double (&xa)[H::DIM], int &g,
+                                                     bool &inr, const unsigned char *smem) {
+        xa[A] = x[H::col[A]];
+        const int b = fused_find_bin<H::vm[A]>(F.ax[A], xa[A], smem);
+        inr &= (b >= 1) & (b <= F.ax[A].n);
+        g += A == 0 ? b : b * (A == 1 ? F.st1 : F.st2);
+    }
+    // steps (1)-(3) of PAPER.md:126 for histogram H on one event (x: the role's columns)
+    template <class X>
+    static __device__ __forceinline__ void event(const FusedP &p, const X &x, double w, bool valid, unsigned char *smem,
+                                                 AccT<H, Rest...> &acc) {
+        const FusedH &F = p.h[H::ID];
+        double xa[H::DIM];
+        int g = 0;
+        bool inr = true;
+        axis_step<0>(F, x, xa, g, inr, smem);
+        if constexpr (H::DIM > 1) axis_step<1>(F, x, xa, g, inr, smem);
+        if constexpr (H::DIM > 2) axis_step<2>(F, x, xa, g, inr, smem);
+        const double wv = H::W ? w : 1.0;
+        fused_sink<H>(F, g, wv, valid, smem);
+        if (valid && inr) acc.a.add(xa, wv);
+        Proc<Rest...>::event(p, x, w, valid, smem, acc.rest);
+    }
+    // zero the private bins, stage the variable-axis tables
+    static __device__ __forceinline__ void init(const FusedP &p, unsigned char *smem) {
+        const FusedH &F = p.h[H::ID];
+        if constexpr (H::SINK != FS_GLOBAL_AGG) {
+            if constexpr (H::W) {
+                double2 *d = reinterpret_cast<double2 *>(smem + F.smem_off);
+                for (int i = threadIdx.x; i < F.G; i += blockDim.x) d[i] = make_double2(0.0, 0.0);
+            } else {
+                uint32_t *c = reinterpret_cast<uint32_t *>(smem + F.smem_off);
+                for (int i = threadIdx.x; i < F.G; i += blockDim.x) c[i] = 0u;
+            }
+        }
+        if constexpr (H::vm[0] == 1 || H::vm[0] == 3) stage_axes<1>(&F.ax[0], smem);
+        if constexpr (H::DIM > 1 && (H::vm[1] == 1 || H::vm[1] == 3)) stage_axes<1>(&F.ax[1], smem);
+        if constexpr (H::DIM > 2 && (H::vm[2] == 1 || H::vm[2] == 3)) stage_axes<1>(&F.ax[2], smem);
+        Proc<Rest...>::init(p, smem);
+    }
+    // merge stage: private bins -> global, once per CTA
+    static __device__ __forceinline__ void flush(const FusedP &p, unsigned char *smem) {
+        const FusedH &F = p.h[H::ID];
+        if constexpr (H::SINK != FS_GLOBAL_AGG) {
+            if constexpr (H::W) {
+                const double2 *d = reinterpret_cast<const double2 *>(smem + F.smem_off);
+                for (int i = threadIdx.x; i < F.G; i += blockDim.x) {
+                    const double2 v = d[i];
+                    if (v.x != 0.0) atomicAdd(F.sumw + i, v.x);
+                    if (v.y != 0.0) atomicAdd(F.sumw2 + i, v.y);
+                }
+            } else {
+                const uint32_t *c = reinterpret_cast<const uint32_t *>(smem + F.smem_off);
+                for (int i = threadIdx.x; i < F.G; i += blockDim.x)
+                    if (c[i]) atomicAdd(F.count + i, (unsigned long long)c[i]);
+            }
+        }
+        Proc<Rest...>::flush(p, smem);
+    }
+    // stats: block sum -> this cluster's partial -> the last of the role's CTAs sums the
+    // partials in cluster order (deterministic for a given grid) and adds them (include-
+    // initial); it also adds the events to entries.  smem: scratch.
+    static __device__ __forceinline__ void finish(const FusedP &p, unsigned char *smem, AccT<H, Rest...> &acc,
+                                                  int cid) {
+        constexpr int K = NStats<H::DIM>::K;
+        const FusedH &F = p.h[H::ID];
+        double *red = reinterpret_cast<double *>(smem);         // [32 warps][K]
+        __shared__ bool last;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        acc.a.finalize_unit();
+        __syncthreads();                                      // scratch free (previous histogram)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double v = acc.a.s[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red[warp * K + k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < K) {
+            double t = 0.0;
+            for (int i = 0; i < nw; ++i) t += red[i * K + threadIdx.x];
+            F.partials[(size_t)cid * K + threadIdx.x] = t;
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(F.counter, 1u) == (unsigned)p.nclusters - 1;
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            for (int k = warp; k < K; k += nw) {
+                double t = 0.0;
+                for (int b = lane; b < p.nclusters; b += 32) t += __ldcg(F.partials + (size_t)b * K + k);
+                t = warp_sum_fixed(t);
+                if (lane == 0) F.stats[k] += t;
+            }
+            if (threadIdx.x == 0) {
+                *F.entries += (unsigned long long)p.n;
+                *F.counter = 0u;
+            }
+        }
+        Proc<Rest...>::finish(p, smem, acc.rest, cid);
+    }
+};
+
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
+template <unsigned SHARED, class... Hs>
+__device__ __forceinline__ void run_role(const FusedP &p, unsigned char *smem, Role<SHARED, Hs...> *) {
+    constexpr unsigned kCols = (0u | ... | Hs::colmask);
+    constexpr bool kW = (false || ... || Hs::W);
+    using P = Proc<Hs...>;
+    P::init(p, smem);
+    __syncthreads();
+    AccT<Hs...> acc;
+    acc.zero();
+    unsigned nclus_sz;
+    asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(nclus_sz));
+    const int cid = (int)(blockIdx.x / nclus_sz);
+    const int64_t T = blockDim.x, tile = T * BH_FUSED_EPT;
+    const int64_t ntiles = (p.n + tile - 1) / tile;
+    int it = 0;
+    for (int64_t t = cid; t < ntiles; t += p.nclusters, ++it) {
+        if (nclus_sz > 1 && it > 0 && it % p.sync_tiles == 0) cluster_sync_relaxed();
+        const int64_t base = t * tile + threadIdx.x;
+        double x[BH_FUSED_EPT][kFusedMaxCols];
+        double w[BH_FUSED_EPT];
+#pragma unroll
+        for (int k = 0; k < BH_FUSED_EPT; ++k) {
+            const int64_t i = base + k * T;
+            const bool valid = i < p.n;
+#pragma unroll
+            for (int c = 0; c < kFusedMaxCols; ++c) {
+                x[k][c] = 0.0;
+                if ((kCols >> c) & 1u)
+                    if (valid) x[k][c] = ((SHARED >> c) & 1u) ? __ldcg(p.cols[c] + i) : __ldcs(p.cols[c] + i);
+            }
+            w[k] = (kW && valid) ? __ldcg(p.w + i) : 1.0;
+        }
+#pragma unroll
+        for (int k = 0; k < BH_FUSED_EPT; ++k) P::event(p, x[k], w[k], base + k * T < p.n, smem, acc);
+    }
+    // the cluster's roles leave the loop together (every CTA runs the same trips)
+    __syncthreads();
+    P::flush(p, smem);
+    P::finish(p, smem, acc, cid);
+}
+
+template <class... Rs>
+__global__ void __launch_bounds__(BH_FUSED_THREADS, 1) k_fused(const __grid_constant__ FusedP p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned rank;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    unsigned r = 0;
+    ((rank == r++ ? run_role(p, smem, static_cast<Rs *>(nullptr)) : void()), ...);
+}
+
+}  // namespace bh

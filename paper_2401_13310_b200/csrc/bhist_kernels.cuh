@@ -9,8 +9,23 @@
 // The statistics end in per-CTA partials reduced in a fixed order by the last CTA
 // to finish, so they are run-to-run deterministic for a given launch shape.
 #pragma once
+#ifdef __CUDACC_RTC__          // run-time compiled (NVRTC, bhist_jit.cu): no host headers
+typedef signed char int8_t;
+typedef short int16_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long long uintptr_t;
+#ifndef BH_FILL_TU
+#define BH_FILL_TU
+#endif
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace bh {
 

@@ -1,0 +1,72 @@
+// bhist_state.h — the opaque bh_hist of include/bhist.h (host-side; shared by the
+// translation units of the library's host code: bhist.cu and bhist_jit.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "../../include/bhist.h"
+#include "bhist_kernels.cuh"
+
+constexpr int kStageSlots = 2;
+
+struct bh_hist {
+    int device = 0;
+    int dim = 0;
+    int nsm = 148;
+    int K = 0;
+    int64_t G = 0;
+    bh::AxisP ax[bh::kMaxDim] = {};
+    int32_t st1 = 1, st2 = 1;
+    int strategy = BH_STRATEGY_AUTO;
+    int debug = 0;
+    int64_t chunk = 1 << 22;
+    int64_t launches = 0;
+    size_t smem_optin = 0;
+    int max_grid = 0;
+    // device state
+    unsigned long long *count = nullptr;
+    double *sumw = nullptr, *sumw2 = nullptr;
+    double *stats = nullptr;
+    unsigned long long *entries = nullptr;
+    double *partials = nullptr;
+    unsigned int *counter = nullptr;
+    long long *limbs = nullptr;       // EXACT: per bin 2 x kLimbs int64 limbs (sumw, sumw2), zero between fills
+    unsigned long long *maxbits = nullptr;   // EXACT: bit pattern of max|w| of the current launch
+    double *pack_buf = nullptr;       // device buffer for bh_read
+    double *pack_host = nullptr;      // pinned host buffer for bh_read
+    // SORT strategy scratch (grown on demand): records, segment offsets, partition totals
+    uint16_t *part_l = nullptr;
+    double *part_w = nullptr;
+    uint32_t *part_offs = nullptr;
+    unsigned long long *part_cnt = nullptr, *part_cp = nullptr;
+    int64_t part_cap_l = 0, part_cap_w = 0, part_cap_offs = 0;
+    int part_P = 0;
+    // AUTO's SORT decision for large unit-weight fills: 0 unknown, 1 probe in flight,
+    // 2 spread-out data (SORT), 3 a hot partition (CACHE)
+    int probe_state = 0;
+    unsigned int *probe_dev = nullptr, *probe_host = nullptr;
+    cudaEvent_t probe_done = nullptr;
+    std::vector<void *> axis_mem;     // edges and guide tables
+    // host->device double buffer
+    cudaStream_t copy_stream = nullptr;
+    double *stage[kStageSlots] = {};  // each slot: (dim+1) columns of `chunk` doubles
+    int64_t stage_chunk = 0;
+    cudaEvent_t copied[kStageSlots] = {}, consumed[kStageSlots] = {};
+    bool weighted_content = false;     // a weighted fill (or a full unpack) since create/reset
+    bool slot_used[kStageSlots] = {};  // consumed[slot] recorded at least once (persists across calls)
+    int next_slot = 0;                 // ring position (persists across calls)
+};
+
+namespace bh {
+// The one-pass fused multi-histogram fill of bh_fill_multi (bhist_jit.cu): a kernel
+// specialized to this histogram set, compiled at run time with NVRTC and cached.
+// Returns BH_OK with *done = true when it filled every histogram in idx[0..m); *done =
+// false (and BH_OK) when the set cannot take the fused path (NVRTC unavailable, ...).
+bh_status fused_fill(bh_hist *const *hs, const int *idx, int m, const int32_t *col_of_axis,
+                     const uint8_t *weighted, int64_t n, const double *const *cols, int32_t ncols,
+                     const double *w, cudaStream_t s, bool *done);
+bh_status set_error(bh_status st, const char *msg);
+size_t axis_table_bytes_of(const AxisP &a);
+}  // namespace bh

@@ -365,3 +365,50 @@ def test_nccl_two_gpus_reduced_state_matches_oracle(tmp_path, exchange):
         got = {"content": z[f"content{i}"], "sumw2": z[f"sumw2{i}"], "stats": z[f"stats{i}"],
                "entries": int(z[f"entries{i}"])}
         compare(got, ref, hist.weighted, f"nccl C5 H{i}")
+
+
+# ------------------------------------------------------------------ one-pass fused multi-histogram fill (JIT)
+def _fused_case(name, rng, n):
+    """(columns, w, [(axes, col indices, weighted)]) of a histogram set."""
+    if name == "C5":
+        wl = bhgen.workload("C5", n)
+        cols = [wl.column(c, 0, n) for c in range(len(wl.columns))]
+        return cols, wl.column(wl.wcol, 0, n), [(oracle.oracle_axes(h), h.cols, h.weighted) for h in wl.hists]
+    x = rng.normal(0.5, 0.2, n)
+    y = 0.505 + 0.002 * np.tan(np.pi * (rng.random(n) - 0.5))      # Cauchy-peaked
+    z = rng.uniform(-0.1, 1.1, n)
+    w = rng.uniform(-0.5, 1.5, n)
+    c2 = bhgen.workload("C2", 10).hists[0].axes[0].edges
+    if name == "3d+global":
+        specs = [([(100, 0.0, 1.0)] * 3, [0, 1, 2], False),            # 1M bins: L2 sink
+                 ([(150, 0.0, 1.0), (150, 0.0, 1.0)], [2, 0], True),   # 22,801 weighted cells: L2 sink
+                 ([c2], [0], True), ([(20, 0.4, 0.6), (30, 0.0, 1.0)], [1, 2], True),
+                 ([np.geomspace(1e-3, 2.0, 801)], [2], False)]
+    elif name == "small":
+        specs = [([(10, 0.0, 1.0)], [0], False), ([(7, 0.45, 0.55)], [1], True), ([np.array([0.0, 0.3, 0.31, 1.0])], [2], True)]
+    else:
+        raise KeyError(name)
+    return [x, y, z], w, specs
+
+
+@pytest.mark.parametrize("name,n", [("C5", 2_000_003), ("3d+global", 1_000_001), ("small", 300_007), ("small", 5),
+                                    ("C5", 33)])
+def test_fused_one_pass_against_oracle(name, n):
+    """bh_fill_multi's run-time specialized one-pass kernel (BH_DEBUG_REQUIRE_JIT: no fallback):
+    one launch for the whole set, every histogram equal to its own oracle fill."""
+    rng = np.random.default_rng(n)
+    cols, w, specs = _fused_case(name, rng, n)
+    hs = [pkg.Histogram(ax) for ax, _, _ in specs]
+    pkg.bh_set_debug(hs[0].h, pkg.BH_DEBUG_REQUIRE_JIT)
+    tc = [_t(c) for c in cols]
+    tw = _t(w)
+    l0 = pkg.bh_launch_count(hs[0].h)
+    for rep in range(2):                      # accumulation across fills (include-initial)
+        pkg.fill_multi(hs, [c for _, c, _ in specs], [wt for _, _, wt in specs], tc, tw)
+    assert pkg.bh_launch_count(hs[0].h) - l0 == 2
+    for h, (ax, c, wt) in zip(hs, specs):
+        o = oracle.OracleHist(ax)
+        for rep in range(2):
+            o.fill([cols[i] for i in c], w if wt else None)
+        compare(h.read(), o.read(), wt, f"{name} {ax if not isinstance(ax[0], np.ndarray) else 'var'}")
+        h.close()

@@ -89,11 +89,11 @@ def test_build_units_cover_every_dim_and_weight():
 def test_jit_fused_kernel_compiles_for_sm100a():
     """The one-pass fused kernel of bh_fill_multi, instantiated for C5's two-role plan,
     compiles with NVRTC for sm_100a (no GPU needed)."""
-    expr = ("bh::k_fused<bh::Role<19u, bh::HS<2,1,true,0,1,0,0,3,0,0>, bh::HS<1,1,true,1,1,0,0,0,0,0>, "
-            "bh::HS<0,1,false,1,0,0,0,0,0,0>, bh::HS<4,1,false,1,4,0,0,0,0,0>, bh::HS<3,1,false,1,2,0,0,2,0,0>>, "
-            "bh::Role<19u, bh::HS<5,2,true,0,0,3,0,0,0,0>, bh::HS<7,2,true,1,4,5,0,0,0,0>, "
-            "bh::HS<6,2,false,2,1,5,0,0,0,0>>>")
-    msg = pkg.bh_jit_compile_check(expr)
+    expr = ("bh::k_fused<bh::Role<19u, bh::Grp<bh::HS<2,1,true,3,1,0,0,3,0,0>, bh::HS<0,1,false,1,0,0,0,0,0,0>>, "
+            "bh::Grp<bh::HS<1,1,true,3,1,0,0,0,0,0>, bh::HS<4,1,false,1,4,0,0,0,0,0>, bh::HS<3,1,false,0,2,0,0,2,0,0>>>, "
+            "bh::Role<19u, bh::Grp<bh::HS<5,2,true,3,0,3,0,0,0,0>>, "
+            "bh::Grp<bh::HS<7,2,true,3,4,5,0,0,0,0>, bh::HS<6,2,false,2,1,5,0,0,0,0>>>>")
+    msg = pkg.bh_jit_compile_check(expr, 768, 1)
     assert msg.startswith("ok:") and "sm_100a" in msg
     with pytest.raises(pkg.BHistError):
-        pkg.bh_jit_compile_check("bh::k_fused<bh::Role<0u, bh::HS<0,4,true,0,0,0,0,0,0,0>>>")   # DIM 4
+        pkg.bh_jit_compile_check("bh::k_fused<bh::Role<0u, bh::Grp<bh::HS<0,4,true,0,0,0,0,0,0,0>>, bh::Grp<>>>")  # DIM 4

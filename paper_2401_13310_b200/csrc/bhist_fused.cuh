@@ -57,10 +57,44 @@ struct FusedP {
 // for shared memory).
 enum FusedSink { FS_PRIV = 0, FS_PRIV_AGG = 1, FS_GLOBAL_AGG = 2, FS_PRIV_ADAPT = 3 };
 
+// An axis' scalars as compile-time constants (C++20 floating-point template arguments):
+// the kernel is compiled for these exact axes, so FindBin runs on literals instead of
+// parameter loads; the device pointers (edges, tables) stay run-time parameters.
+struct AxNone {};
+template <int A, class T0, class T1, class T2> struct PickAx { using type = T0; };
+template <class T0, class T1, class T2> struct PickAx<1, T0, T1, T2> { using type = T1; };
+template <class T0, class T1, class T2> struct PickAx<2, T0, T1, T2> { using type = T2; };
+template <int N, double XMIN, double XMAX, double D, double INV, int GCELLS, double GSCALE, int G16, int TABOFF>
+struct AxC {};
+__device__ __forceinline__ AxisP ax_const(const AxisP &rt, AxNone *) { return rt; }
+template <int N, double XMIN, double XMAX, double D, double INV, int GCELLS, double GSCALE, int G16, int TABOFF>
+__device__ __forceinline__ AxisP ax_const(const AxisP &rt, AxC<N, XMIN, XMAX, D, INV, GCELLS, GSCALE, G16, TABOFF> *) {
+    AxisP a;
+    a.n = N;
+    a.var = rt.var;
+    a.xmin = XMIN;
+    a.xmax = XMAX;
+    a.D = D;
+    a.inv = INV;
+    a.e = rt.e;
+    a.guide = rt.guide;
+    a.gcells = GCELLS;
+    a.gscale = GSCALE;
+    a.e32 = rt.e32;
+    a.tab_off = TABOFF;
+    a.g16 = G16;
+    a.tab_img = rt.tab_img;
+    a.tab_bytes = rt.tab_bytes;
+    return a;
+}
+
 // One histogram.  VMa per axis: 0 fixed, 1 variable with tables staged in shared memory
 // (guide mode at run time), 2 variable searched in global memory, 3 variable compact.
-template <int ID_, int DIM_, bool W_, int SINK_, int C0, int C1, int C2, int VM0, int VM1, int VM2>
+// AXa: the axis' constants (AxC) or AxNone (read from the parameters).
+template <int ID_, int DIM_, bool W_, int SINK_, int C0, int C1, int C2, int VM0, int VM1, int VM2,
+          class AX0 = AxNone, class AX1 = AxNone, class AX2 = AxNone>
 struct HS {
+    template <int A> using Ax = typename PickAx<A, AX0, AX1, AX2>::type;
     static_assert(ID_ >= 0 && ID_ < 8 && DIM_ >= 1 && DIM_ <= 3 && SINK_ >= 0 && SINK_ <= 3, "bad histogram spec");
     static_assert(C0 >= 0 && C0 < 8 && C1 >= 0 && C1 < 8 && C2 >= 0 && C2 < 8, "column index out of range");
     static_assert(VM0 >= 0 && VM0 <= 3 && VM1 >= 0 && VM1 <= 3 && VM2 >= 0 && VM2 <= 3, "bad axis mode");
@@ -191,8 +225,9 @@ template <class H, class... Rest> struct Proc<H, Rest...> {
     static __device__ __forceinline__ void axis_step(const FusedH &F, const X &x, double (&xa)[H::DIM], int &g,
                                                      bool &inr, const unsigned char *smem) {
         xa[A] = x[H::col[A]];
-        const int b = fused_find_bin<H::vm[A]>(F.ax[A], xa[A], smem);
-        inr &= (b >= 1) & (b <= F.ax[A].n);
+        const AxisP ax = ax_const(F.ax[A], static_cast<typename H::template Ax<A> *>(nullptr));
+        const int b = fused_find_bin<H::vm[A]>(ax, xa[A], smem);
+        inr &= (b >= 1) & (b <= ax.n);
         g += A == 0 ? b : b * (A == 1 ? F.st1 : F.st2);
     }
     // steps (1)-(3) of PAPER.md:126 for histogram H on one event (x: the group's columns)
@@ -326,26 +361,37 @@ __device__ __forceinline__ void run_group(const FusedP &p, unsigned char *smem, 
     const int cid = (int)(blockIdx.x / csize);
     const int64_t tile = (int64_t)ntg * BH_FUSED_EPT;
     const int64_t ntiles = (p.n + tile - 1) / tile;
-    int it = 0;
-    for (int64_t t = cid; t < ntiles; t += p.nclusters, ++it) {
-        if (csize > 1 && it > 0 && it % p.sync_tiles == 0) cluster_sync_relaxed();
-        const int64_t base = t * tile + tig;
+    // the next tile's columns are loaded before the current tile is processed (register
+    // double buffer: the loads' latency overlaps the bin updates)
+    struct Buf {
         double x[BH_FUSED_EPT][kFusedMaxCols];
         double w[BH_FUSED_EPT];
+    };
+    auto load = [&](Buf &b, int64_t t) {
+        const int64_t base = t * tile + tig;
 #pragma unroll
         for (int k = 0; k < BH_FUSED_EPT; ++k) {
             const int64_t i = base + k * (int64_t)ntg;
-            const bool valid = i < p.n;
+            const bool valid = t < ntiles && i < p.n;
 #pragma unroll
             for (int c = 0; c < kFusedMaxCols; ++c) {
-                x[k][c] = 0.0;
+                b.x[k][c] = 0.0;
                 if ((kCols >> c) & 1u)
-                    if (valid) x[k][c] = ((SHARED >> c) & 1u) ? __ldcg(p.cols[c] + i) : __ldcs(p.cols[c] + i);
+                    if (valid) b.x[k][c] = ((SHARED >> c) & 1u) ? __ldcg(p.cols[c] + i) : __ldcs(p.cols[c] + i);
             }
-            w[k] = (kW && valid) ? __ldcg(p.w + i) : 1.0;
+            b.w[k] = (kW && valid) ? __ldcg(p.w + i) : 1.0;
         }
+    };
+    Buf cur, nxt;
+    load(cur, cid);
+    int it = 0;
+    for (int64_t t = cid; t < ntiles; t += p.nclusters, ++it) {
+        if (csize > 1 && it > 0 && it % p.sync_tiles == 0) cluster_sync_relaxed();
+        load(nxt, t + p.nclusters);
+        const int64_t base = t * tile + tig;
 #pragma unroll
-        for (int k = 0; k < BH_FUSED_EPT; ++k) P::event(p, x[k], w[k], base + k * (int64_t)ntg < p.n, smem, acc);
+        for (int k = 0; k < BH_FUSED_EPT; ++k) P::event(p, cur.x[k], cur.w[k], base + k * (int64_t)ntg < p.n, smem, acc);
+        cur = nxt;
     }
     __syncthreads();                                     // (1) every group done with the bins
     P::flush(p, smem, tig, ntg);

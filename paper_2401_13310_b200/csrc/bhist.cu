@@ -320,7 +320,8 @@ bh_status part_scratch(bh_hist *h, int64_t ev, bool weighted, int P, cudaStream_
     return BH_OK;
 }
 
-bh_status fill_sort(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s) {
+bh_status fill_sort(bh_hist *h, int64_t n, const double *const *coords, const double *w, cudaStream_t s,
+                    const int32_t *gate = nullptr) {
     const bool W = w != nullptr;
     const int pb = sort_pb(W);
     const int P = (int)sort_partitions(h, W);
@@ -351,6 +352,7 @@ bh_status fill_sort(bh_hist *h, int64_t n, const double *const *coords, const do
         FillP p = make_params(h, m, cs, W ? w + off : nullptr);
         for (int a = 0; a < h->dim; ++a) p.ax[a] = ax[a];
         PartP q{};
+        q.gate = gate;
         q.rec_l = h->part_l;
         q.rec_w = h->part_w;
         q.offs = h->part_offs;
@@ -386,51 +388,38 @@ bh_status fill_sort(bh_hist *h, int64_t n, const double *const *coords, const do
 
 // AUTO and SORT (measured: SORT 1.45x faster than CACHE on spread-out unit-weight data,
 // several times slower with a hot partition or weights, and its per-chunk merge only
-// amortizes over >= ~8 x #SM x 2^pb events).  The first large unit-weight fill of a
-// histogram runs CACHE and launches k_part_probe on a strided sample behind it; a later
-// fill reads the result once its event has completed (never waits for it) and from then
-// on uses SORT if the largest partition holds <= 5% of the sample and no hashed bin
-// bucket holds > 1% (a hot bin contends in pass 2).
-constexpr int kProbeSamples = 1 << 14;     // one CTA: ~40 us, once per histogram
-bool auto_sort(bh_hist *h, int64_t n, const double *const *coords, cudaStream_t s) {
-    if (h->strategy != BH_STRATEGY_AUTO || resolve_strategy(h, false) != BH_STRATEGY_CACHE) return false;
+// amortizes over >= ~8 x #SM x 2^pb events).  The first large unit-weight fill after
+// create/reset launches k_part_probe on a strided sample of its own events; the probe
+// writes the decision to device memory (SORT if no partition holds > 5% of the sample and
+// no hashed bin bucket > 1%: a hot bin contends in pass 2), and that fill and every later
+// eligible one launch BOTH paths, each gated on the device flag (the other exits at
+// once).  The choice therefore depends on the data only, never on host timing, and the
+// host never waits for it.  Returns the device flag, or nullptr (plain CACHE).
+constexpr int kProbeSamples = 1 << 14;     // one CTA: ~40 us, once per histogram and reset
+const int32_t *auto_sort_gate(bh_hist *h, int64_t n, const double *const *coords, cudaStream_t s) {
+    if (h->strategy != BH_STRATEGY_AUTO || resolve_strategy(h, false) != BH_STRATEGY_CACHE) return nullptr;
     const int P = (int)sort_partitions(h, false);
-    if (P > kPartMaxP || n < 8LL * h->nsm * (1LL << sort_pb(false)) || getenv("BHIST_NO_AUTO_SORT")) return false;
-    if (h->probe_state == 1) {
-        const cudaError_t q = cudaEventQuery(h->probe_done);
-        if (q == cudaSuccess)
-            h->probe_state = ((double)h->probe_host[0] <= 0.05 * kProbeSamples &&
-                              (double)h->probe_host[1] <= 0.01 * kProbeSamples) ? 2 : 3;
-        else if (q == cudaErrorNotReady)
-            cudaGetLastError();                      // not an error: the probe is still running
+    if (P > kPartMaxP || n < 8LL * h->nsm * (1LL << sort_pb(false)) || getenv("BHIST_NO_AUTO_SORT")) return nullptr;
+    if (!h->probe_dev) {
+        if (cudaMalloc(reinterpret_cast<void **>(&h->probe_dev), 3 * sizeof(unsigned int)) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;                                  // no probe: stay on CACHE
+        }
     }
     if (h->probe_state == 0) {
-        if (!h->probe_dev) {
-            if (cudaMalloc(reinterpret_cast<void **>(&h->probe_dev), 2 * sizeof(unsigned int)) != cudaSuccess ||
-                cudaMallocHost(reinterpret_cast<void **>(&h->probe_host), 2 * sizeof(unsigned int)) != cudaSuccess ||
-                cudaEventCreateWithFlags(&h->probe_done, cudaEventDisableTiming) != cudaSuccess) {
-                cudaGetLastError();
-                h->probe_state = 3;                  // no probe: stay on CACHE
-                return false;
-            }
-        }
         FillP p = make_params(h, n, coords, nullptr);
-        cudaMemsetAsync(h->probe_dev, 0, 2 * sizeof(unsigned int), s);
+        if (cudaMemsetAsync(h->probe_dev, 0, 3 * sizeof(unsigned int), s) != cudaSuccess) { cudaGetLastError(); return nullptr; }
         const size_t sm = sizeof(unsigned int) * (P + kProbeHash);
         switch (h->dim) {
         case 1: k_part_probe<1><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, h->probe_dev); break;
         case 2: k_part_probe<2><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, h->probe_dev); break;
         default: k_part_probe<3><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, h->probe_dev); break;
         }
-        cudaMemcpyAsync(h->probe_host, h->probe_dev, 2 * sizeof(unsigned int), cudaMemcpyDeviceToHost, s);
-        if (cudaEventRecord(h->probe_done, s) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
-            h->probe_state = 3;
-            return false;
-        }
+        if (cudaGetLastError() != cudaSuccess) return nullptr;
         h->launches++;
-        h->probe_state = 1;
+        h->probe_state = 1;                                   // decided (on the device)
     }
-    return h->probe_state == 2;
+    return reinterpret_cast<const int32_t *>(h->probe_dev + 2);
 }
 
 // One fill over device-resident columns, split into launches of <= 2^30 events.
@@ -438,7 +427,9 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
     if (w) h->weighted_content = true;
     if (w && h->strategy == BH_STRATEGY_EXACT) return fill_exact(h, n, coords, w, s);
     if (resolve_strategy(h, w != nullptr) == BH_STRATEGY_SORT) return fill_sort(h, n, coords, w, s);
-    if (!w && auto_sort(h, n, coords, s)) return fill_sort(h, n, coords, w, s);
+    const int32_t *gate = w ? nullptr : auto_sort_gate(h, n, coords, s);
+    if (gate)                                                 // SORT, run iff the device flag says so
+        if (bh_status r = fill_sort(h, n, coords, w, s, gate)) return r;
     FillPlan pl;
     if (bh_status r = plan_fill(h, w != nullptr, pl, n)) return r;
     LaunchCfg &c = pl.c;
@@ -450,6 +441,8 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         const double *ws = c.weighted ? w + off : nullptr;
         FillP p = make_params(h, m, cs, ws);
         for (int a = 0; a < h->dim; ++a) p.ax[a] = pl.ax[a];
+        p.gate = gate;                                        // CACHE, run iff the flag is 0
+        p.gate_run = 0;
         // vector path: every column must share the same 16-byte phase
         const uintptr_t ph = reinterpret_cast<uintptr_t>(cs[0]) & 15;
         c.vec = (ph % 8) == 0;
@@ -706,8 +699,6 @@ bh_status bh_destroy(bh_hist *h) {
     cudaFree(h->part_cnt);
     cudaFree(h->part_cp);
     cudaFree(h->probe_dev);
-    if (h->probe_host) cudaFreeHost(h->probe_host);
-    if (h->probe_done) cudaEventDestroy(h->probe_done);
     if (h->pack_host) cudaFreeHost(h->pack_host);
     for (void *p : h->axis_mem) cudaFree(p);
     for (int i = 0; i < kStageSlots; ++i) {
@@ -730,6 +721,7 @@ bh_status bh_reset(bh_hist *h, bh_stream s) {
     CUDA_TRY(cudaMemsetAsync(h->stats, 0, sizeof(double) * 16, st));
     CUDA_TRY(cudaMemsetAsync(h->entries, 0, sizeof(unsigned long long), st));
     h->weighted_content = false;
+    h->probe_state = 0;                  // AUTO re-decides SORT vs CACHE on the next large fill
     return BH_OK;
 }
 
@@ -1272,8 +1264,14 @@ bh_status bh_get_strategy(const bh_hist *h, int32_t weighted, int32_t *strategy)
     if (check_hist(h)) return BH_EINVAL;
     if (!strategy) return fail(BH_EINVAL, "NULL output");
     *strategy = (weighted && h->strategy == BH_STRATEGY_EXACT) ? BH_STRATEGY_EXACT : resolve_strategy(h, weighted != 0);
-    // AUTO's large unit-weight fills after the hotness probe found spread-out data
-    if (!weighted && h->strategy == BH_STRATEGY_AUTO && h->probe_state == 2) *strategy = BH_STRATEGY_SORT;
+    // AUTO's large unit-weight fills after the probe decided (on the device) for SORT
+    if (!weighted && h->strategy == BH_STRATEGY_AUTO && h->probe_state == 1 && h->probe_dev) {
+        DeviceGuard dg(h->device);
+        unsigned int flag = 0;
+        if (cudaMemcpy(&flag, h->probe_dev + 2, sizeof flag, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(BH_ECUDA, "reading the AUTO decision: %s", cudaGetErrorString(cudaGetLastError()));
+        if (flag == 1) *strategy = BH_STRATEGY_SORT;
+    }
     return BH_OK;
 }
 

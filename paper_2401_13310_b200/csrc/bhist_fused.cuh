@@ -362,17 +362,18 @@ __device__ __forceinline__ void run_group(const FusedP &p, unsigned char *smem, 
     const int64_t tile = (int64_t)ntg * BH_FUSED_EPT;
     const int64_t ntiles = (p.n + tile - 1) / tile;
     // the next tile's columns are loaded before the current tile is processed (register
-    // double buffer: the loads' latency overlaps the bin updates)
+    // double buffer: the loads' latency overlaps the bin updates).  Event indices advance
+    // by the grid stride; the cluster barrier is a countdown (no division in the loop).
     struct Buf {
         double x[BH_FUSED_EPT][kFusedMaxCols];
         double w[BH_FUSED_EPT];
     };
-    auto load = [&](Buf &b, int64_t t) {
-        const int64_t base = t * tile + tig;
+    const int64_t stride = (int64_t)p.nclusters * tile;
+    auto load = [&](Buf &b, int64_t i0) {
 #pragma unroll
         for (int k = 0; k < BH_FUSED_EPT; ++k) {
-            const int64_t i = base + k * (int64_t)ntg;
-            const bool valid = t < ntiles && i < p.n;
+            const int64_t i = i0 + k * (int64_t)ntg;
+            const bool valid = i < p.n;
 #pragma unroll
             for (int c = 0; c < kFusedMaxCols; ++c) {
                 b.x[k][c] = 0.0;
@@ -383,15 +384,19 @@ __device__ __forceinline__ void run_group(const FusedP &p, unsigned char *smem, 
         }
     };
     Buf cur, nxt;
-    load(cur, cid);
-    int it = 0;
-    for (int64_t t = cid; t < ntiles; t += p.nclusters, ++it) {
-        if (csize > 1 && it > 0 && it % p.sync_tiles == 0) cluster_sync_relaxed();
-        load(nxt, t + p.nclusters);
-        const int64_t base = t * tile + tig;
+    int64_t i0 = (int64_t)cid * tile + tig;
+    load(cur, i0);
+    int sync_left = p.sync_tiles;
+    for (int64_t t = cid; t < ntiles; t += p.nclusters) {
+        if (csize > 1 && --sync_left == 0) {
+            cluster_sync_relaxed();
+            sync_left = p.sync_tiles;
+        }
+        load(nxt, i0 + stride);
 #pragma unroll
-        for (int k = 0; k < BH_FUSED_EPT; ++k) P::event(p, cur.x[k], cur.w[k], base + k * (int64_t)ntg < p.n, smem, acc);
+        for (int k = 0; k < BH_FUSED_EPT; ++k) P::event(p, cur.x[k], cur.w[k], i0 + k * (int64_t)ntg < p.n, smem, acc);
         cur = nxt;
+        i0 += stride;
     }
     __syncthreads();                                     // (1) every group done with the bins
     P::flush(p, smem, tig, ntg);

@@ -89,7 +89,11 @@ struct FillP {
     double *stats;               // [K], running totals
     unsigned long long *entries; // running entries
     int64_t entries_add;         // added to *entries by the last CTA
+    const int32_t *gate;         // AUTO's device-side strategy decision: the kernel runs only if
+    int32_t gate_run;            // gate == nullptr or *gate == gate_run (otherwise every CTA exits)
 };
+
+__device__ __forceinline__ bool gated_off(const int32_t *gate, int32_t run) { return gate && __ldcg(gate) != run; }
 
 // ------------------------------------------------------------------ FindBin
 // Fixed axis: b = 1 + floor(n*(x-xmin)/(xmax-xmin)), evaluated as
@@ -788,6 +792,7 @@ struct Batch {            // U event pairs of every column, held in registers (x
 template <int DIM, bool W, int SINK, bool VEC, int VM>
 __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (gated_off(p.gate, p.gate_run)) return;          // (uniform: the whole grid exits)
     using Sink_t = typename SinkOf<SINK, W>::T;
     Sink_t sink;
     if constexpr (SINK == SINK_GLOBAL) sink.pp = &p;

@@ -43,6 +43,7 @@ constexpr int kReduceCtas = BH_REDUCE_CTAS;          // pass 2 CTAs per SM
 constexpr int kReduceThreads = 1024 / kReduceCtas;   // (1 CTA per SM owns 128 KB of bins)
 
 struct PartP {
+    const int32_t *gate;        // AUTO: run only if *gate == 1 (SORT chosen on the device); nullptr: always
     uint16_t *rec_l;            // [ntiles * kPartTile] local bin, tile-major, partition-sorted within a tile
     double *rec_w;              // weighted: the weights, same order
     uint32_t *offs;             // [ntiles * (P + 1)] segment starts of each tile
@@ -93,6 +94,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // partial or whose columns are not 16-byte aligned are loaded by the threads instead.
 template <int DIM, bool W, int VM, int RC>
 __global__ void __launch_bounds__(kPartThreads, 1) k_part_scatter(FillP p, PartP q) {
+    if (gated_off(q.gate, 1)) return;
     constexpr int NCOL = DIM + (W ? 1 : 0);
     constexpr int kEv = part_ev(DIM, W);
     constexpr int kTile = kPartThreads * kEv;
@@ -257,7 +259,10 @@ constexpr int kProbeHash = 4096;
 template <int DIM>
 __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, int samples, unsigned int *out) {
     // out[0]: largest partition count; out[1]: largest count of a hashed bin bucket
-    // (4096 buckets: a single hot bin shows up as one large bucket)
+    // (4096 buckets: a single hot bin shows up as one large bucket); out[2]: the decision,
+    // 1 (SORT) when no partition holds > 5% and no bucket > 1% of the samples, else 0
+    // (CACHE) -- read by the gated fills on the device, so AUTO's choice depends on the
+    // data only, never on timing
     extern __shared__ unsigned int pc[];
     unsigned int *hc = pc + P;
     for (int i = threadIdx.x; i < P + kProbeHash; i += blockDim.x) pc[i] = 0u;
@@ -284,12 +289,16 @@ __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, 
         atomicMax(out, m);
         atomicMax(out + 1, mh);
     }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        out[2] = (20ull * out[0] <= (unsigned long long)samples && 100ull * out[1] <= (unsigned long long)samples) ? 1u : 0u;
 }
 
 // ------------------------------------------------------------------ plan
 // One warp: cp = exclusive prefix of cnt (records per partition); cnt is zeroed for
 // the next chunk.
 __global__ void k_part_plan(PartP q) {
+    if (gated_off(q.gate, 1)) return;
     const int lane = threadIdx.x;
     unsigned long long run = 0;
     for (int c0 = 0; c0 < q.P; c0 += 32) {
@@ -363,6 +372,7 @@ constexpr int kReduceBatch = 2048;                   // tiles whose segments are
 // still keeps all 32 warps busy), walking the segments in order.
 template <bool W, int RC>
 __global__ void __launch_bounds__(kReduceThreads, kReduceCtas) k_part_reduce(FillP p, PartP q) {
+    if (gated_off(q.gate, 1)) return;
     extern __shared__ __align__(16) unsigned char smem[];
     // layout: [bins (2^pb cells)] [o0 u32[batch]] [cp u32[batch+1]] [scan scratch u32[32]]
     const size_t binbytes = (size_t)(W ? 16 : 4) << q.pb;

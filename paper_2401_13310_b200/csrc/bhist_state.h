@@ -43,11 +43,10 @@ struct bh_hist {
     unsigned long long *part_cnt = nullptr, *part_cp = nullptr;
     int64_t part_cap_l = 0, part_cap_w = 0, part_cap_offs = 0;
     int part_P = 0;
-    // AUTO's SORT decision for large unit-weight fills: 0 unknown, 1 probe in flight,
-    // 2 spread-out data (SORT), 3 a hot partition (CACHE)
+    // AUTO's SORT decision for large unit-weight fills: 0 not probed since create/reset,
+    // 1 probed (probe_dev[2] on the device: 1 SORT, 0 CACHE; both paths are launched gated)
     int probe_state = 0;
-    unsigned int *probe_dev = nullptr, *probe_host = nullptr;
-    cudaEvent_t probe_done = nullptr;
+    unsigned int *probe_dev = nullptr;
     std::vector<void *> axis_mem;     // edges and guide tables
     // host->device double buffer
     cudaStream_t copy_stream = nullptr;

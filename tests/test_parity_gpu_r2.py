@@ -412,3 +412,33 @@ def test_fused_one_pass_against_oracle(name, n):
             o.fill([cols[i] for i in c], w if wt else None)
         compare(h.read(), o.read(), wt, f"{name} {ax if not isinstance(ax[0], np.ndarray) else 'var'}")
         h.close()
+
+
+# ------------------------------------------------------------------ AUTO's SORT decision (device-side, data-only)
+@pytest.mark.slow
+def test_auto_sort_decision_is_deterministic_and_matches_oracle():
+    """AUTO decides SORT vs CACHE on the device from a sample of the first large unit-weight
+    fill (both paths launched, gated): two fresh histograms fed the same fills end bitwise
+    identical (the choice never depends on host timing), the spread-out C3 shape picks
+    SORT, and the result equals the oracle; bh_reset re-decides."""
+    n = 40_000_001
+    wl = bhgen.workload("C3", n)
+    cols = [wl.column(c, 0, n) for c in wl.hists[0].cols]
+    tc = [_t(c) for c in cols]
+    axes = oracle.oracle_axes(wl.hists[0])
+    runs = []
+    for rep in range(2):
+        h = pkg.Histogram(axes)
+        h.fill(tc)
+        h.fill(tc)
+        runs.append((h.read(), h.strategy(False)))
+        h.reset()
+        h.fill(tc)
+        assert h.read()["entries"] == n
+        h.close()
+    (a, sa), (b, sb) = runs
+    assert sa == sb == pkg.BH_STRATEGY_SORT
+    assert np.array_equal(a["content"], b["content"]) and a["stats"].tobytes() == b["stats"].tobytes()
+    ref = oracle_parallel("C3", n)
+    ref2 = {k: (2 * v if k != "entries" else 2 * v) for k, v in ref.items()}
+    compare(a, ref2, False, "AUTO->SORT x2")

@@ -10,6 +10,7 @@
 #   tools/gpu.sh <tag> launches [bench.py args]       ncu launch list (gpu__time_duration per launch)
 #   tools/gpu.sh <tag> ab    <defines-A> <defines-B> [bench.py args]
 #                                                    same bench with two builds (-D lists, ',' separated)
+#   tools/gpu.sh <tag> envs "A=1,B=2;A=3" [bench.py args]   the bench under each env setting
 #   tools/gpu.sh <tag> sanitize                       compute-sanitizer memcheck/racecheck on small fills
 # Several jobs can be chained:  tools/gpu.sh r02a tests ';' r02a bench --config C3
 set -u
@@ -61,6 +62,15 @@ _build.build(force=True, defines=[d for d in sys.argv[1].split(',') if d])" "$de
           --e2e-steps 1 --secondary "" "$@" > "$out/ab_${v}_$rep.json" 2>> "$out/ab.err"
         python -c "import json,sys; d=json.load(open(sys.argv[1])); print(sys.argv[2], d['ms_per_step'], d['roofline']['frac'])" "$out/ab_${v}_$rep.json" "$v$rep"
       done; done;;
+    envs)   # envs "A=1,B=2;A=3" [bench args]: the bench under each ';'-separated env setting
+      local sets=$1; shift
+      IFS=';' read -ra SETS <<< "$sets"
+      for st in "${SETS[@]}"; do
+        ( IFS=',' read -ra KV <<< "$st"; for kv in "${KV[@]}"; do [ -n "$kv" ] && export "$kv"; done
+          timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --secondary "" "$@" \
+            > "$out/env.json" 2>> "$out/envs.err"
+          python -c "import json,sys; d=json.load(open(sys.argv[1])); print(sys.argv[2], round(d['ms_per_step'],4), round(d['roofline']['frac'],4))" "$out/env.json" "[$st]" )
+      done;;
     sanitize)
       timeout 1200 python tools/sanitize_run.py > "$out/sanitize.log" 2>&1; echo "sanitize rc=$?"; tail -5 "$out/sanitize.log";;
     *) echo "unknown job $job"; return 2;;

@@ -382,27 +382,34 @@ __device__ __forceinline__ bool cas128_shared(uint32_t addr, unsigned long long 
     return ol == cl && oh == ch;
 }
 
-// (sumw, sumw2) += (w, w*w) on one 16-byte shared-memory cell with a single 128-bit
-// CAS (ATOMS.CAS.128): one load + one CAS per event instead of two of each (smem
-// float64 add has no native atomic on sm_100a; nvcc's atomicAdd(double*) is a CAS loop).
-__device__ __forceinline__ void add2_shared(double2 *cell, double w, double w2) {
-    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(cell);
-    double2 cur = *cell;
-    while (true) {
-        unsigned long long ol, oh;
-        const double nx = cur.x + w, ny = cur.y + w2;
-        if (cas128_shared(addr, __double_as_longlong(cur.x), __double_as_longlong(cur.y), __double_as_longlong(nx),
-                          __double_as_longlong(ny), ol, oh))
-            break;
-        cur = make_double2(__longlong_as_double(ol), __longlong_as_double(oh));
-    }
+__device__ __forceinline__ void exch128_shared(uint32_t addr, unsigned long long il, unsigned long long ih,
+                                               unsigned long long &ol, unsigned long long &oh) {
+    asm volatile(
+        "{\n .reg .b128 d, v;\n mov.b128 v, {%2, %3};\n atom.shared.exch.b128 d, [%4], v;\n mov.b128 {%0, %1}, d;\n}"
+        : "=l"(ol), "=l"(oh)
+        : "l"(il), "l"(ih), "r"(addr)
+        : "memory");
 }
 
-// Same, returning how many CAS attempts lost (contention telemetry for PrivSink).
+// (sumw, sumw2) += (w, w*w) on one 16-byte shared-memory cell (smem float64 add has no
+// native atomic on sm_100a; nvcc's atomicAdd(double*) is a CAS loop).  Returns how many
+// rounds collided with another thread's add (contention telemetry for PrivSink).
+//
+// Take-and-return with 128-bit exchanges (ATOMS.EXCH.128), no load and no compare: take the
+// cell's pair (leaving +0,+0), add, exchange the sum back; if that exchange brought back a
+// pair another thread deposited in the meantime, take the cell again, merge, and repeat.
+// Every exchange is atomic, so (cell + the pairs threads hold) always equals the sum of the
+// adds made so far, and an add ends when its sum lands in an empty cell (a deposit of +0,+0
+// carries nothing).  Measured on 10,002 random cells (tools/microbench/mb4.cu, 1024
+// threads/SM): 0.93 adds/clk/SM vs 0.64 for a load + 128-bit CAS loop, and 99 vs 1.2 G
+// adds/s when a quarter of the adds hit one cell (a lost CAS re-reads and retries; a
+// deposit is merged by whoever finds it).
+// BH_SINK_CAS (A/B builds): the round-1 load + ATOMS.CAS.128 loop.
 __device__ __forceinline__ int add2_shared_count(double2 *cell, double w, double w2) {
     const uint32_t addr = (uint32_t)__cvta_generic_to_shared(cell);
-    double2 cur = *cell;
     int lost = 0;
+#ifdef BH_SINK_CAS
+    double2 cur = *cell;
     while (true) {
         unsigned long long ol, oh;
         if (cas128_shared(addr, __double_as_longlong(cur.x), __double_as_longlong(cur.y),
@@ -411,7 +418,23 @@ __device__ __forceinline__ int add2_shared_count(double2 *cell, double w, double
         ++lost;
         cur = make_double2(__longlong_as_double(ol), __longlong_as_double(oh));
     }
+#else
+    unsigned long long l, h;
+    exch128_shared(addr, 0ull, 0ull, l, h);
+    double s1 = __longlong_as_double(l) + w, s2 = __longlong_as_double(h) + w2;
+    while (true) {
+        exch128_shared(addr, __double_as_longlong(s1), __double_as_longlong(s2), l, h);
+        if ((l | h) == 0ull) return lost;
+        ++lost;
+        unsigned long long l2, h2;
+        exch128_shared(addr, 0ull, 0ull, l2, h2);
+        s1 = __longlong_as_double(l) + __longlong_as_double(l2);
+        s2 = __longlong_as_double(h) + __longlong_as_double(h2);
+    }
+#endif
 }
+
+__device__ __forceinline__ void add2_shared(double2 *cell, double w, double w2) { (void)add2_shared_count(cell, w, w2); }
 
 // Shared-memory layout of the PRIV sink: unit -> uint32 count[G];
 // weighted -> double2 (sumw, sumw2)[G].
@@ -719,9 +742,7 @@ struct CacheSink {
     __device__ __forceinline__ void put(int g, double s1, double s2) {
         const int sl = lookup((uint32_t)g);
         if (sl >= 0) {
-            double *d = reinterpret_cast<double *>(vals);
-            atomicAdd(d + sl, s1);
-            atomicAdd(d + S + sl, s2);
+            add2_shared(reinterpret_cast<double2 *>(vals) + sl, s1, s2);     // (sumw, sumw2) cell
         } else {
             atomicAdd(pp->sumw + g, s1);
             atomicAdd(pp->sumw2 + g, s2);
@@ -733,9 +754,9 @@ struct CacheSink {
             const uint32_t k = keys[i];
             if (k == kEmpty) continue;
             if (W) {
-                const double *d = reinterpret_cast<const double *>(vals);
-                if (d[i] != 0.0) atomicAdd(p.sumw + k, d[i]);
-                if (d[S + i] != 0.0) atomicAdd(p.sumw2 + k, d[S + i]);
+                const double2 d = reinterpret_cast<const double2 *>(vals)[i];
+                if (d.x != 0.0) atomicAdd(p.sumw + k, d.x);
+                if (d.y != 0.0) atomicAdd(p.sumw2 + k, d.y);
             } else {
                 const uint32_t v = reinterpret_cast<const uint32_t *>(vals)[i];
                 if (v) atomicAdd(p.count + k, (unsigned long long)v);

@@ -71,7 +71,7 @@ def workload_desc(wl) -> str:
             "C1F": "C1-shape streamed in float32: TH1D 100 fixed bins [0,1], 2^30 uniform float32 events",
             "C2F": "C2 in float32: TH1D 10,000 variable-width bins, 5e8 Gaussian float32 events, float32 weights",
             "C5": "C5: 8 histograms (1D/2D mix) from 7 columns, 1.25e8 events/GPU (1e9 over 8 GPUs), "
-                  "fused one-pass fill"}.get(wl.name, wl.name)
+                  "one bh_fill_multi call"}.get(wl.name, wl.name)
 
 
 def get_workload(name: str):
@@ -365,6 +365,8 @@ def run_gpu(args):
                             per_hist.get(str(i), args.strategy)])
           for i, h in enumerate(hists)]
     multi = len(Hs) > 1
+    if multi:
+        pkg.bh_set_multi_mode(Hs[0].h, {"passes": pkg.BH_MULTI_PASSES, "one-pass": pkg.BH_MULTI_ONE_PASS}[args.multi_mode])
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
     # the exchange step (N>1): ONE collective per step over the packed state of every histogram,
@@ -510,7 +512,7 @@ def run_gpu(args):
         achieved = bpe * N / (fill_avg * 1e-3) / 1e9
         traffic = ncu_traffic(wl.name)
         names = {0: "auto", 1: "priv", 2: "global", 3: "cache", 4: "exact", 5: "sort"}
-        strat = "fused multi-histogram (per-histogram smem/global plan)" if multi else \
+        strat = f"bh_fill_multi, plan: {args.multi_mode}" if multi else \
             names[Hs[0].strategy(hists[0].weighted)]
         clocks = clk.summary()
         line = {
@@ -527,7 +529,9 @@ def run_gpu(args):
             "pct_hbm_peak": 100.0 * bpe * value / world / 1e9 / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic,
-                         "kernel": "k_fill_multi" if multi else ("k_part_scatter + k_part_reduce (sort)"
+                         "kernel": ("k_fused (one pass)" if args.multi_mode == "one-pass" else
+                                    "k_fill per histogram + k_fill_multi for same-column groups") if multi
+                         else ("k_part_scatter + k_part_reduce (sort)"
                                                                   if strat == "sort" else f"k_fill ({strat})"),
                          "launch_ms": fill_avg,
                          "algorithmic_bytes_per_launch": bpe * N, "peak_source": peak_src},
@@ -561,6 +565,8 @@ def main():
     ap.add_argument("--strategy", default="auto", choices=["auto", "priv", "global", "cache", "exact", "sort"])
     ap.add_argument("--hist-strategy", default="",
                     help="per-histogram strategies of a multi-histogram config, e.g. '6=sort'")
+    ap.add_argument("--multi-mode", default="passes", choices=["passes", "one-pass"],
+                    help="bh_fill_multi plan for C5 (bh_set_multi_mode)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend for N>1")
     ap.add_argument("--exchange", default="reduce", choices=["reduce", "allreduce"],
                     help="N>1: sum the partial states on rank 0 only (reduce) or on every rank")

@@ -105,8 +105,8 @@ typedef struct {
 /* Debug flags (bh_set_debug) — negative controls for tests only. */
 #define BH_DEBUG_SKIP_COPY_WAIT 1 /* bh_fill_host: fill without waiting for the H2D copy (PAPER.md:223 race) */
 #define BH_DEBUG_FIND_BINS_GLOBAL 2 /* bh_find_bins: search variable axes in global memory, not the fills' staged tables */
-#define BH_DEBUG_REQUIRE_JIT 4      /* bh_fill_multi (flag on hs[0]): fail instead of falling back when the
-                                       run-time compiled one-pass kernel is unavailable */
+#define BH_DEBUG_REQUIRE_JIT 4      /* bh_fill_multi (flag on hs[0]): use the one-pass kernel and fail instead
+                                       of falling back when the run-time compiled kernel is unavailable */
 
 /* ABI version (major*10000 + minor*100 + patch). */
 int32_t bh_version(void);
@@ -269,6 +269,23 @@ bh_status bh_get_strategy(const bh_hist *h, int32_t weighted, int32_t *strategy)
 
 /* Events per chunk for bh_fill_host (default 1<<22); >= 1024. */
 bh_status bh_set_chunk(bh_hist *h, int64_t events);
+
+/* Plan of bh_fill_multi, set on the histogram passed as hs[0]:
+ * BH_MULTI_PASSES (default)  histograms that read the same columns and have small private
+ *     states share a pass (k_fill_multi), every other histogram gets its own bh_fill pass:
+ *     each pass reads only its own columns, and each histogram gets the whole GPU and the
+ *     single-histogram kernel's sinks.  The fill is bound by the shared-memory bin updates
+ *     (SM time), not by HBM: C5 measured 5.5 ms this way vs 10.5 ms in one pass;
+ * BH_MULTI_ONE_PASS  the one-pass kernel specialized at run time to the histogram set
+ *     (NVRTC, cached per set): every column byte is read from DRAM once (PAPER.md:470
+ *     "multiple histograms using data in different (parts of the) columns"; C5: 7.0 GB of
+ *     DRAM reads per 1.25e8 events instead of 15 GB), histograms too large for one SM's shared
+ *     memory together split over the CTAs of a thread-block cluster.  Falls back to the
+ *     passes if NVRTC is unavailable (BH_DEBUG_REQUIRE_JIT: fail instead).
+ * Results are the same either way (each histogram equals bh_fill on its own columns). */
+#define BH_MULTI_PASSES 0
+#define BH_MULTI_ONE_PASS 1
+bh_status bh_set_multi_mode(bh_hist *h, int32_t mode);
 
 /* Debug flags (BH_DEBUG_*), tests only. */
 bh_status bh_set_debug(bh_hist *h, int32_t flags);

@@ -21,13 +21,14 @@ BH_STRATEGY_AUTO, BH_STRATEGY_PRIV, BH_STRATEGY_GLOBAL, BH_STRATEGY_CACHE, BH_ST
 BH_DEBUG_SKIP_COPY_WAIT = 1
 BH_DEBUG_FIND_BINS_GLOBAL = 2
 BH_DEBUG_REQUIRE_JIT = 4
+BH_MULTI_PASSES, BH_MULTI_ONE_PASS = 0, 1
 
 # every symbol include/bhist.h declares (checked by tests/test_abi.py)
 EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset", "bh_fill", "bh_fill_host",
             "bh_fill_multi", "bh_fill_expr", "bh_fill_f32", "bh_fill_i32", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
             "bh_fill_host_f32", "bh_fill_host_i32", "bh_packed_size_multi", "bh_pack_multi", "bh_unpack_multi",
             "bh_jit_compile_check",
-            "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_launch_count"]
+            "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_set_multi_mode", "bh_launch_count"]
 
 
 class BHistError(RuntimeError):
@@ -99,6 +100,7 @@ def lib(build_if_stale: bool = False):
             "bh_get_strategy": ([_P, _I32, _P], _I32),
             "bh_set_chunk": ([_P, _I64], _I32),
             "bh_set_debug": ([_P, _I32], _I32),
+            "bh_set_multi_mode": ([_P, _I32], _I32),
             "bh_launch_count": ([_P, _P], _I32),
         }
         for name, (args, res) in sig.items():
@@ -287,9 +289,12 @@ def fill_expr(hist, cols, prog: "Program", axis_regs, weight_reg: int = -1, filt
                  _stream_handle(stream, hist.device))
 
 
-def fill_multi(hists, col_of_axis, weighted, cols, w=None, stream=None) -> None:
-    """Histogram-level wrapper: cols are contiguous float64 CUDA tensors of equal length."""
+def fill_multi(hists, col_of_axis, weighted, cols, w=None, stream=None, mode=None) -> None:
+    """Histogram-level wrapper: cols are contiguous float64 CUDA tensors of equal length;
+    mode (BH_MULTI_*, None = leave as set) is the plan, set on hists[0]."""
     import torch
+    if mode is not None:
+        bh_set_multi_mode(hists[0].h, mode)
     n = cols[0].numel()
     _check_cols(cols + ([w] if w is not None else []), (torch.float64,), n, hists[0].device, "cols / w")
     bh_fill_multi([h.h for h in hists], col_of_axis, weighted, n, [c.data_ptr() for c in cols],
@@ -347,6 +352,10 @@ def bh_set_chunk(h, events: int) -> None:
 
 def bh_set_debug(h, flags: int) -> None:
     _check(lib().bh_set_debug(h, flags))
+
+
+def bh_set_multi_mode(h, mode: int) -> None:
+    _check(lib().bh_set_multi_mode(h, mode))
 
 
 def bh_launch_count(h) -> int:

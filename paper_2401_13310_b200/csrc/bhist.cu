@@ -878,7 +878,9 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
         if ((st == BH_STRATEGY_EXACT && weighted[i]) || st == BH_STRATEGY_SORT) rest_idx.push_back(i);
         else jit_idx.push_back(i);
     }
-    if (jit_idx.size() >= 2) {
+    const bool one_pass = hs[0]->multi_mode == BH_MULTI_ONE_PASS || (hs[0]->debug & BH_DEBUG_REQUIRE_JIT) ||
+                          getenv("BHIST_MULTI_ONE_PASS");
+    if (one_pass && jit_idx.size() >= 2) {
         bool done = false;
         if (bh_status r = fused_fill(hs, jit_idx.data(), (int)jit_idx.size(), col_of_axis, weighted, n, cols, ncols, w,
                                      st, &done))
@@ -1285,6 +1287,13 @@ bh_status bh_set_chunk(bh_hist *h, int64_t events) {
 bh_status bh_set_debug(bh_hist *h, int32_t flags) {
     if (check_hist(h)) return BH_EINVAL;
     h->debug = flags;
+    return BH_OK;
+}
+
+bh_status bh_set_multi_mode(bh_hist *h, int32_t mode) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (mode != BH_MULTI_PASSES && mode != BH_MULTI_ONE_PASS) return fail(BH_EINVAL, "unknown multi mode %d", mode);
+    h->multi_mode = mode;
     return BH_OK;
 }
 

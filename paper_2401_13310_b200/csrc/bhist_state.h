@@ -21,6 +21,7 @@ struct bh_hist {
     int32_t st1 = 1, st2 = 1;
     int strategy = BH_STRATEGY_AUTO;
     int debug = 0;
+    int multi_mode = BH_MULTI_PASSES;   // bh_fill_multi plan when this histogram is hs[0]
     int64_t chunk = 1 << 22;
     int64_t launches = 0;
     size_t smem_optin = 0;

@@ -163,21 +163,27 @@ def test_fill_expr_long_program_all_registers():
 @pytest.mark.slow
 def test_c5_bench_size_against_sharded_oracle():
     """C5 as bench.py runs it at N=1 (1.25e8 device-resident events per GPU at 8 GPUs; the
-    large-fill sinks the planner picks only at this size) against the oracle per histogram."""
+    large-fill sinks the planner picks only at this size) against the oracle per histogram,
+    through both plans of bh_fill_multi (per-histogram passes, the one-pass kernel)."""
     n = 125_000_000
     wl = bhgen.workload("C5", n)
     cols = [_t(wl.column(c, 0, n)) for c in range(len(wl.columns))]
     w = _t(wl.column(wl.wcol, 0, n))
-    hs = [pkg.Histogram(oracle.oracle_axes(hist)) for hist in wl.hists]
-    pkg.fill_multi(hs, [hist.cols for hist in wl.hists], [hist.weighted for hist in wl.hists], cols, w)
-    got = [h.read() for h in hs]
-    for h in hs:
-        h.close()
+    got = {}
+    for mode in (pkg.BH_MULTI_PASSES, pkg.BH_MULTI_ONE_PASS):     # both plans of bh_fill_multi
+        hs = [pkg.Histogram(oracle.oracle_axes(hist)) for hist in wl.hists]
+        if mode == pkg.BH_MULTI_ONE_PASS:
+            pkg.bh_set_debug(hs[0].h, pkg.BH_DEBUG_REQUIRE_JIT)
+        pkg.fill_multi(hs, [hist.cols for hist in wl.hists], [hist.weighted for hist in wl.hists], cols, w, mode=mode)
+        got[mode] = [h.read() for h in hs]
+        for h in hs:
+            h.close()
     del cols, w
     torch.cuda.empty_cache()
     for i, hist in enumerate(wl.hists):
         ref = oracle_parallel("C5", n, hidx=i)
-        compare(got[i], ref, hist.weighted, f"C5 H{i}")
+        for mode, g in got.items():
+            compare(g[i], ref, hist.weighted, f"C5 H{i} plan {mode}")
 
 
 # ------------------------------------------------------------------ host -> device path

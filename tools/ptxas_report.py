@@ -4,9 +4,10 @@ import re
 import subprocess
 import sys
 
-src = "paper_2401_13310_b200/csrc/bhist.cu"
+import sys
+src = sys.argv[1] if len(sys.argv) > 1 else "paper_2401_13310_b200/csrc/bhist.cu"
 out = subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xptxas", "-v",
-                      "-c", "-o", "/dev/null", src], capture_output=True, text=True).stderr
+                      "-I", "paper_2401_13310_b200/build/libbhist.so.obj", "-c", "-o", "/dev/null", src], capture_output=True, text=True).stderr
 cur = None
 rows = []
 for line in out.splitlines():

@@ -282,8 +282,9 @@ def measure_bulk_regime(local: int, total: int = 1 << 25, bulk: int = 32768) -> 
     [0,1] (random widths), uniform float64 events handed over in bulks of 32768 from host
     memory, end to end (H2D inside, steady clock, result read back once at the end,
     PAPER.md:129).  Rows: one bh_fill_host call per bulk from pinned bulk buffers (the
-    RDataFrame pattern), and one call over the whole array with the library's staging
-    chunk swept (32768 ... 2^22 events)."""
+    RDataFrame pattern); the persistent bulk consumer (bh_bulk_fill per bulk, and
+    bh_bulk_submit with up to 4 bulks in flight); and one bh_fill_host call over the whole
+    array with the library's staging chunk swept (32768 ... 2^22 events)."""
     import torch
     import paper_2401_13310_b200 as pkg
     edges = bhgen.edges_random_widths(bhgen.seed_of(6, 15), 1000)
@@ -310,6 +311,24 @@ def measure_bulk_regime(local: int, total: int = 1 << 25, bulk: int = 32768) -> 
             H.fill_host([b])
     pkg.bh_set_chunk(H.h, bulk)
     out["per_bulk_calls_events_per_s"] = run(per_bulk)
+
+    # the persistent bulk consumer (bh_bulk_*): one resident kernel reads each bulk straight
+    # from pinned host memory; per bulk no launch and no cudaMemcpy
+    def consumer_sync():                                  # bh_bulk_fill: returns when consumed
+        H.bulk_begin(False)
+        for b in bulks:
+            H.bulk_fill([b])
+        H.bulk_end()
+
+    def consumer_pipelined():                             # up to 4 bulks in flight
+        H.bulk_begin(False)
+        t = 0
+        for b in bulks:
+            t = H.bulk_submit([b])
+        H.bulk_wait(t)
+        H.bulk_end()
+    out["persistent_consumer_per_bulk_events_per_s"] = run(consumer_sync)
+    out["persistent_consumer_pipelined_events_per_s"] = run(consumer_pipelined)
     sweep = {}
     for chunk in (bulk, 1 << 18, 1 << 20, 1 << 22):
         pkg.bh_set_chunk(H.h, chunk)

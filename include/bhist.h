@@ -158,6 +158,38 @@ bh_status bh_fill_host_f32(bh_hist *h, int64_t n, const float *const *coords, co
  * semantics), HOST pointers. */
 bh_status bh_fill_host_i32(bh_hist *h, int64_t n, const int32_t *const *coords, const float *w, bh_stream s);
 
+/* Persistent bulk consumer: the paper's per-bulk fill loop (RHnCUDA "transfers bulk of events
+ * to the GPU and launches kernels ... per bulk"; bulks of 32768 events,
+ * PAPER.md:241) without a kernel launch or a copy per bulk (at such sizes
+ * launch and transfer overheads dominate).  bh_bulk_begin launches ONE kernel on stream s that
+ * stays resident (one CTA per SM) until bh_bulk_end; each bh_bulk_submit posts a bulk to it
+ * through a descriptor ring in mapped pinned host memory, and every CTA reads its share of the
+ * bulk straight from the host columns over PCIe (zero-copy) into its private bins and register
+ * statistics; the bins are flushed and the statistics reduced once, at bh_bulk_end.
+ *  bh_bulk_begin(h, weighted, timeout_ms, s): weighted != 0 -> every bulk carries weights.
+ *      timeout_ms (0 = 10000): the kernel leaves (dropping the session's fills, reported as
+ *      BH_ECUDA by the next bulk call) if no bulk arrives for that long, so a host that dies
+ *      mid-session cannot leave the GPU occupied.  Strategy as for a large bh_fill (PRIV, CACHE
+ *      or GLOBAL; EXACT/SORT histograms get BH_EINVAL).  Nothing else may be issued on s until
+ *      bh_bulk_end: work queued behind the resident kernel waits for the session's end.
+ *  bh_bulk_submit(h, n, coords, w, &ticket): HOST columns of n (<= 2^31) float64 events (w iff
+ *      weighted).  Pinned (page-locked) columns are read in place: the caller must not modify
+ *      them until bh_bulk_wait(ticket) returns; pageable columns are first copied into pinned
+ *      staging (then the call returns with them reusable).  Up to 4 bulks are in flight; a 5th
+ *      submit waits for the oldest.
+ *  bh_bulk_wait(h, ticket): returns once the bulk's host bytes are consumed.
+ *  bh_bulk_fill(h, n, coords, w) = submit + wait.
+ *  bh_bulk_end(h): posts the end of the sequence and returns once every CTA has flushed its
+ *      bins and statistics (the kernel then exits; bh_read(h, ..., s) sees the full result);
+ *      BH_ECUDA if the consumer had timed out (the session's fills are lost).
+ * While a session is active the histogram's other calls (fill, read, reset, pack, ...) return
+ * BH_EINVAL.  The result equals bh_fill of the concatenated bulks (entries += n per bulk). */
+bh_status bh_bulk_begin(bh_hist *h, int32_t weighted, int32_t timeout_ms, bh_stream s);
+bh_status bh_bulk_submit(bh_hist *h, int64_t n, const double *const *coords, const double *w, int64_t *ticket);
+bh_status bh_bulk_wait(bh_hist *h, int64_t ticket);
+bh_status bh_bulk_fill(bh_hist *h, int64_t n, const double *const *coords, const double *w);
+bh_status bh_bulk_end(bh_hist *h);
+
 /* Fused multi-histogram fill (one pass over the columns; PAPER.md:470 future work,
  * BASELINE.json config 5).  hs[nh] (1 <= nh <= 8, distinct, same device);
  * col_of_axis[3*i + a] = index into cols[] of the column feeding axis a of

@@ -28,7 +28,8 @@ EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset"
             "bh_fill_multi", "bh_fill_expr", "bh_fill_f32", "bh_fill_i32", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
             "bh_fill_host_f32", "bh_fill_host_i32", "bh_packed_size_multi", "bh_pack_multi", "bh_unpack_multi",
             "bh_jit_compile_check",
-            "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_set_multi_mode", "bh_launch_count"]
+            "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_set_multi_mode", "bh_launch_count",
+            "bh_bulk_begin", "bh_bulk_submit", "bh_bulk_wait", "bh_bulk_fill", "bh_bulk_end"]
 
 
 class BHistError(RuntimeError):
@@ -101,6 +102,11 @@ def lib(build_if_stale: bool = False):
             "bh_set_chunk": ([_P, _I64], _I32),
             "bh_set_debug": ([_P, _I32], _I32),
             "bh_set_multi_mode": ([_P, _I32], _I32),
+            "bh_bulk_begin": ([_P, _I32, _I32, _P], _I32),
+            "bh_bulk_submit": ([_P, _I64, _P, _P, _P], _I32),
+            "bh_bulk_wait": ([_P, _I64], _I32),
+            "bh_bulk_fill": ([_P, _I64, _P, _P], _I32),
+            "bh_bulk_end": ([_P], _I32),
             "bh_launch_count": ([_P, _P], _I32),
         }
         for name, (args, res) in sig.items():
@@ -354,6 +360,30 @@ def bh_set_debug(h, flags: int) -> None:
     _check(lib().bh_set_debug(h, flags))
 
 
+def bh_bulk_begin(h, weighted: bool, timeout_ms: int = 0, stream=None) -> None:
+    _check(lib().bh_bulk_begin(h, int(bool(weighted)), timeout_ms, stream))
+
+
+def bh_bulk_submit(h, n: int, host_col_ptrs, host_w_ptr=None) -> int:
+    arr = _ptrs(host_col_ptrs)
+    t = _I64()
+    _check(lib().bh_bulk_submit(h, n, ctypes.addressof(arr), host_w_ptr, ctypes.byref(t)))
+    return t.value
+
+
+def bh_bulk_wait(h, ticket: int) -> None:
+    _check(lib().bh_bulk_wait(h, ticket))
+
+
+def bh_bulk_fill(h, n: int, host_col_ptrs, host_w_ptr=None) -> None:
+    arr = _ptrs(host_col_ptrs)
+    _check(lib().bh_bulk_fill(h, n, ctypes.addressof(arr), host_w_ptr))
+
+
+def bh_bulk_end(h) -> None:
+    _check(lib().bh_bulk_end(h))
+
+
 def bh_set_multi_mode(h, mode: int) -> None:
     _check(lib().bh_set_multi_mode(h, mode))
 
@@ -462,6 +492,35 @@ class Histogram:
         n = len(coords[0])
         ptrs = [_host_col(c, n, "coords") for c in coords]
         bh_fill_host(self.h, n, ptrs, None if w is None else _host_col(w, n, "w"), self._s(stream))
+        return self
+
+    # persistent bulk consumer (bh_bulk_*): one resident kernel for a sequence of host bulks
+    def bulk_begin(self, weighted: bool, timeout_ms: int = 0, stream=None):
+        bh_bulk_begin(self.h, weighted, timeout_ms, self._s(stream))
+        return self
+
+    def _bulk_ptrs(self, coords, w):
+        if len(coords) != self.dim:
+            raise ValueError(f"need {self.dim} coordinate columns, got {len(coords)}")
+        n = len(coords[0])
+        return n, [_host_col(c, n, "coords") for c in coords], None if w is None else _host_col(w, n, "w")
+
+    def bulk_submit(self, coords, w=None) -> int:
+        """Post host columns (pinned: read in place, keep them unmodified until bulk_wait)."""
+        n, ptrs, wp = self._bulk_ptrs(coords, w)
+        return bh_bulk_submit(self.h, n, ptrs, wp)
+
+    def bulk_wait(self, ticket: int):
+        bh_bulk_wait(self.h, ticket)
+        return self
+
+    def bulk_fill(self, coords, w=None):
+        n, ptrs, wp = self._bulk_ptrs(coords, w)
+        bh_bulk_fill(self.h, n, ptrs, wp)
+        return self
+
+    def bulk_end(self):
+        bh_bulk_end(self.h)
         return self
 
     def fill_host_f32(self, coords, w=None, stream=None):

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdint>
@@ -516,6 +518,14 @@ bh_status check_hist(const bh_hist *h) {
     return BH_OK;
 }
 
+// calls that touch the state or its stream may not run while a persistent bulk consumer
+// (bh_bulk_begin .. bh_bulk_end) owns the histogram
+bh_status bulk_check(const bh_hist *h) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (h->bulk_active) return fail(BH_EINVAL, "a bulk session (bh_bulk_begin) is active on this histogram");
+    return BH_OK;
+}
+
 }  // namespace
 
 namespace bh {
@@ -682,7 +692,12 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
 bh_status bh_destroy(bh_hist *h) {
     if (!h) return BH_OK;
     DeviceGuard dg(h->device);
+    if (h->bulk_active) bh_bulk_end(h);      // let the persistent consumer finish before freeing
     cudaDeviceSynchronize();
+    if (h->bulk_ctl) cudaFreeHost(h->bulk_ctl);
+    cudaFree(h->bulk_arrive);
+    for (int i = 0; i < kBulkRing; ++i)
+        if (h->bulk_stage[i]) cudaFreeHost(h->bulk_stage[i]);
     cudaFree(h->count);
     cudaFree(h->sumw);
     cudaFree(h->sumw2);
@@ -712,7 +727,7 @@ bh_status bh_destroy(bh_hist *h) {
 }
 
 bh_status bh_reset(bh_hist *h, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     DeviceGuard dg(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(s);
     CUDA_TRY(cudaMemsetAsync(h->count, 0, sizeof(unsigned long long) * h->G, st));
@@ -726,7 +741,7 @@ bh_status bh_reset(bh_hist *h, bh_stream s) {
 }
 
 bh_status bh_fill(bh_hist *h, int64_t n, const double *const *coords, const double *w, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     if (n < 0) return fail(BH_EINVAL, "n < 0");
     if (n == 0) return BH_OK;
     if (!coords) return fail(BH_EINVAL, "coords is NULL");
@@ -737,7 +752,7 @@ bh_status bh_fill(bh_hist *h, int64_t n, const double *const *coords, const doub
 }
 
 bh_status bh_fill_f32(bh_hist *h, int64_t n, const float *const *coords, const float *w, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     if (n < 0) return fail(BH_EINVAL, "n < 0");
     if (n == 0) return BH_OK;
     if (!coords) return fail(BH_EINVAL, "coords is NULL");
@@ -748,7 +763,7 @@ bh_status bh_fill_f32(bh_hist *h, int64_t n, const float *const *coords, const f
 }
 
 bh_status bh_fill_i32(bh_hist *h, int64_t n, const int32_t *const *coords, const float *w, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     if (n < 0) return fail(BH_EINVAL, "n < 0");
     if (n == 0) return BH_OK;
     if (!coords) return fail(BH_EINVAL, "coords is NULL");
@@ -765,7 +780,7 @@ namespace {
 // (double: bh_fill path; float / int32_t: the 4-byte path with float32 weights).
 template <typename CT, typename WT>
 bh_status fill_host_impl(bh_hist *h, int64_t n, const CT *const *coords, const WT *w, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     if (n < 0) return fail(BH_EINVAL, "n < 0");
     if (n == 0) return BH_OK;
     if (!coords) return fail(BH_EINVAL, "coords is NULL");
@@ -844,6 +859,203 @@ bh_status bh_fill_host_i32(bh_hist *h, int64_t n, const int32_t *const *coords, 
     return fill_host_impl<int32_t, float>(h, n, coords, w, s);
 }
 
+// ---------------------------------------------------------------- persistent bulk consumer
+// (bhist_bulk.cuh).  The host side of the descriptor ring: post a bulk (plain stores of its
+// fields, then its sequence number with release semantics) and wait for the device's "done".
+
+}  // extern "C"
+
+namespace {
+volatile long long &bulk_done(const bh_hist *h) { return *reinterpret_cast<volatile long long *>(&h->bulk_ctl->done); }
+
+// wait until the device has consumed bulk `seq` (false on timeout or device-side abort)
+bool bulk_wait_done(const bh_hist *h, long long seq) {
+    if (bulk_done(h) >= seq) return true;
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto limit = std::chrono::nanoseconds(h->bulk_timeout_ns + 2000000000LL);
+    for (uint64_t spin = 0;; ++spin) {
+        if (bulk_done(h) >= seq) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            return true;
+        }
+        if ((spin & 1023) == 0) {
+            if (*reinterpret_cast<volatile long long *>(&h->bulk_ctl->status) != 0) return false;
+            if (std::chrono::steady_clock::now() - t0 > limit) return false;
+        }
+    }
+}
+
+void bulk_post(bh_hist *h, long long seq, int64_t n, const double *const *x, const double *w) {
+    BulkDesc *d = &h->bulk_ctl->ring[(seq - 1) % kBulkRing];
+    d->n = n;
+    for (int a = 0; a < kMaxDim; ++a) d->x[a] = a < h->dim && x ? x[a] : nullptr;
+    d->w = w;
+    std::atomic_thread_fence(std::memory_order_release);
+    *reinterpret_cast<volatile long long *>(&d->seq) = seq;
+}
+
+}  // namespace
+
+extern "C" {
+
+bh_status bh_bulk_begin(bh_hist *h, int32_t weighted, int32_t timeout_ms, bh_stream s) {
+    if (bulk_check(h)) return BH_EINVAL;
+    if (timeout_ms < 0) return fail(BH_EINVAL, "timeout_ms < 0");
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    if (!h->bulk_ctl) {
+        void *p = nullptr;
+        if (cudaHostAlloc(&p, sizeof(BulkCtl), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(BH_ENOMEM, "pinned bulk descriptor ring");
+        }
+        h->bulk_ctl = static_cast<BulkCtl *>(p);
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(&h->bulk_arrive), sizeof(unsigned long long)));
+    }
+    memset(h->bulk_ctl, 0, sizeof(BulkCtl));
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    BulkCtl *dctl = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dctl), h->bulk_ctl, 0));
+    CUDA_TRY(cudaMemsetAsync(h->bulk_arrive, 0, sizeof(unsigned long long), st));
+    // the plan of a large fill: the kernel lives for the whole sequence, so PRIV's zeroing and
+    // flushing of the private bins is paid once, not per bulk
+    const bool W = weighted != 0;
+    if (W) h->weighted_content = true;
+    const int strategy = resolve_one_pass(h, W);
+    if (strategy != BH_STRATEGY_PRIV && strategy != BH_STRATEGY_CACHE && strategy != BH_STRATEGY_GLOBAL)
+        return fail(BH_EINVAL, "bulk sessions support the PRIV, CACHE and GLOBAL strategies");
+    FillPlan pl;
+    if (bh_status r = plan_fill(h, W, pl, int64_t(1) << 40)) return r;
+    LaunchCfg &c = pl.c;
+    const double *none[kMaxDim] = {};
+    FillP p = make_params(h, 0, none, nullptr);
+    for (int a = 0; a < h->dim; ++a) p.ax[a] = pl.ax[a];
+    p.entries_add = 0;                     // entries are added per bulk by the kernel
+    p.cache_slots = cache_slots_for(W);
+    p.replicas = pl.replicas;
+    p.wc_off = pl.wc_off;
+    c.grid = h->nsm * resident_blocks(c.strategy);   // every CTA resident: each one takes a share of every bulk
+    const long long tmo = (long long)(timeout_ms ? timeout_ms : 10000) * 1000000LL;
+    cudaError_t e;
+    switch (h->dim) {
+    case 1: e = W ? fill_launch_bulk<1, true>(p, c, dctl, h->bulk_arrive, tmo, st) : fill_launch_bulk<1, false>(p, c, dctl, h->bulk_arrive, tmo, st); break;
+    case 2: e = W ? fill_launch_bulk<2, true>(p, c, dctl, h->bulk_arrive, tmo, st) : fill_launch_bulk<2, false>(p, c, dctl, h->bulk_arrive, tmo, st); break;
+    default: e = W ? fill_launch_bulk<3, true>(p, c, dctl, h->bulk_arrive, tmo, st) : fill_launch_bulk<3, false>(p, c, dctl, h->bulk_arrive, tmo, st); break;
+    }
+    if (e != cudaSuccess) return fail(BH_ECUDA, "bulk kernel launch: %s", cudaGetErrorString(e));
+    ++h->launches;
+    h->bulk_active = true;
+    h->bulk_weighted = W;
+    h->bulk_seq = 0;
+    h->bulk_timeout_ns = tmo;
+    h->bulk_stream = st;
+    return BH_OK;
+}
+
+bh_status bh_bulk_submit(bh_hist *h, int64_t n, const double *const *coords, const double *w, int64_t *ticket) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (!h->bulk_active) return fail(BH_EINVAL, "no bulk session (bh_bulk_begin)");
+    if (n < 0 || n > (int64_t(1) << 31)) return fail(BH_EINVAL, "bulk size %lld out of [0, 2^31]", (long long)n);
+    if ((w != nullptr) != h->bulk_weighted) return fail(BH_EINVAL, "weights must be given iff the session is weighted");
+    if (n > 0) {
+        if (!coords) return fail(BH_EINVAL, "coords is NULL");
+        for (int a = 0; a < h->dim; ++a)
+            if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
+    }
+    DeviceGuard dg(h->device);
+    const long long seq = h->bulk_seq + 1;
+    // the ring slot is free once the bulk posted kBulkRing earlier is consumed
+    if (!bulk_wait_done(h, seq - kBulkRing)) return fail(BH_ECUDA, "bulk consumer not responding (timed out or aborted)");
+    const double *dx[kMaxDim] = {};
+    const double *dw = nullptr;
+    if (n > 0) {
+        // pinned columns are read in place (zero-copy); pageable ones are copied into this slot's
+        // pinned staging area first
+        bool pinned = true;
+        const double *src[kMaxDim + 1] = {};
+        for (int a = 0; a < h->dim; ++a) src[a] = coords[a];
+        src[h->dim] = w;
+        const double *dev[kMaxDim + 1] = {};
+        for (int a = 0; a <= h->dim; ++a) {
+            if (!src[a]) continue;
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, src[a]) != cudaSuccess) { cudaGetLastError(); at.type = cudaMemoryTypeUnregistered; }
+            if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged)
+                return fail(BH_EINVAL, "bh_bulk_submit takes HOST columns (use bh_fill for device columns)");
+            if (at.type == cudaMemoryTypeHost && at.devicePointer) dev[a] = static_cast<const double *>(at.devicePointer);
+            else pinned = false;
+        }
+        if (!pinned) {
+            const int ncol = h->dim + (w ? 1 : 0);
+            if (h->bulk_stage_cap < ncol * n) {
+                if (!bulk_wait_done(h, h->bulk_seq)) return fail(BH_ECUDA, "bulk consumer not responding");
+                for (int i = 0; i < kBulkRing; ++i) {
+                    if (h->bulk_stage[i]) cudaFreeHost(h->bulk_stage[i]);
+                    h->bulk_stage[i] = nullptr;
+                }
+                h->bulk_stage_cap = 0;
+                for (int i = 0; i < kBulkRing; ++i)
+                    if (cudaHostAlloc(reinterpret_cast<void **>(&h->bulk_stage[i]), sizeof(double) * ncol * n,
+                                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+                        cudaGetLastError();
+                        return fail(BH_ENOMEM, "pinned bulk staging");
+                    }
+                h->bulk_stage_cap = ncol * n;
+            }
+            double *buf = h->bulk_stage[(seq - 1) % kBulkRing];
+            for (int a = 0; a <= h->dim; ++a) {
+                if (!src[a]) continue;
+                memcpy(buf + (size_t)a * n, src[a], sizeof(double) * n);
+                double *d = nullptr;
+                CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&d), buf + (size_t)a * n, 0));
+                dev[a] = d;
+            }
+        }
+        for (int a = 0; a < h->dim; ++a) dx[a] = dev[a];
+        dw = w ? dev[h->dim] : nullptr;
+    }
+    bulk_post(h, seq, n, dx, dw);
+    h->bulk_seq = seq;
+    if (ticket) *ticket = seq;
+    return BH_OK;
+}
+
+bh_status bh_bulk_wait(bh_hist *h, int64_t ticket) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (!h->bulk_active) return fail(BH_EINVAL, "no bulk session (bh_bulk_begin)");
+    if (ticket > h->bulk_seq) return fail(BH_EINVAL, "ticket %lld was not issued", (long long)ticket);
+    if (!bulk_wait_done(h, ticket)) return fail(BH_ECUDA, "bulk consumer not responding (timed out or aborted)");
+    return BH_OK;
+}
+
+bh_status bh_bulk_fill(bh_hist *h, int64_t n, const double *const *coords, const double *w) {
+    int64_t t = 0;
+    if (bh_status r = bh_bulk_submit(h, n, coords, w, &t)) return r;
+    return bh_bulk_wait(h, t);
+}
+
+bh_status bh_bulk_end(bh_hist *h) {
+    if (check_hist(h)) return BH_EINVAL;
+    if (!h->bulk_active) return fail(BH_EINVAL, "no bulk session (bh_bulk_begin)");
+    DeviceGuard dg(h->device);
+    const long long seq = h->bulk_seq + 1;
+    bool ok = bulk_wait_done(h, seq - kBulkRing);
+    if (ok) {
+        bulk_post(h, seq, -1, nullptr, nullptr);
+        ok = bulk_wait_done(h, seq);                 // every CTA has flushed its bins and stats
+    }
+    ok = ok && *reinterpret_cast<volatile long long *>(&h->bulk_ctl->status) == 0;
+    h->bulk_active = false;
+    h->bulk_seq = seq;
+    if (!ok) {
+        // the kernel has left (or will leave) on its own after its timeout
+        cudaStreamSynchronize(h->bulk_stream);
+        cudaGetLastError();
+        return fail(BH_ECUDA, "bulk consumer not responding (timed out or aborted); the session's fills are lost");
+    }
+    return BH_OK;
+}
+
 bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_axis, const uint8_t *weighted,
                         int64_t n, const double *const *cols, int32_t ncols, const double *w, bh_stream s) {
     if (!hs || nh < 1 || nh > kMaxHist) return fail(BH_EINVAL, "need 1..%d histograms", kMaxHist);
@@ -855,6 +1067,7 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
     int nstats = 0;
     for (int i = 0; i < nh; ++i) {
         if (!hs[i]) return fail(BH_EINVAL, "histogram %d is NULL", i);
+        if (bulk_check(hs[i])) return BH_EINVAL;
         if (hs[i]->device != hs[0]->device) return fail(BH_EMISMATCH, "histograms live on different devices");
         for (int j = 0; j < i; ++j)
             if (hs[j] == hs[i]) return fail(BH_EINVAL, "histogram %d appears twice", i);
@@ -1022,7 +1235,7 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
 
 bh_status bh_fill_expr(bh_hist *h, int64_t n, const double *const *cols, int32_t ncols, const bh_op *prog,
                        int32_t nops, const int32_t *axis_reg, int32_t weight_reg, int32_t filter_reg, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     if (n < 0) return fail(BH_EINVAL, "n < 0");
     if (ncols < 0 || ncols > kExprRegs) return fail(BH_EINVAL, "need 0..%d columns", kExprRegs);
     if (nops < 0 || nops > kExprOps) return fail(BH_EINVAL, "need 0..%d ops", kExprOps);
@@ -1083,7 +1296,7 @@ bh_status bh_fill_expr(bh_hist *h, int64_t n, const double *const *cols, int32_t
 }
 
 bh_status bh_find_bins(const bh_hist *h, int64_t n, const double *const *coords, int32_t *out, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     if (n < 0) return fail(BH_EINVAL, "n < 0");
     if (n == 0) return BH_OK;
     if (!coords || !out) return fail(BH_EINVAL, "NULL pointer");
@@ -1141,7 +1354,7 @@ bh_status bh_packed_size(const bh_hist *h, int64_t *n_doubles) {
 }
 
 bh_status bh_pack(const bh_hist *h, double *dev_out, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     if (!dev_out) return fail(BH_EINVAL, "NULL output");
     DeviceGuard dg(h->device);
     const int64_t tot = 2 * h->G + h->K + 1;
@@ -1154,7 +1367,7 @@ bh_status bh_pack(const bh_hist *h, double *dev_out, bh_stream s) {
 }
 
 bh_status bh_unpack(bh_hist *h, const double *dev_in, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     if (!dev_in) return fail(BH_EINVAL, "NULL input");
     DeviceGuard dg(h->device);
     const int64_t tot = 2 * h->G + h->K + 1;
@@ -1236,7 +1449,7 @@ bh_status bh_unpack_multi(bh_hist *const *hs, int32_t nh, const uint8_t *unit, c
 }
 
 bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *stats, int64_t *entries, bh_stream s) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     DeviceGuard dg(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(s);
     bh_status r = bh_pack(h, h->pack_buf, s);
@@ -1252,7 +1465,7 @@ bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *sta
 }
 
 bh_status bh_set_strategy(bh_hist *h, int32_t strategy) {
-    if (check_hist(h)) return BH_EINVAL;
+    if (bulk_check(h)) return BH_EINVAL;
     if (strategy < BH_STRATEGY_AUTO || strategy > BH_STRATEGY_SORT) return fail(BH_EINVAL, "unknown strategy %d", strategy);
     if (strategy == BH_STRATEGY_PRIV && 4 * (size_t)h->G + kStaticSmemReserve > h->smem_optin)
         return fail(BH_EINVAL, "PRIV cannot hold %lld bins in shared memory", (long long)h->G);

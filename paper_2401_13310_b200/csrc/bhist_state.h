@@ -8,6 +8,7 @@
 
 #include "../../include/bhist.h"
 #include "bhist_kernels.cuh"
+#include "bhist_bulk.cuh"
 
 constexpr int kStageSlots = 2;
 
@@ -57,6 +58,15 @@ struct bh_hist {
     bool weighted_content = false;     // a weighted fill (or a full unpack) since create/reset
     bool slot_used[kStageSlots] = {};  // consumed[slot] recorded at least once (persists across calls)
     int next_slot = 0;                 // ring position (persists across calls)
+    // persistent bulk consumer (bh_bulk_*; bhist_bulk.cuh)
+    bh::BulkCtl *bulk_ctl = nullptr;                 // pinned, mapped host memory
+    unsigned long long *bulk_arrive = nullptr;       // device: CTA arrivals, all bulks of the session
+    double *bulk_stage[bh::kBulkRing] = {};          // pinned copies of pageable bulks, per ring slot
+    int64_t bulk_stage_cap = 0;                      // doubles per staging slot
+    bool bulk_active = false, bulk_weighted = false;
+    long long bulk_seq = 0;                          // bulks posted in this session
+    long long bulk_timeout_ns = 0;
+    cudaStream_t bulk_stream = nullptr;
 };
 
 namespace bh {

@@ -102,11 +102,16 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
         // this CTA's contiguous share of the bulk, coalesced over its threads
         const long long lo = (long long)(((unsigned long long)n * blockIdx.x) / G);
         const long long hi = (long long)(((unsigned long long)n * (blockIdx.x + 1)) / G);
-        for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-            double x[DIM];
+        // warp-uniform trips: SINK_PRIVA's warp hot-bin caches are used by converged full warps
+        for (long long i0 = lo; i0 < hi; i0 += blockDim.x) {
+            const long long i = i0 + threadIdx.x;
+            if (SINK == SINK_PRIVA) __syncwarp();
+            if (i < hi) {
+                double x[DIM];
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) x[a] = ld_host(s_x[a] + i);
-            do_event<DIM, W, VM>(p, x, W ? ld_host(s_w + i) : 1.0, sink, acc, smem);
+                for (int a = 0; a < DIM; ++a) x[a] = ld_host(s_x[a] + i);
+                do_event<DIM, W, VM>(p, x, W ? ld_host(s_w + i) : 1.0, sink, acc, smem);
+            }
         }
         __syncthreads();                  // every load of this CTA's share has returned
         if (threadIdx.x == 0) {

@@ -170,13 +170,14 @@ bh_status bh_fill_host_i32(bh_hist *h, int64_t n, const int32_t *const *coords, 
  *      timeout_ms (0 = 10000): the kernel leaves (dropping the session's fills, reported as
  *      BH_ECUDA by the next bulk call) if no bulk arrives for that long, so a host that dies
  *      mid-session cannot leave the GPU occupied.  Strategy as for a large bh_fill (PRIV, CACHE
- *      or GLOBAL; EXACT/SORT histograms get BH_EINVAL).  Nothing else may be issued on s until
- *      bh_bulk_end: work queued behind the resident kernel waits for the session's end.
+ *      or GLOBAL; EXACT/SORT histograms get BH_EINVAL).  The kernel runs on a stream of the
+ *      library's own, after the work queued on s before the call; bh_bulk_end orders s after
+ *      the session, so other work on s or any other stream is never held back by it.
  *  bh_bulk_submit(h, n, coords, w, &ticket): HOST columns of n (<= 2^31) float64 events (w iff
  *      weighted).  Pinned (page-locked) columns are read in place: the caller must not modify
  *      them until bh_bulk_wait(ticket) returns; pageable columns are first copied into pinned
- *      staging (then the call returns with them reusable).  Up to 4 bulks are in flight; a 5th
- *      submit waits for the oldest.
+ *      staging (in pieces of <= 65536 events; the call returns with them reusable).  Up to 4
+ *      bulks (pieces) are in flight; a further submit waits for the oldest.
  *  bh_bulk_wait(h, ticket): returns once the bulk's host bytes are consumed.
  *  bh_bulk_fill(h, n, coords, w) = submit + wait.
  *  bh_bulk_end(h): posts the end of the sequence and returns once every CTA has flushed its

@@ -161,7 +161,7 @@ struct FillPlan {
 // through CACHE (warp-aggregated, hot-bin safe) instead.
 bool small_fill(const bh_hist *h, int64_t n) { return n < 2 * h->G * (int64_t)h->nsm; }
 
-bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n) {
+bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n, size_t reserve = 0) {
     LaunchCfg &c = pl.c;
     c.weighted = weighted;
     c.strategy = resolve_one_pass(h, c.weighted);
@@ -178,7 +178,7 @@ bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n) {
             tabs += axis_table_bytes(pl.ax[a]);
         }
     }
-    c.vsm = tabs > 0 && sink + tabs + kStaticSmemReserve <= h->smem_optin;
+    c.vsm = tabs > 0 && sink + tabs + reserve + kStaticSmemReserve <= h->smem_optin;
     c.vm = tabs == 0 ? 0 : (c.vsm ? 1 : 2);
     if (c.vm == 1) {                     // every variable axis compact: the specialized search
         bool all3 = true;
@@ -191,7 +191,10 @@ bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n) {
     pl.wc_off = -1;
     size_t wcb = 0;
     if (c.strategy == BH_STRATEGY_PRIV) {
-        size_t spare = h->smem_optin - kStaticSmemReserve - (c.vsm ? tabs : 0);
+        if (sink + reserve + kStaticSmemReserve > h->smem_optin)
+            return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", c.strategy,
+                        sink + reserve, h->smem_optin);
+        size_t spare = h->smem_optin - kStaticSmemReserve - reserve - (c.vsm ? tabs : 0);
         const int cap = threads_of(c.strategy, c.weighted) / 32;
         // weighted fills get the collision-adaptive sink with per-warp hot-bin caches when
         // they fit, except a single replica next to variable-axis tables (C2's shape: the
@@ -214,7 +217,7 @@ bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n) {
         if (wcb) pl.wc_off = (int)(sink + (c.vsm ? tabs : 0));     // behind replicas and tables
     }
     c.smem = sink + (c.vsm ? tabs : 0) + wcb;
-    if (c.smem + kStaticSmemReserve > h->smem_optin)
+    if (c.smem + reserve + kStaticSmemReserve > h->smem_optin)
         return fail(BH_EINVAL, "strategy %d needs %zu B of shared memory (device max %zu)", c.strategy, c.smem,
                     h->smem_optin);
     return BH_OK;
@@ -695,7 +698,10 @@ bh_status bh_destroy(bh_hist *h) {
     if (h->bulk_active) bh_bulk_end(h);      // let the persistent consumer finish before freeing
     cudaDeviceSynchronize();
     if (h->bulk_ctl) cudaFreeHost(h->bulk_ctl);
-    cudaFree(h->bulk_arrive);
+    if (h->bulk_kstream) cudaStreamDestroy(h->bulk_kstream);
+    for (cudaEvent_t ev : h->bulk_ev)
+        if (ev) cudaEventDestroy(ev);
+    cudaFree(h->bulk_dev);
     for (int i = 0; i < kBulkRing; ++i)
         if (h->bulk_stage[i]) cudaFreeHost(h->bulk_stage[i]);
     cudaFree(h->count);
@@ -866,15 +872,19 @@ bh_status bh_fill_host_i32(bh_hist *h, int64_t n, const int32_t *const *coords, 
 }  // extern "C"
 
 namespace {
-volatile long long &bulk_done(const bh_hist *h) { return *reinterpret_cast<volatile long long *>(&h->bulk_ctl->done); }
+// bulk `seq` is consumed once the done word of its ring slot has reached it
+bool bulk_is_done(const bh_hist *h, long long seq) {
+    if (seq <= 0) return true;
+    return *reinterpret_cast<volatile long long *>(&h->bulk_ctl->done[(seq - 1) % kBulkRing]) >= seq;
+}
 
 // wait until the device has consumed bulk `seq` (false on timeout or device-side abort)
 bool bulk_wait_done(const bh_hist *h, long long seq) {
-    if (bulk_done(h) >= seq) return true;
+    if (bulk_is_done(h, seq)) return true;
     const auto t0 = std::chrono::steady_clock::now();
     const auto limit = std::chrono::nanoseconds(h->bulk_timeout_ns + 2000000000LL);
     for (uint64_t spin = 0;; ++spin) {
-        if (bulk_done(h) >= seq) {
+        if (bulk_is_done(h, seq)) {
             std::atomic_thread_fence(std::memory_order_acquire);
             return true;
         }
@@ -910,13 +920,32 @@ bh_status bh_bulk_begin(bh_hist *h, int32_t weighted, int32_t timeout_ms, bh_str
             return fail(BH_ENOMEM, "pinned bulk descriptor ring");
         }
         h->bulk_ctl = static_cast<BulkCtl *>(p);
-        CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(&h->bulk_arrive), sizeof(unsigned long long)));
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(&h->bulk_dev), sizeof(BulkDev)));
     }
+    if (!h->bulk_stage[0]) {          // pinned staging for pageable bulks (kBulkRing slots)
+        const int64_t cap = 1 << 16;
+        for (int i = 0; i < kBulkRing; ++i)
+            if (cudaHostAlloc(reinterpret_cast<void **>(&h->bulk_stage[i]), sizeof(double) * (kMaxDim + 1) * cap,
+                              cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(BH_ENOMEM, "pinned bulk staging");
+            }
+        h->bulk_stage_cap = cap;
+    }
+    // the resident kernel runs on a non-blocking stream of the histogram's own, ordered after
+    // the caller's earlier work on s; bh_bulk_end orders s after it.  (On the caller's stream
+    // it would hold back everything queued behind it -- with the legacy default stream, every
+    // blocking stream of the process.)
+    if (!h->bulk_kstream) CUDA_TRY(cudaStreamCreateWithFlags(&h->bulk_kstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i)
+        if (!h->bulk_ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->bulk_ev[i], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(h->bulk_ev[0], st));
+    CUDA_TRY(cudaStreamWaitEvent(h->bulk_kstream, h->bulk_ev[0], 0));
     memset(h->bulk_ctl, 0, sizeof(BulkCtl));
     std::atomic_thread_fence(std::memory_order_seq_cst);
     BulkCtl *dctl = nullptr;
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dctl), h->bulk_ctl, 0));
-    CUDA_TRY(cudaMemsetAsync(h->bulk_arrive, 0, sizeof(unsigned long long), st));
+    CUDA_TRY(cudaMemsetAsync(h->bulk_dev, 0, sizeof(BulkDev), h->bulk_kstream));
     // the plan of a large fill: the kernel lives for the whole sequence, so PRIV's zeroing and
     // flushing of the private bins is paid once, not per bulk
     const bool W = weighted != 0;
@@ -924,9 +953,22 @@ bh_status bh_bulk_begin(bh_hist *h, int32_t weighted, int32_t timeout_ms, bh_str
     const int strategy = resolve_one_pass(h, W);
     if (strategy != BH_STRATEGY_PRIV && strategy != BH_STRATEGY_CACHE && strategy != BH_STRATEGY_GLOBAL)
         return fail(BH_EINVAL, "bulk sessions support the PRIV, CACHE and GLOBAL strategies");
+    // shared memory for the TMA staging of bulks (two tiles of te events per column), as
+    // much as the plan leaves; none: the threads read the host columns directly
+    const int ncol = h->dim + (W ? 1 : 0);
+    auto stage_bytes = [&](int te) { return align16((size_t)2 * ncol * (te + 2) * 8 + 16 + (size_t)2 * ncol * 4); };
     FillPlan pl;
-    if (bh_status r = plan_fill(h, W, pl, int64_t(1) << 40)) return r;
+    int te = 0;
+    if (!getenv("BHIST_BULK_NO_TMA"))
+        for (int t : {2048, 1024, 512, 256}) {
+            FillPlan q;
+            if (plan_fill(h, W, q, int64_t(1) << 40, stage_bytes(t)) == BH_OK) { pl = q; te = t; break; }
+        }
+    if (te == 0)
+        if (bh_status r = plan_fill(h, W, pl, int64_t(1) << 40)) return r;
     LaunchCfg &c = pl.c;
+    const int stage_off = (int)align16(c.smem);
+    if (te) c.smem = stage_off + stage_bytes(te);
     const double *none[kMaxDim] = {};
     FillP p = make_params(h, 0, none, nullptr);
     for (int a = 0; a < h->dim; ++a) p.ax[a] = pl.ax[a];
@@ -938,11 +980,12 @@ bh_status bh_bulk_begin(bh_hist *h, int32_t weighted, int32_t timeout_ms, bh_str
     const long long tmo = (long long)(timeout_ms ? timeout_ms : 10000) * 1000000LL;
     cudaError_t e;
     switch (h->dim) {
-    case 1: e = W ? fill_launch_bulk<1, true>(p, c, dctl, h->bulk_arrive, tmo, st) : fill_launch_bulk<1, false>(p, c, dctl, h->bulk_arrive, tmo, st); break;
-    case 2: e = W ? fill_launch_bulk<2, true>(p, c, dctl, h->bulk_arrive, tmo, st) : fill_launch_bulk<2, false>(p, c, dctl, h->bulk_arrive, tmo, st); break;
-    default: e = W ? fill_launch_bulk<3, true>(p, c, dctl, h->bulk_arrive, tmo, st) : fill_launch_bulk<3, false>(p, c, dctl, h->bulk_arrive, tmo, st); break;
+    case 1: e = W ? fill_launch_bulk<1, true>(p, c, dctl, h->bulk_dev, tmo, stage_off, te, h->bulk_kstream) : fill_launch_bulk<1, false>(p, c, dctl, h->bulk_dev, tmo, stage_off, te, h->bulk_kstream); break;
+    case 2: e = W ? fill_launch_bulk<2, true>(p, c, dctl, h->bulk_dev, tmo, stage_off, te, h->bulk_kstream) : fill_launch_bulk<2, false>(p, c, dctl, h->bulk_dev, tmo, stage_off, te, h->bulk_kstream); break;
+    default: e = W ? fill_launch_bulk<3, true>(p, c, dctl, h->bulk_dev, tmo, stage_off, te, h->bulk_kstream) : fill_launch_bulk<3, false>(p, c, dctl, h->bulk_dev, tmo, stage_off, te, h->bulk_kstream); break;
     }
     if (e != cudaSuccess) return fail(BH_ECUDA, "bulk kernel launch: %s", cudaGetErrorString(e));
+    CUDA_TRY(cudaEventRecord(h->bulk_ev[1], h->bulk_kstream));
     ++h->launches;
     h->bulk_active = true;
     h->bulk_weighted = W;
@@ -956,67 +999,62 @@ bh_status bh_bulk_submit(bh_hist *h, int64_t n, const double *const *coords, con
     if (check_hist(h)) return BH_EINVAL;
     if (!h->bulk_active) return fail(BH_EINVAL, "no bulk session (bh_bulk_begin)");
     if (n < 0 || n > (int64_t(1) << 31)) return fail(BH_EINVAL, "bulk size %lld out of [0, 2^31]", (long long)n);
-    if ((w != nullptr) != h->bulk_weighted) return fail(BH_EINVAL, "weights must be given iff the session is weighted");
+    if (n > 0 && (w != nullptr) != h->bulk_weighted) return fail(BH_EINVAL, "weights must be given iff the session is weighted");
     if (n > 0) {
         if (!coords) return fail(BH_EINVAL, "coords is NULL");
         for (int a = 0; a < h->dim; ++a)
             if (!coords[a]) return fail(BH_EINVAL, "coords[%d] is NULL", a);
     }
     DeviceGuard dg(h->device);
-    const long long seq = h->bulk_seq + 1;
-    // the ring slot is free once the bulk posted kBulkRing earlier is consumed
-    if (!bulk_wait_done(h, seq - kBulkRing)) return fail(BH_ECUDA, "bulk consumer not responding (timed out or aborted)");
-    const double *dx[kMaxDim] = {};
-    const double *dw = nullptr;
-    if (n > 0) {
-        // pinned columns are read in place (zero-copy); pageable ones are copied into this slot's
-        // pinned staging area first
-        bool pinned = true;
-        const double *src[kMaxDim + 1] = {};
-        for (int a = 0; a < h->dim; ++a) src[a] = coords[a];
-        src[h->dim] = w;
-        const double *dev[kMaxDim + 1] = {};
-        for (int a = 0; a <= h->dim; ++a) {
-            if (!src[a]) continue;
-            cudaPointerAttributes at{};
-            if (cudaPointerGetAttributes(&at, src[a]) != cudaSuccess) { cudaGetLastError(); at.type = cudaMemoryTypeUnregistered; }
-            if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged)
-                return fail(BH_EINVAL, "bh_bulk_submit takes HOST columns (use bh_fill for device columns)");
-            if (at.type == cudaMemoryTypeHost && at.devicePointer) dev[a] = static_cast<const double *>(at.devicePointer);
-            else pinned = false;
-        }
-        if (!pinned) {
-            const int ncol = h->dim + (w ? 1 : 0);
-            if (h->bulk_stage_cap < ncol * n) {
-                if (!bulk_wait_done(h, h->bulk_seq)) return fail(BH_ECUDA, "bulk consumer not responding");
-                for (int i = 0; i < kBulkRing; ++i) {
-                    if (h->bulk_stage[i]) cudaFreeHost(h->bulk_stage[i]);
-                    h->bulk_stage[i] = nullptr;
-                }
-                h->bulk_stage_cap = 0;
-                for (int i = 0; i < kBulkRing; ++i)
-                    if (cudaHostAlloc(reinterpret_cast<void **>(&h->bulk_stage[i]), sizeof(double) * ncol * n,
-                                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
-                        cudaGetLastError();
-                        return fail(BH_ENOMEM, "pinned bulk staging");
-                    }
-                h->bulk_stage_cap = ncol * n;
-            }
-            double *buf = h->bulk_stage[(seq - 1) % kBulkRing];
-            for (int a = 0; a <= h->dim; ++a) {
-                if (!src[a]) continue;
-                memcpy(buf + (size_t)a * n, src[a], sizeof(double) * n);
-                double *d = nullptr;
-                CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&d), buf + (size_t)a * n, 0));
-                dev[a] = d;
-            }
-        }
-        for (int a = 0; a < h->dim; ++a) dx[a] = dev[a];
-        dw = w ? dev[h->dim] : nullptr;
+    // pinned columns are read in place (zero-copy); pageable ones are copied, in pieces of at
+    // most bulk_stage_cap events, into the pinned staging area of the ring slot (allocated at
+    // bh_bulk_begin: no allocation may run while the consumer kernel is resident)
+    const double *src[kMaxDim + 1] = {};
+    for (int a = 0; a < h->dim && n > 0; ++a) src[a] = coords[a];
+    if (n > 0) src[h->dim] = w;
+    const double *dev[kMaxDim + 1] = {};
+    bool pinned = true;
+    for (int a = 0; a <= h->dim && n > 0; ++a) {
+        if (!src[a]) continue;
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, src[a]) != cudaSuccess) { cudaGetLastError(); at.type = cudaMemoryTypeUnregistered; }
+        if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged)
+            return fail(BH_EINVAL, "bh_bulk_submit takes HOST columns (use bh_fill for device columns)");
+        if (at.type == cudaMemoryTypeHost && at.devicePointer) dev[a] = static_cast<const double *>(at.devicePointer);
+        else pinned = false;
     }
-    bulk_post(h, seq, n, dx, dw);
-    h->bulk_seq = seq;
-    if (ticket) *ticket = seq;
+    const int64_t piece = pinned ? std::max<int64_t>(n, 1) : h->bulk_stage_cap;
+    int64_t off = 0;
+    do {
+        const int64_t m = std::min<int64_t>(piece, n - off);
+        const long long seq = h->bulk_seq + 1;
+        // the ring slot is free once the bulk posted kBulkRing earlier is consumed
+        if (!bulk_wait_done(h, seq - kBulkRing)) return fail(BH_ECUDA, "bulk consumer not responding (timed out or aborted)");
+        const double *dx[kMaxDim] = {};
+        const double *dw = nullptr;
+        if (m > 0) {
+            const double *col[kMaxDim + 1] = {};
+            if (pinned) {
+                for (int a = 0; a <= h->dim; ++a) col[a] = dev[a];
+            } else {
+                double *buf = h->bulk_stage[(seq - 1) % kBulkRing];
+                for (int a = 0; a <= h->dim; ++a) {
+                    if (!src[a]) continue;
+                    double *slotcol = buf + (size_t)a * h->bulk_stage_cap;
+                    memcpy(slotcol, src[a] + off, sizeof(double) * m);
+                    double *d = nullptr;
+                    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&d), slotcol, 0));
+                    col[a] = d - off;                     // indexed from `off` below
+                }
+            }
+            for (int a = 0; a < h->dim; ++a) dx[a] = col[a] + off;
+            dw = w ? col[h->dim] + off : nullptr;
+        }
+        bulk_post(h, seq, m, dx, dw);
+        h->bulk_seq = seq;
+        off += m;
+    } while (off < n);
+    if (ticket) *ticket = h->bulk_seq;
     return BH_OK;
 }
 
@@ -1047,9 +1085,10 @@ bh_status bh_bulk_end(bh_hist *h) {
     ok = ok && *reinterpret_cast<volatile long long *>(&h->bulk_ctl->status) == 0;
     h->bulk_active = false;
     h->bulk_seq = seq;
+    CUDA_TRY(cudaStreamWaitEvent(h->bulk_stream, h->bulk_ev[1], 0));    // s after the session
     if (!ok) {
         // the kernel has left (or will leave) on its own after its timeout
-        cudaStreamSynchronize(h->bulk_stream);
+        cudaStreamSynchronize(h->bulk_kstream);
         cudaGetLastError();
         return fail(BH_ECUDA, "bulk consumer not responding (timed out or aborted); the session's fills are lost");
     }

@@ -150,26 +150,26 @@ cudaError_t launch_expr_w(const FillP &p, const ExprP &e, const LaunchCfg &c, cu
 
 
 template <int DIM, bool W, int SINK>
-cudaError_t launch_bulk_s(const FillP &p, const LaunchCfg &c, BulkCtl *ctl, unsigned long long *arrive,
-                          long long timeout_ns, cudaStream_t s) {
+cudaError_t launch_bulk_s(const FillP &p, const LaunchCfg &c, BulkCtl *ctl, BulkDev *dev,
+                          long long timeout_ns, int stage_off, int te, cudaStream_t s) {
     auto kern = c.vm == 0 ? k_bulk<DIM, W, SINK, 0>
                           : c.vm == 1 ? k_bulk<DIM, W, SINK, 1> : c.vm == 3 ? k_bulk<DIM, W, SINK, 3> : k_bulk<DIM, W, SINK, 2>;
     if (cudaError_t r = ensure_smem(reinterpret_cast<const void *>(kern), c.smem)) return r;
-    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p, ctl, arrive, timeout_ns);
+    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p, ctl, dev, timeout_ns, stage_off, te);
     return cudaGetLastError();
 }
 
 template <int DIM, bool W>
-cudaError_t launch_bulk_w(const FillP &p, const LaunchCfg &c, BulkCtl *ctl, unsigned long long *arrive,
-                          long long timeout_ns, cudaStream_t s) {
+cudaError_t launch_bulk_w(const FillP &p, const LaunchCfg &c, BulkCtl *ctl, BulkDev *dev,
+                          long long timeout_ns, int stage_off, int te, cudaStream_t s) {
     switch (c.strategy) {
     case BH_STRATEGY_PRIV:
         if constexpr (W) {
-            if (p.wc_off >= 0) return launch_bulk_s<DIM, W, SINK_PRIVA>(p, c, ctl, arrive, timeout_ns, s);
+            if (p.wc_off >= 0) return launch_bulk_s<DIM, W, SINK_PRIVA>(p, c, ctl, dev, timeout_ns, stage_off, te, s);
         }
-        return launch_bulk_s<DIM, W, SINK_PRIV>(p, c, ctl, arrive, timeout_ns, s);
-    case BH_STRATEGY_CACHE: return launch_bulk_s<DIM, W, SINK_CACHE>(p, c, ctl, arrive, timeout_ns, s);
-    default: return launch_bulk_s<DIM, W, SINK_GLOBAL>(p, c, ctl, arrive, timeout_ns, s);
+        return launch_bulk_s<DIM, W, SINK_PRIV>(p, c, ctl, dev, timeout_ns, stage_off, te, s);
+    case BH_STRATEGY_CACHE: return launch_bulk_s<DIM, W, SINK_CACHE>(p, c, ctl, dev, timeout_ns, stage_off, te, s);
+    default: return launch_bulk_s<DIM, W, SINK_GLOBAL>(p, c, ctl, dev, timeout_ns, stage_off, te, s);
     }
 }
 
@@ -180,7 +180,8 @@ template <int DIM, bool W> cudaError_t fill_launch_i32(const FillP &p, const Lau
 template <int DIM, bool W> cudaError_t fill_launch_expr(const FillP &p, const ExprP &e, const LaunchCfg &c, cudaStream_t s);
 template <int DIM, bool W> cudaError_t fill_launch_part1(const FillP &p, const PartP &q, int vm, int rc, int grid, size_t smem, cudaStream_t s);
 template <int DIM, bool W> cudaError_t fill_launch_bulk(const FillP &p, const LaunchCfg &c, BulkCtl *ctl,
-                                                        unsigned long long *arrive, long long timeout_ns, cudaStream_t s);
+                                                        BulkDev *dev, long long timeout_ns, int stage_off, int te,
+                                                        cudaStream_t s);
 
 #define BH_DEFINE_FILL_TU(DIM, W)                                                                          \
     template <> cudaError_t fill_launch<DIM, W>(const FillP &p, const LaunchCfg &c, cudaStream_t s) {      \
@@ -201,9 +202,9 @@ template <int DIM, bool W> cudaError_t fill_launch_bulk(const FillP &p, const La
         return launch_part1_v<DIM, W>(p, q, vm, rc, grid, smem, s);                                        \
     }                                                                                                      \
     template <> cudaError_t fill_launch_bulk<DIM, W>(const FillP &p, const LaunchCfg &c, BulkCtl *ctl,     \
-                                                     unsigned long long *arrive, long long timeout_ns,     \
-                                                     cudaStream_t s) {                                     \
-        return launch_bulk_w<DIM, W>(p, c, ctl, arrive, timeout_ns, s);                                    \
+                                                     BulkDev *dev, long long timeout_ns, int stage_off,    \
+                                                     int te, cudaStream_t s) {                             \
+        return launch_bulk_w<DIM, W>(p, c, ctl, dev, timeout_ns, stage_off, te, s);                                    \
     }
 
 }  // namespace bh

@@ -60,13 +60,15 @@ struct bh_hist {
     int next_slot = 0;                 // ring position (persists across calls)
     // persistent bulk consumer (bh_bulk_*; bhist_bulk.cuh)
     bh::BulkCtl *bulk_ctl = nullptr;                 // pinned, mapped host memory
-    unsigned long long *bulk_arrive = nullptr;       // device: CTA arrivals, all bulks of the session
+    bh::BulkDev *bulk_dev = nullptr;                 // device: arrivals + the forwarded descriptors
     double *bulk_stage[bh::kBulkRing] = {};          // pinned copies of pageable bulks, per ring slot
     int64_t bulk_stage_cap = 0;                      // doubles per staging slot
     bool bulk_active = false, bulk_weighted = false;
     long long bulk_seq = 0;                          // bulks posted in this session
     long long bulk_timeout_ns = 0;
-    cudaStream_t bulk_stream = nullptr;
+    cudaStream_t bulk_stream = nullptr;              // the caller's stream of the session
+    cudaStream_t bulk_kstream = nullptr;             // the library's stream the resident kernel runs on
+    cudaEvent_t bulk_ev[2] = {};                     // [0] caller's work before begin, [1] kernel done
 };
 
 namespace bh {

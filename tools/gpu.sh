@@ -72,7 +72,11 @@ _build.build(force=True, defines=[d for d in sys.argv[1].split(',') if d])" "$de
           python -c "import json,sys; d=json.load(open(sys.argv[1])); print(sys.argv[2], round(d['ms_per_step'],4), round(d['roofline']['frac'],4))" "$out/env.json" "[$st]" )
       done;;
     sanitize)
-      timeout 1200 python tools/sanitize_run.py > "$out/sanitize.log" 2>&1; echo "sanitize rc=$?"; tail -5 "$out/sanitize.log";;
+      for tool in memcheck racecheck synccheck; do
+        echo "== compute-sanitizer --tool $tool" >> "$out/sanitize.log"
+        timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py >> "$out/sanitize.log" 2>&1
+        echo "$tool rc=$?"; tail -2 "$out/sanitize.log"
+      done;;
     *) echo "unknown job $job"; return 2;;
   esac
 }

@@ -62,6 +62,32 @@ pkg.fill_multi(hs, [h.cols for h in wl.hists], [h.weighted for h in wl.hists], c
 for H in hs:
     H.read()
     H.close()
+# the one-pass fused kernel (NVRTC) of the same set
+hs = [pkg.Histogram(h.axes_spec()) for h in wl.hists]
+pkg.bh_set_debug(hs[0].h, pkg.BH_DEBUG_REQUIRE_JIT)
+pkg.fill_multi(hs, [h.cols for h in wl.hists], [h.weighted for h in wl.hists], cols, cols[wl.wcol],
+               mode=pkg.BH_MULTI_ONE_PASS)
+for H in hs:
+    H.read()
+    H.close()
+# the persistent bulk consumer: TMA-staged (C2 axis, weighted) and direct loads (large PRIV state),
+# pinned and pageable bulks, bulks in flight
+wl = bhgen.workload("C2", n)
+xs, ws = wl.column(0, 0, n), wl.column(wl.wcol, 0, n)
+for axes in (wl.hists[0].axes_spec(), [(13000, 0.0, 1.0)]):
+    H = pkg.Histogram(axes)
+    H.bulk_begin(True, timeout_ms=20000)
+    t = 0
+    for a in range(0, n, 3001):
+        b = min(n, a + 3001)
+        if a % 2:
+            t = H.bulk_submit([torch.from_numpy(xs[a:b]).pin_memory()], torch.from_numpy(ws[a:b]).pin_memory())
+        else:
+            H.bulk_fill([np.ascontiguousarray(xs[a:b])], np.ascontiguousarray(ws[a:b]))
+    H.bulk_wait(t)
+    H.bulk_end()
+    H.read()
+    H.close()
 H = pkg.Histogram([(1000, 0.0, 1.0)])
 pkg.bh_set_chunk(H.h, 4096)
 H.fill_host([torch.from_numpy(rng.random(n)).pin_memory()])

@@ -956,7 +956,7 @@ bh_status bh_bulk_begin(bh_hist *h, int32_t weighted, int32_t timeout_ms, bh_str
     // shared memory for the TMA staging of bulks (two tiles of te events per column), as
     // much as the plan leaves; none: the threads read the host columns directly
     const int ncol = h->dim + (W ? 1 : 0);
-    auto stage_bytes = [&](int te) { return align16((size_t)2 * ncol * (te + 2) * 8 + 16 + (size_t)2 * ncol * 4); };
+    auto stage_bytes = [&](int te) { return align16((size_t)2 * ncol * (te + 4) * 8 + 16 + (size_t)2 * ncol * 4); };
     FillPlan pl;
     int te = 0;
     if (!getenv("BHIST_BULK_NO_TMA"))

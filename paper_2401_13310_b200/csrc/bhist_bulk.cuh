@@ -95,6 +95,12 @@ __device__ __forceinline__ void bulk_mbar_expect_tx(uint64_t *bar, uint32_t byte
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bulk_smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void bulk_mbar_tx(uint64_t *bar, uint32_t bytes) {      // expect, no arrive
+    asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(bulk_smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bulk_smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void bulk_mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
     while (!done)
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     uint32_t phase[2] = {0u, 0u};                 // TMA staging: mbarrier parity per stage
     if (te > 0 && threadIdx.x == 0) {
         constexpr int NCOL = DIM + (W ? 1 : 0);
-        uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + stage_off + 2 * NCOL * (te + 2) * 8);
+        uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + stage_off + 2 * NCOL * (te + 4) * 8);
         bulk_mbar_init(mbar, 1);
         bulk_mbar_init(mbar + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -188,39 +194,67 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
             if (n == -2) return;          // the host went away: leave the state unflushed
             break;                        // end of the sequence
         }
-        // this CTA's contiguous share of the bulk, coalesced over its threads
-        const long long lo = (long long)(((unsigned long long)n * blockIdx.x) / G);
-        const long long hi = (long long)(((unsigned long long)n * (blockIdx.x + 1)) / G);
+        // this CTA's contiguous share of the bulk, its inner boundaries on the 16-byte grid of
+        // the first column (no off-grid ends for the TMA staging when the columns share a phase)
+        const long long ph = (long long)((reinterpret_cast<uintptr_t>(s_x[0]) >> 3) & 1);
+        auto bound = [&](unsigned long long k) -> long long {
+            if (k == 0) return 0;
+            if (k == G) return n;
+            const long long b = ((((long long)(((unsigned long long)n * k) / G)) + ph) & ~1LL) - ph;
+            return b < 0 ? 0 : (b > n ? n : b);
+        };
+        const long long lo = bound(blockIdx.x), hi = bound(blockIdx.x + 1);
         if (te > 0) {
-            // TMA-staged: tiles of te events, stage k % 2; column c of a stage starts at the
-            // 16-byte boundary at or below the tile's first event (shift[c] = 0 or 1 element;
-            // the <= 8 bytes read before / after the tile lie in the same host page)
+            // TMA-staged: tiles of te events, stage k % 2.  Per column the 16-byte-aligned middle
+            // of the tile comes by TMA; a leading / trailing event off the 16-byte grid is loaded
+            // by thread 0 (no byte outside the bulk is read).  Event i of the tile sits at index
+            // i - a0 + 2 - lead of the staged column, so the TMA destination is 16-byte aligned.
             constexpr int NCOL = DIM + (W ? 1 : 0);
-            const int cstride = te + 2;                                  // doubles per staged column
+            const int cstride = te + 4;                                  // doubles per staged column
             double *stg = reinterpret_cast<double *>(smem + stage_off);
             uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + stage_off + 2 * NCOL * cstride * 8);
-            int *shift = reinterpret_cast<int *>(mbar + 2);
+            int *lead = reinterpret_cast<int *>(mbar + 2);
             const long long ntile = (hi - lo + te - 1) / te;
             auto issue = [&](long long k) {                              // thread 0
                 const int st = (int)(k & 1);
                 const long long a0 = lo + k * te, a1 = a0 + te < hi ? a0 + te : hi;
                 uint32_t total = 0;
-                const double *src[NCOL];
+                long long b0[NCOL], b1[NCOL];
 #pragma unroll
                 for (int c = 0; c < NCOL; ++c) {
                     const double *col = c < DIM ? s_x[c] : s_w;
-                    const int sh = (int)((reinterpret_cast<uintptr_t>(col + a0) >> 3) & 1);
-                    src[c] = col + a0 - sh;
-                    shift[st * NCOL + c] = sh;
-                    total += (uint32_t)((((a1 - a0 + sh) * 8) + 15) & ~15LL);
+                    const int ld = (int)((reinterpret_cast<uintptr_t>(col + a0) >> 3) & 1);
+                    b0[c] = a0 + ld;
+                    b1[c] = a1 - (long long)((reinterpret_cast<uintptr_t>(col + a1) >> 3) & 1);
+                    if (b1[c] < b0[c]) b1[c] = b0[c];
+                    lead[st * NCOL + c] = ld;
+                    total += (uint32_t)((b1[c] - b0[c]) * 8);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                bulk_mbar_expect_tx(mbar + st, total);
+                bulk_mbar_tx(mbar + st, total);
 #pragma unroll
                 for (int c = 0; c < NCOL; ++c)
-                    bulk_tma_g2s(stg + (st * NCOL + c) * cstride, src[c],
-                                 (uint32_t)((((a1 - a0 + shift[st * NCOL + c]) * 8) + 15) & ~15LL), mbar + st);
-            };
+                    if (b1[c] > b0[c])
+                        bulk_tma_g2s(stg + (st * NCOL + c) * cstride + 2, (c < DIM ? s_x[c] : s_w) + b0[c],
+                                     (uint32_t)((b1[c] - b0[c]) * 8), mbar + st);
+                // the off-grid ends (<= 2 events per column), all loads in flight together
+                double hv[NCOL], tv[NCOL];
+#pragma unroll
+                for (int c = 0; c < NCOL; ++c) {
+                    const double *col = c < DIM ? s_x[c] : s_w;
+                    const long long t = b1[c] > b0[c] ? b1[c] : b0[c];       // first event after the TMA part
+                    if (b0[c] > a0) hv[c] = ld_host(col + a0);
+                    if (t < a1) tv[c] = ld_host(col + t);
+                }
+#pragma unroll
+                for (int c = 0; c < NCOL; ++c) {
+                    double *dst = stg + (st * NCOL + c) * cstride + 2 - lead[st * NCOL + c];
+                    const long long t = b1[c] > b0[c] ? b1[c] : b0[c];
+                    if (b0[c] > a0) dst[0] = hv[c];
+                    if (t < a1) dst[t - a0] = tv[c];
+                }
+                bulk_mbar_arrive(mbar + st);                             // the phase completes when
+            };                                                           // the TMA bytes land too
             if (threadIdx.x == 0 && ntile > 0) issue(0);
             for (long long k = 0; k < ntile; ++k) {
                 const int st = (int)(k & 1);
@@ -234,8 +268,8 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
                     if (i < a1) {
                         double x[DIM];
 #pragma unroll
-                        for (int a = 0; a < DIM; ++a) x[a] = stg[(st * NCOL + a) * cstride + (i - a0) + shift[st * NCOL + a]];
-                        const double wv = W ? stg[(st * NCOL + NCOL - 1) * cstride + (i - a0) + shift[st * NCOL + NCOL - 1]] : 1.0;
+                        for (int a = 0; a < DIM; ++a) x[a] = stg[(st * NCOL + a) * cstride + (i - a0) + 2 - lead[st * NCOL + a]];
+                        const double wv = W ? stg[(st * NCOL + NCOL - 1) * cstride + (i - a0) + 2 - lead[st * NCOL + NCOL - 1]] : 1.0;
                         do_event<DIM, W, VM>(p, x, wv, sink, acc, smem);
                     }
                 }

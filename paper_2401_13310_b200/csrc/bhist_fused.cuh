@@ -329,9 +329,13 @@ template <class H, class... Rest> struct Proc<H, Rest...> {
     }
 };
 
+// The warp groups of a role run in different branches of run_role, so their block and cluster
+// barriers are the non-.aligned forms (barriers reached from different code locations; every
+// group executes the same number of them).
 __device__ __forceinline__ void cluster_sync_relaxed() {
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed;\n\tbarrier.cluster.wait;" ::: "memory");
 }
+__device__ __forceinline__ void block_sync_any() { asm volatile("barrier.sync 0;" ::: "memory"); }
 
 template <class... Hs> __device__ constexpr unsigned grp_cols(Grp<Hs...> *) { return (0u | ... | Hs::colmask); }
 template <class... Hs> __device__ constexpr bool grp_w(Grp<Hs...> *) { return (false || ... || Hs::W); }
@@ -398,18 +402,18 @@ __device__ __forceinline__ void run_group(const FusedP &p, unsigned char *smem, 
         cur = nxt;
         i0 += stride;
     }
-    __syncthreads();                                     // (1) every group done with the bins
+    block_sync_any();                                     // (1) every group done with the bins
     P::flush(p, smem, tig, ntg);
-    __syncthreads();                                     // (2) bins flushed: scratch is free
+    block_sync_any();                                     // (2) bins flushed: scratch is free
     double *red = reinterpret_cast<double *>(red_base);
     bool *last = reinterpret_cast<bool *>(red + (size_t)P::NSTATS * gw);
     P::warp_stats(red, wg, gw, acc);
-    __syncthreads();                                     // (3)
+    block_sync_any();                                     // (3)
     P::partials(p, red, gw, tig, ntg, cid, 0);
     __threadfence();
-    __syncthreads();                                     // (4)
+    block_sync_any();                                     // (4)
     P::tickets(p, last, tig, 0);
-    __syncthreads();                                     // (5)
+    block_sync_any();                                     // (5)
     __threadfence();
     P::last_sum(p, last, wg, gw, tig, 0);
 }

@@ -327,8 +327,12 @@ def measure_bulk_regime(local: int, total: int = 1 << 25, bulk: int = 32768) -> 
             t = H.bulk_submit([b])
         H.bulk_wait(t)
         H.bulk_end()
-    out["persistent_consumer_per_bulk_events_per_s"] = run(consumer_sync)
-    out["persistent_consumer_pipelined_events_per_s"] = run(consumer_pipelined)
+    for key, fn in (("persistent_consumer_per_bulk_events_per_s", consumer_sync),
+                    ("persistent_consumer_pipelined_events_per_s", consumer_pipelined)):
+        try:
+            out[key] = run(fn)
+        except pkg.BHistError as e:       # e.g. under a profiler that serializes kernel launches,
+            out[key] = f"unavailable: {e}"    # the resident kernel never sees a bulk (times out)
     sweep = {}
     for chunk in (bulk, 1 << 18, 1 << 20, 1 << 22):
         pkg.bh_set_chunk(H.h, chunk)

@@ -535,6 +535,9 @@ struct WarpHot {
 #ifndef BH_LANE_CACHE
 #define BH_LANE_CACHE 1
 #endif
+#ifndef BH_LANE_CACHE_U      // the same for CACHE's unit-weight counts (no warp aggregation behind it):
+#define BH_LANE_CACHE_U 1    // C4 1.32 -> 1.19 ms, C5 5.47 -> 5.42 ms; uniform C3 forced to CACHE
+#endif                       // 1.81 -> 1.99 ms (AUTO runs C3 through SORT)
 struct RegHot {
     int g = -1;
     uint32_t n = 0, miss = 0;
@@ -757,6 +760,15 @@ struct CacheSink {
         return k == g ? sl : -1;
     }
     RegHot lc;        // W: this thread's hot bin (in front of the warp aggregation)
+    // unit weights: the thread's hot bin as a register count (same stickiness rule as RegHot);
+    // the other events go one by one to their slot or the global count, no warp aggregation
+    int ug = -1;
+    uint32_t un = 0, umiss = 0;
+    __device__ __forceinline__ void put_count(int g, uint32_t c) {
+        const int sl = lookup((uint32_t)g);
+        if (sl >= 0) atomicAdd(reinterpret_cast<uint32_t *>(vals) + sl, c);
+        else atomicAdd(pp->count + g, (unsigned long long)c);
+    }
     __device__ __forceinline__ void add(int g, double w) {
 #if BH_LANE_CACHE
         if (W) {
@@ -765,6 +777,17 @@ struct CacheSink {
             int og;
             if (lc.step(g, w, og, on, o1, o2)) return;
             add_item(og, on != 0, o1, o2);
+            return;
+        }
+#endif
+#if BH_LANE_CACHE_U
+        if (!W) {
+            if (g == ug) { ++un; return; }
+            if (un >= 2 && umiss < 4 * un) { ++umiss; put_count(g, 1u); return; }
+            if (un) put_count(ug, un);
+            ug = g;
+            un = 1;
+            umiss = 0;
             return;
         }
 #endif
@@ -822,6 +845,11 @@ struct CacheSink {
         }
     }
     __device__ __forceinline__ void drain() {
+        if (!W && BH_LANE_CACHE_U && un) {
+            put_count(ug, un);
+            un = 0;
+            ug = -1;
+        }
         if (W && BH_LANE_CACHE) {
             int og;
             uint32_t on;

@@ -535,6 +535,9 @@ struct WarpHot {
 #ifndef BH_LANE_CACHE
 #define BH_LANE_CACHE 1
 #endif
+#ifndef BH_CACHE_W_AGG       // CACHE weighted: combine the lanes' items of equal bins before the put
+#define BH_CACHE_W_AGG 1     // (0: one put per lane -- C4w 3.36 -> 8.72 ms: the float64 exchanges on
+#endif                       // a warm slot serialize, unlike the native u32 atomics of unit counts)
 #ifndef BH_LANE_CACHE_U      // the same for CACHE's unit-weight counts (no warp aggregation behind it):
 #define BH_LANE_CACHE_U 1    // C4 1.32 -> 1.19 ms, C5 5.47 -> 5.42 ms; uniform C3 forced to CACHE
 #endif                       // 1.81 -> 1.99 ms (AUTO runs C3 through SORT)
@@ -820,6 +823,10 @@ struct CacheSink {
     // with has=true: equal bins of the warp combine first (match.any + a shuffle walk over
     // the peer mask), then the group leader puts the sums
     __device__ __forceinline__ void add_item(int g, bool has, double w1, double w2) {
+#if !BH_CACHE_W_AGG
+        if (has) put(g, w1, w2);
+        return;
+#endif
         const unsigned act = __ballot_sync(__activemask(), has);
         if (!has) return;
         const unsigned peers = __match_any_sync(act, g);

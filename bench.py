@@ -333,6 +333,10 @@ def measure_bulk_regime(local: int, total: int = 1 << 25, bulk: int = 32768) -> 
             out[key] = run(fn)
         except pkg.BHistError as e:       # e.g. under a profiler that serializes kernel launches,
             out[key] = f"unavailable: {e}"    # the resident kernel never sees a bulk (times out)
+            try:
+                H.bulk_end()              # close the abandoned session (reports the timeout again)
+            except pkg.BHistError:
+                pass
     sweep = {}
     for chunk in (bulk, 1 << 18, 1 << 20, 1 << 22):
         pkg.bh_set_chunk(H.h, chunk)

@@ -956,11 +956,14 @@ bh_status bh_bulk_begin(bh_hist *h, int32_t weighted, int32_t timeout_ms, bh_str
     // shared memory for the TMA staging of bulks (two tiles of te events per column), as
     // much as the plan leaves; none: the threads read the host columns directly
     const int ncol = h->dim + (W ? 1 : 0);
-    auto stage_bytes = [&](int te) { return align16((size_t)2 * ncol * (te + 4) * 8 + 16 + (size_t)2 * ncol * 4); };
+    auto stage_bytes = [&](int te) {      // kBulkStages stages + full/empty barriers + tile records
+        return align16((size_t)kBulkStages * ncol * (te + 4) * 8 + 16 * kBulkStages + sizeof(BulkTile) * kBulkStages +
+                       sizeof(BulkDesc) + 16);
+    };
     FillPlan pl;
     int te = 0;
     if (!getenv("BHIST_BULK_NO_TMA"))
-        for (int t : {2048, 1024, 512, 256}) {
+        for (int t : {1024, 512, 256, 128}) {
             FillPlan q;
             if (plan_fill(h, W, q, int64_t(1) << 40, stage_bytes(t)) == BH_OK) { pl = q; te = t; break; }
         }

@@ -239,7 +239,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
         if (threadIdx.x == 0) {
             for (int s = 0; s < kBulkStages; ++s) {
                 bulk_mbar_init(full + s, 1);
-                bulk_mbar_init(empty + s, (uint32_t)(nw - 1));
+                bulk_mbar_init(empty + s, (uint32_t)((nw - 1) * 32));   // every consumer thread
             }
             bulk_mbar_init(lbar, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -376,8 +376,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
                         do_event<DIM, W, VM>(p, x, wv, sink, acc, smem);
                     }
                 }
-                __syncwarp();
-                if (lane == 0) bulk_mbar_arrive(empty + st);    // stage consumed by this warp
+                bulk_mbar_arrive(empty + st);                   // this thread is done with the stage
             }
         }
         __syncthreads();

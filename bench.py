@@ -445,6 +445,9 @@ def run_gpu(args):
     if world > 1:        # one pack (+ one unpack where the sum lands) per step, counted by the library
         pass
     ms = t0.elapsed_time(t1)
+    # the strategy the timed fills ran (AUTO's device-side SORT decision is reset by the e2e leg)
+    names = {0: "auto", 1: "priv", 2: "global", 3: "cache", 4: "exact", 5: "sort"}
+    strat = f"bh_fill_multi, plan: {args.multi_mode}" if multi else names[Hs[0].strategy(hists[0].weighted)]
     fill_ms = [a.elapsed_time(b) for a, b in fill_ev]
     if world > 1:
         m = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -538,9 +541,6 @@ def run_gpu(args):
         fill_avg = float(np.mean(fill_ms))
         achieved = bpe * N / (fill_avg * 1e-3) / 1e9
         traffic = ncu_traffic(wl.name)
-        names = {0: "auto", 1: "priv", 2: "global", 3: "cache", 4: "exact", 5: "sort"}
-        strat = f"bh_fill_multi, plan: {args.multi_mode}" if multi else \
-            names[Hs[0].strategy(hists[0].weighted)]
         clocks = clk.summary()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

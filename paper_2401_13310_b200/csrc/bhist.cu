@@ -736,11 +736,10 @@ bh_status bh_reset(bh_hist *h, bh_stream s) {
     if (bulk_check(h)) return BH_EINVAL;
     DeviceGuard dg(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(s);
-    CUDA_TRY(cudaMemsetAsync(h->count, 0, sizeof(unsigned long long) * h->G, st));
-    CUDA_TRY(cudaMemsetAsync(h->sumw, 0, sizeof(double) * h->G, st));
-    CUDA_TRY(cudaMemsetAsync(h->sumw2, 0, sizeof(double) * h->G, st));
-    CUDA_TRY(cudaMemsetAsync(h->stats, 0, sizeof(double) * 16, st));
-    CUDA_TRY(cudaMemsetAsync(h->entries, 0, sizeof(unsigned long long), st));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((h->G / 2 + 255) / 256, (int64_t)h->nsm * 8));
+    k_reset<<<grid, 256, 0, st>>>((int)h->G, h->count, h->sumw, h->sumw2, h->stats, h->entries);
+    CUDA_TRY(cudaGetLastError());
+    ++h->launches;
     h->weighted_content = false;
     h->probe_state = 0;                  // AUTO re-decides SORT vs CACHE on the next large fill
     return BH_OK;

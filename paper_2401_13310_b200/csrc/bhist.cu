@@ -978,7 +978,7 @@ bh_status bh_bulk_begin(bh_hist *h, int32_t weighted, int32_t timeout_ms, bh_str
     p.cache_slots = cache_slots_for(W);
     p.replicas = pl.replicas;
     p.wc_off = pl.wc_off;
-    c.grid = h->nsm * resident_blocks(c.strategy);   // every CTA resident: each one takes a share of every bulk
+    c.grid = h->nsm;                  // x the resident CTAs per SM (launch_bulk_s, occupancy query)
     const long long tmo = (long long)(timeout_ms ? timeout_ms : 10000) * 1000000LL;
     cudaError_t e;
     switch (h->dim) {

@@ -155,7 +155,12 @@ cudaError_t launch_bulk_s(const FillP &p, const LaunchCfg &c, BulkCtl *ctl, Bulk
     auto kern = c.vm == 0 ? k_bulk<DIM, W, SINK, 0>
                           : c.vm == 1 ? k_bulk<DIM, W, SINK, 1> : c.vm == 3 ? k_bulk<DIM, W, SINK, 3> : k_bulk<DIM, W, SINK, 2>;
     if (cudaError_t r = ensure_smem(reinterpret_cast<const void *>(kern), c.smem)) return r;
-    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p, ctl, dev, timeout_ns, stage_off, te);
+    // every CTA must be resident at once (each takes a share of every bulk): c.grid is the SM
+    // count, times the CTAs per SM the kernel's shared memory and registers allow
+    int per_sm = 0;
+    if (cudaError_t r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ThreadsOf<SINK>::v, c.smem)) return r;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    kern<<<c.grid * per_sm, ThreadsOf<SINK>::v, c.smem, s>>>(p, ctl, dev, timeout_ns, stage_off, te);
     return cudaGetLastError();
 }
 

@@ -139,3 +139,34 @@ def test_bulk_consumer_times_out_and_releases_the_gpu():
     h.fill([torch.from_numpy(x).cuda()])
     compare(h.read(), oracle.OracleHist(axes).fill([x]).read(), False, "after timeout")
     h.close()
+
+
+@pytest.mark.parametrize("case", ["priva 50x50 peaked", "cache 1M weighted", "direct 13000 weighted", "global 3d"])
+def test_bulk_every_sink_and_the_direct_path(case):
+    """Weighted sessions through the collision-adaptive PRIV sink (peaked 2-D), the CACHE sink
+    (1M weighted cells), a private state too large to leave shared memory for the TMA staging
+    (threads read the host columns directly), and a forced GLOBAL 3-D histogram."""
+    rng = np.random.default_rng(17)
+    n = 300_007
+    x = 0.505 + 0.002 * np.tan(np.pi * (rng.random(n) - 0.5))
+    y = rng.normal(0.5, 0.05, n)
+    z = rng.uniform(-0.1, 1.1, n)
+    w = rng.uniform(0.5, 1.5, n)
+    strategy = pkg.BH_STRATEGY_AUTO
+    if case.startswith("priva"):
+        axes, cols = [(50, 0.0, 1.0), (50, 0.0, 1.0)], [x, y]
+    elif case.startswith("cache"):
+        axes, cols = [(1000, 0.0, 1.0), (1000, 0.0, 1.0)], [z, y]
+    elif case.startswith("direct"):
+        axes, cols = [(13000, 0.0, 1.0)], [z]
+    else:
+        axes, cols, strategy = [(20, 0.0, 1.0)] * 3, [x, y, z], pkg.BH_STRATEGY_GLOBAL
+    h = pkg.Histogram(axes, strategy=strategy)
+    h.bulk_begin(True)
+    t = 0
+    for a, b in _splits(n, [32768, 7, 65536]):
+        t = h.bulk_submit([_pinned(c[a:b]) for c in cols], _pinned(w[a:b]))
+        h.bulk_wait(t)
+    h.bulk_end()
+    compare(h.read(), oracle.OracleHist(axes).fill(cols, w).read(), True, f"bulk {case}")
+    h.close()

@@ -145,7 +145,10 @@ FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, cons
     return p;
 }
 
-int threads_of(int strategy, bool) { return strategy == BH_STRATEGY_GLOBAL ? kThreadsGlobal : kThreadsSmem; }
+int threads_of(int strategy, bool weighted, int dim = 0) {     // dim: k_fill's FillThreads rule
+    if (strategy == BH_STRATEGY_CACHE && weighted && dim == 3) return 768;
+    return strategy == BH_STRATEGY_GLOBAL ? kThreadsGlobal : kThreadsSmem;
+}
 int resident_blocks(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? 2 : 1; }
 
 // Shared-memory plan of one fill: strategy, variable-axis tables (VSM), PRIV replicas.
@@ -226,7 +229,7 @@ bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n, si
 // Persistent grid (resident CTAs on every SM), but each block should see enough events
 // to amortize zeroing + flushing its private bins.
 int grid_for(const bh_hist *h, const LaunchCfg &c, int64_t m) {
-    const int nt = threads_of(c.strategy, c.weighted);
+    const int nt = threads_of(c.strategy, c.weighted, h->dim);
     // small fills are latency-bound: spread them over many SMs (>= 2 events per thread);
     // PRIV blocks must still amortize zeroing + flushing their private bins (>= 8 events
     // per thread and >= 4 G per block: measured best for C1's 1e6 events)

@@ -38,6 +38,12 @@ constexpr int kThreadsSmem = BH_SMEM_THREADS;   // PRIV / CACHE sinks: 1 CTA/SM 
 template <int SINK> struct ThreadsOf {   // SINK_GLOBAL == 1
     static constexpr int v = SINK == 1 ? kThreadsGlobal : kThreadsSmem;
 };
+// k_fill: the weighted 3-D CACHE fill (11 float64 stats, the register hot bin, warp
+// aggregation) spills at 64 registers/thread; 768 threads (80 registers) measured C4w 3.43 ->
+// 3.12 ms, while every other shape is faster at 1024 (C4 1.19 vs 1.37 ms)
+template <int SINK, int DIM, bool W> struct FillThreads {    // SINK_CACHE == 2
+    static constexpr int v = (SINK == 2 && W && DIM == 3) ? 768 : ThreadsOf<SINK>::v;
+};
 
 // Streaming (evict-first) loads of the input columns: each byte is read once.
 __device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }
@@ -926,7 +932,7 @@ struct Batch {            // U event pairs of every column, held in registers (x
 // leading events; the next batch is loaded before the current one is processed
 // (register double-buffering) so each thread keeps 2*U*ncol 16-byte loads in flight.
 template <int DIM, bool W, int SINK, bool VEC, int VM>
-__global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
+__global__ void __launch_bounds__((FillThreads<SINK, DIM, W>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (gated_off(p.gate, p.gate_run)) return;          // (uniform: the whole grid exits)
     using Sink_t = typename SinkOf<SINK, W>::T;

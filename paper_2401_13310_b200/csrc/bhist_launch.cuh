@@ -49,7 +49,7 @@ template <int DIM, bool W, int SINK, bool VEC, int VM>
 cudaError_t launch_t(const FillP &p, const LaunchCfg &c, cudaStream_t s) {
     auto kern = k_fill<DIM, W, SINK, VEC, VM>;
     if (cudaError_t e = ensure_smem(reinterpret_cast<const void *>(kern), c.smem)) return e;
-    kern<<<c.grid, ThreadsOf<SINK>::v, c.smem, s>>>(p);
+    kern<<<c.grid, FillThreads<SINK, DIM, W>::v, c.smem, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -134,8 +134,7 @@ FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, cons
     p.G = (int32_t)h->G;
     p.K = h->K;
     p.count = h->count;
-    p.sumw = h->sumw;
-    p.sumw2 = h->sumw2;
+    p.sw = h->sw;
     p.partials = h->partials;
     p.counter = h->counter;
     p.stats = h->stats;
@@ -164,11 +163,11 @@ struct FillPlan {
 // through CACHE (warp-aggregated, hot-bin safe) instead.
 bool small_fill(const bh_hist *h, int64_t n) { return n < 2 * h->G * (int64_t)h->nsm; }
 
-bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n, size_t reserve = 0) {
+bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n, size_t reserve = 0, int force = -1) {
     LaunchCfg &c = pl.c;
     c.weighted = weighted;
-    c.strategy = resolve_one_pass(h, c.weighted);
-    if (c.strategy == BH_STRATEGY_PRIV && (h->strategy == BH_STRATEGY_AUTO || h->strategy == BH_STRATEGY_EXACT) &&
+    c.strategy = force >= 0 ? force : resolve_one_pass(h, c.weighted);
+    if (force < 0 && c.strategy == BH_STRATEGY_PRIV && (h->strategy == BH_STRATEGY_AUTO || h->strategy == BH_STRATEGY_EXACT) &&
         small_fill(h, n))
         c.strategy = BH_STRATEGY_CACHE;
     size_t sink = sink_bytes(h, c.strategy, c.weighted);
@@ -268,7 +267,7 @@ bh_status fill_exact(bh_hist *h, int64_t n, const double *const *coords, const d
         default: k_fill_exact<3><<<g2, 512, 0, s>>>(p, h->limbs, h->maxbits); break;
         }
         const int g3 = (int)std::min<int64_t>((h->G + 255) / 256, (int64_t)h->nsm * 8);
-        k_exact_fold<<<g3, 256, 0, s>>>((int)h->G, h->limbs, h->maxbits, h->sumw, h->sumw2);
+        k_exact_fold<<<g3, 256, 0, s>>>((int)h->G, h->limbs, h->maxbits, h->sw);
         CUDA_TRY(cudaGetLastError());
         h->launches += 3;
     }
@@ -394,29 +393,33 @@ bh_status fill_sort(bh_hist *h, int64_t n, const double *const *coords, const do
     return BH_OK;
 }
 
-// AUTO and SORT (measured: SORT 1.45x faster than CACHE on spread-out unit-weight data,
-// several times slower with a hot partition or weights, and its per-chunk merge only
-// amortizes over >= ~8 x #SM x 2^pb events).  The first large unit-weight fill after
-// create/reset launches k_part_probe on a strided sample of its own events; the probe
-// writes the decision to device memory (SORT if no partition holds > 5% of the sample and
-// no hashed bin bucket > 1%: a hot bin contends in pass 2), and that fill and every later
-// eligible one launch BOTH paths, each gated on the device flag (the other exits at
-// once).  The choice therefore depends on the data only, never on host timing, and the
-// host never waits for it.  Returns the device flag, or nullptr (plain CACHE).
+// AUTO for bin spaces that do not fit PRIV (measured: SORT 1.45x faster than CACHE on
+// spread-out unit-weight data, several times slower with a hot partition or weights, and its
+// per-chunk merge only amortizes over >= ~8 x #SM x 2^pb events; for weights, GLOBAL's
+// paired-lane REDs are 1.6x faster than CACHE on spread-out data (C3w 2.0 vs 3.2 ms) and
+// ~40x slower on a hot bin (C4w), whose same-address REDs serialize in L2).  The first large
+// fill after create/reset launches k_part_probe on a strided sample of its own events; the
+// probe writes both decisions to device memory (unit weights: SORT if no partition holds
+// > 5% of the sample and no hashed bin bucket > 1%; weights: GLOBAL if no bucket holds
+// > 0.2%), and that fill and every later eligible one launch BOTH paths, each gated on the
+// device flag (the other exits at once).  The choice therefore depends on the data only,
+// never on host timing, and the host never waits for it.  Returns the device flag of this
+// fill's choice (1: SORT / GLOBAL), or nullptr (plain CACHE).
 constexpr int kProbeSamples = 1 << 14;     // one CTA: ~40 us, once per histogram and reset
-const int32_t *auto_sort_gate(bh_hist *h, int64_t n, const double *const *coords, cudaStream_t s) {
-    if (h->strategy != BH_STRATEGY_AUTO || resolve_strategy(h, false) != BH_STRATEGY_CACHE) return nullptr;
+const int32_t *auto_gate(bh_hist *h, int64_t n, const double *const *coords, bool weighted, cudaStream_t s) {
+    if (h->strategy != BH_STRATEGY_AUTO || resolve_strategy(h, weighted) != BH_STRATEGY_CACHE) return nullptr;
     const int P = (int)sort_partitions(h, false);
-    if (P > kPartMaxP || n < 8LL * h->nsm * (1LL << sort_pb(false)) || getenv("BHIST_NO_AUTO_SORT")) return nullptr;
+    if (P > kPartMaxP || n < 8LL * h->nsm * (1LL << sort_pb(false))) return nullptr;
+    if (getenv(weighted ? "BHIST_NO_AUTO_GLOBAL" : "BHIST_NO_AUTO_SORT")) return nullptr;
     if (!h->probe_dev) {
-        if (cudaMalloc(reinterpret_cast<void **>(&h->probe_dev), 3 * sizeof(unsigned int)) != cudaSuccess) {
+        if (cudaMalloc(reinterpret_cast<void **>(&h->probe_dev), 4 * sizeof(unsigned int)) != cudaSuccess) {
             cudaGetLastError();
             return nullptr;                                  // no probe: stay on CACHE
         }
     }
     if (h->probe_state == 0) {
         FillP p = make_params(h, n, coords, nullptr);
-        if (cudaMemsetAsync(h->probe_dev, 0, 3 * sizeof(unsigned int), s) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        if (cudaMemsetAsync(h->probe_dev, 0, 4 * sizeof(unsigned int), s) != cudaSuccess) { cudaGetLastError(); return nullptr; }
         const size_t sm = sizeof(unsigned int) * (P + kProbeHash);
         switch (h->dim) {
         case 1: k_part_probe<1><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, h->probe_dev); break;
@@ -427,7 +430,7 @@ const int32_t *auto_sort_gate(bh_hist *h, int64_t n, const double *const *coords
         h->launches++;
         h->probe_state = 1;                                   // decided (on the device)
     }
-    return reinterpret_cast<const int32_t *>(h->probe_dev + 2);
+    return reinterpret_cast<const int32_t *>(h->probe_dev + (weighted ? 3 : 2));
 }
 
 // One fill over device-resident columns, split into launches of <= 2^30 events.
@@ -435,11 +438,13 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
     if (w) h->weighted_content = true;
     if (w && h->strategy == BH_STRATEGY_EXACT) return fill_exact(h, n, coords, w, s);
     if (resolve_strategy(h, w != nullptr) == BH_STRATEGY_SORT) return fill_sort(h, n, coords, w, s);
-    const int32_t *gate = w ? nullptr : auto_sort_gate(h, n, coords, s);
-    if (gate)                                                 // SORT, run iff the device flag says so
+    const int32_t *gate = auto_gate(h, n, coords, w != nullptr, s);
+    if (gate && !w)                                           // SORT, run iff the device flag says so
         if (bh_status r = fill_sort(h, n, coords, w, s, gate)) return r;
-    FillPlan pl;
+    FillPlan pl, pg;                                          // pg: weighted GLOBAL, run iff the flag says so
     if (bh_status r = plan_fill(h, w != nullptr, pl, n)) return r;
+    if (gate && w)
+        if (bh_status r = plan_fill(h, true, pg, n, 0, BH_STRATEGY_GLOBAL)) return r;
     LaunchCfg &c = pl.c;
     const int64_t kMaxLaunch = int64_t(1) << 30;   // in-kernel event indices are int32
     for (int64_t off = 0; off < n; off += kMaxLaunch) {
@@ -463,6 +468,21 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         p.wc_off = pl.wc_off;
         c.grid = grid_for(h, c, m);
         cudaError_t e;
+        if (gate && w) {                                      // weighted AUTO: the gated GLOBAL fill first
+            FillP pq = p;
+            for (int a = 0; a < h->dim; ++a) pq.ax[a] = pg.ax[a];
+            pq.gate_run = 1;
+            LaunchCfg &cg = pg.c;
+            cg.vec = c.vec;
+            cg.grid = grid_for(h, cg, m);
+            switch (h->dim) {
+            case 1: e = fill_launch<1, true>(pq, cg, s); break;
+            case 2: e = fill_launch<2, true>(pq, cg, s); break;
+            default: e = fill_launch<3, true>(pq, cg, s); break;
+            }
+            if (e != cudaSuccess) return fail(BH_ECUDA, "fill launch: %s", cudaGetErrorString(e));
+            ++h->launches;
+        }
         switch (h->dim) {
         case 1: e = c.weighted ? fill_launch<1, true>(p, c, s) : fill_launch<1, false>(p, c, s); break;
         case 2: e = c.weighted ? fill_launch<2, true>(p, c, s) : fill_launch<2, false>(p, c, s); break;
@@ -600,8 +620,7 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
         }                                                                                          \
     } while (0)
     ALLOC(h->count, sizeof(unsigned long long) * G);
-    ALLOC(h->sumw, sizeof(double) * G);
-    ALLOC(h->sumw2, sizeof(double) * G);
+    ALLOC(h->sw, 2 * sizeof(double) * G);
     ALLOC(h->stats, sizeof(double) * 16);
     ALLOC(h->entries, sizeof(unsigned long long));
     ALLOC(h->partials, sizeof(double) * 16 * h->max_grid);
@@ -684,8 +703,7 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
     }
 #undef ALLOC
     if (cudaMemset(h->count, 0, sizeof(unsigned long long) * G) != cudaSuccess ||
-        cudaMemset(h->sumw, 0, sizeof(double) * G) != cudaSuccess ||
-        cudaMemset(h->sumw2, 0, sizeof(double) * G) != cudaSuccess ||
+        cudaMemset(h->sw, 0, 2 * sizeof(double) * G) != cudaSuccess ||
         cudaMemset(h->stats, 0, sizeof(double) * 16) != cudaSuccess ||
         cudaMemset(h->entries, 0, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMemset(h->counter, 0, sizeof(unsigned int)) != cudaSuccess)
@@ -708,8 +726,7 @@ bh_status bh_destroy(bh_hist *h) {
     for (int i = 0; i < kBulkRing; ++i)
         if (h->bulk_stage[i]) cudaFreeHost(h->bulk_stage[i]);
     cudaFree(h->count);
-    cudaFree(h->sumw);
-    cudaFree(h->sumw2);
+    cudaFree(h->sw);
     cudaFree(h->stats);
     cudaFree(h->entries);
     cudaFree(h->partials);
@@ -740,7 +757,7 @@ bh_status bh_reset(bh_hist *h, bh_stream s) {
     DeviceGuard dg(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(s);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((h->G / 2 + 255) / 256, (int64_t)h->nsm * 8));
-    k_reset<<<grid, 256, 0, st>>>((int)h->G, h->count, h->sumw, h->sumw2, h->stats, h->entries);
+    k_reset<<<grid, 256, 0, st>>>((int)h->G, h->count, h->sw, h->stats, h->entries);
     CUDA_TRY(cudaGetLastError());
     ++h->launches;
     h->weighted_content = false;
@@ -1248,8 +1265,7 @@ bh_status bh_fill_multi(bh_hist *const *hs, int32_t nh, const int32_t *col_of_ax
                 }
             }
             M.count = H->count;
-            M.sumw = H->sumw;
-            M.sumw2 = H->sumw2;
+            M.sw = H->sw;
             M.stats = H->stats;
             M.partials = H->partials;
             M.entries = H->entries;
@@ -1403,7 +1419,7 @@ bh_status bh_pack(const bh_hist *h, double *dev_out, bh_stream s) {
     DeviceGuard dg(h->device);
     const int64_t tot = 2 * h->G + h->K + 1;
     const int grid = (int)std::min<int64_t>((tot + 255) / 256, (int64_t)h->nsm * 8);
-    k_pack<<<grid, 256, 0, static_cast<cudaStream_t>(s)>>>((int)h->G, h->K, h->count, h->sumw, h->sumw2, h->stats,
+    k_pack<<<grid, 256, 0, static_cast<cudaStream_t>(s)>>>((int)h->G, h->K, h->count, h->sw, h->stats,
                                                             h->entries, dev_out);
     CUDA_TRY(cudaGetLastError());
     const_cast<bh_hist *>(h)->launches++;
@@ -1416,7 +1432,7 @@ bh_status bh_unpack(bh_hist *h, const double *dev_in, bh_stream s) {
     DeviceGuard dg(h->device);
     const int64_t tot = 2 * h->G + h->K + 1;
     const int grid = (int)std::min<int64_t>((tot + 255) / 256, (int64_t)h->nsm * 8);
-    k_unpack<<<grid, 256, 0, static_cast<cudaStream_t>(s)>>>((int)h->G, h->K, h->count, h->sumw, h->sumw2, h->stats,
+    k_unpack<<<grid, 256, 0, static_cast<cudaStream_t>(s)>>>((int)h->G, h->K, h->count, h->sw, h->stats,
                                                               h->entries, dev_in);
     CUDA_TRY(cudaGetLastError());
     h->launches++;
@@ -1445,8 +1461,7 @@ bh_status pack_plan(bh_hist *const *hs, int32_t nh, const uint8_t *unit, PackMul
         D.K = h->K;
         D.unit = u ? 1 : 0;
         D.count = h->count;
-        D.sumw = h->sumw;
-        D.sumw2 = h->sumw2;
+        D.sw = h->sw;
         D.stats = h->stats;
         D.entries = h->entries;
         off += (u ? 1 : 2) * h->G + h->K + 1;
@@ -1523,13 +1538,14 @@ bh_status bh_get_strategy(const bh_hist *h, int32_t weighted, int32_t *strategy)
     if (check_hist(h)) return BH_EINVAL;
     if (!strategy) return fail(BH_EINVAL, "NULL output");
     *strategy = (weighted && h->strategy == BH_STRATEGY_EXACT) ? BH_STRATEGY_EXACT : resolve_strategy(h, weighted != 0);
-    // AUTO's large unit-weight fills after the probe decided (on the device) for SORT
-    if (!weighted && h->strategy == BH_STRATEGY_AUTO && h->probe_state == 1 && h->probe_dev) {
+    // AUTO's large fills after the probe decided (on the device) for SORT (unit weights) or
+    // GLOBAL (weights)
+    if (h->strategy == BH_STRATEGY_AUTO && *strategy == BH_STRATEGY_CACHE && h->probe_state == 1 && h->probe_dev) {
         DeviceGuard dg(h->device);
         unsigned int flag = 0;
-        if (cudaMemcpy(&flag, h->probe_dev + 2, sizeof flag, cudaMemcpyDeviceToHost) != cudaSuccess)
+        if (cudaMemcpy(&flag, h->probe_dev + (weighted ? 3 : 2), sizeof flag, cudaMemcpyDeviceToHost) != cudaSuccess)
             return fail(BH_ECUDA, "reading the AUTO decision: %s", cudaGetErrorString(cudaGetLastError()));
-        if (flag == 1) *strategy = BH_STRATEGY_SORT;
+        if (flag == 1) *strategy = weighted ? BH_STRATEGY_GLOBAL : BH_STRATEGY_SORT;
     }
     return BH_OK;
 }

@@ -34,7 +34,7 @@ struct FusedH {
     int32_t st1, st2, G, K;
     int32_t smem_off;             // PRIV sinks: byte offset of the private bins
     unsigned long long *count;    // unit-weight counts [G]
-    double *sumw, *sumw2;         // weighted sums [G]
+    double *sw;                   // weighted (sum w, sum w^2) pairs [2G]
     double *stats, *partials;     // running stats [K]; per-cluster partials [nclusters * K]
     unsigned long long *entries;
     unsigned int *counter;        // last-CTA ticket of this histogram
@@ -190,17 +190,17 @@ __device__ __forceinline__ void fused_sink(const FusedH &F, int g, double w, boo
         const unsigned peers = __match_any_sync(act, g);
         double s1, s2;
         unsigned cnt;
-        if (!agg_group<H::W>(act, peers, w, s1, s2, cnt)) return;
+        const bool lead = agg_group<H::W>(act, peers, w, s1, s2, cnt);
+        if constexpr (H::SINK == FS_GLOBAL_AGG && H::W) {    // group sums: paired-lane REDs
+            red_sw_pairs(act, __ballot_sync(act, lead), F.sw, g, s1, s2);
+            return;
+        }
+        if (!lead) return;
         if constexpr (H::SINK == FS_PRIV_AGG) {
             if constexpr (H::W) add2_shared(reinterpret_cast<double2 *>(smem + F.smem_off) + g, s1, s2);
             else atomicAdd(reinterpret_cast<uint32_t *>(smem + F.smem_off) + g, cnt);
-        } else {
-            if constexpr (H::W) {
-                atomicAdd(F.sumw + g, s1);
-                atomicAdd(F.sumw2 + g, s2);
-            } else {
-                atomicAdd(F.count + g, (unsigned long long)cnt);
-            }
+        } else if constexpr (!H::W) {
+            atomicAdd(F.count + g, (unsigned long long)cnt);
         }
     }
 }
@@ -268,12 +268,9 @@ template <class H, class... Rest> struct Proc<H, Rest...> {
         const FusedH &F = p.h[H::ID];
         if constexpr (H::SINK != FS_GLOBAL_AGG) {
             if constexpr (H::W) {
-                const double2 *d = reinterpret_cast<const double2 *>(smem + F.smem_off);
-                for (int i = tig; i < F.G; i += ntg) {
-                    const double2 v = d[i];
-                    if (v.x != 0.0) atomicAdd(F.sumw + i, v.x);
-                    if (v.y != 0.0) atomicAdd(F.sumw2 + i, v.y);
-                }
+                const double *d = reinterpret_cast<const double *>(smem + F.smem_off);
+                for (int i = tig; i < 2 * F.G; i += ntg)
+                    if (d[i] != 0.0) atomicAdd(F.sw + i, d[i]);
             } else {
                 const uint32_t *c = reinterpret_cast<const uint32_t *>(smem + F.smem_off);
                 for (int i = tig; i < F.G; i += ntg)

@@ -88,8 +88,8 @@ struct FillP {
     int32_t wc_off;          // weighted PRIV: byte offset of the per-warp hot-bin caches (-1: none,
                              // plain CAS sink; >= 0: collision-adaptive sink SINK_PRIVA)
     unsigned long long *count;   // unit-weight counts [G]
-    double *sumw;                // weighted sums [G]
-    double *sumw2;               // weighted sums of squares [G]
+    double *sw;                  // weighted (sum w, sum w^2) of bin g at sw[2g], sw[2g+1]: one 16-byte
+                                 // cell per bin, so one warp RED instruction can add both (red_sw_pairs)
     double *partials;            // [gridDim.x * K]
     unsigned int *counter;       // last-CTA ticket
     double *stats;               // [K], running totals
@@ -442,6 +442,40 @@ __device__ __forceinline__ int add2_shared_count(double2 *cell, double w, double
 
 __device__ __forceinline__ void add2_shared(double2 *cell, double w, double w2) { (void)add2_shared_count(cell, w, w2); }
 
+// Global (sum w, sum w^2) of bin g: sw[2g], sw[2g+1], one 16-byte cell.  The L2 atomic units
+// serve one request per 32-byte sector, not per element: two lanes adding the two halves of
+// one cell in the SAME warp RED instruction cost one request, the same as one u64 RED
+// (tools/microbench/mb6.cu on 1M random cells: 193 G (w, w^2) pairs/s paired vs 96 G/s with
+// the halves in two instructions; u64 192 G/s).
+__device__ __forceinline__ void red_sw(double *sw, int g, double a, double b) {
+    atomicAdd(sw + 2 * (size_t)g, a);
+    atomicAdd(sw + 2 * (size_t)g + 1, b);
+}
+
+// Warp-cooperative (a, b) adds into the global cells: every lane of `act` calls this; the lanes
+// in `ib` (a subset of act) each hold one item (g, a, b).  Participating lanes pair up by rank in
+// act -- the even one adds an item's a, the odd one its b, in one RED instruction -- so each
+// round adds floor(|act| / 2) items with one sector request each.
+__device__ __forceinline__ void red_sw_pairs(unsigned act, unsigned ib, double *sw, int g, double a, double b) {
+    if (ib == 0u) return;
+    const int lane = (int)(threadIdx.x & 31);
+    const int np = __popc(act);
+    if (np < 2) {
+        if (ib & (1u << lane)) red_sw(sw, g, a, b);
+        return;
+    }
+    const int rank = __popc(act & ((1u << lane) - 1u));
+    const int per = np >> 1, half = rank & 1, slot = rank >> 1, k = __popc(ib);
+    for (int base = 0; base < k; base += per) {
+        const int j = base + slot;
+        const bool mine = slot < per && j < k;
+        const int src = !mine ? lane : ib == 0xffffffffu ? j : (int)__fns(ib, 0, j + 1);
+        const int gg = __shfl_sync(act, g, src);
+        const double va = __shfl_sync(act, a, src), vb = __shfl_sync(act, b, src);
+        if (mine) atomicAdd(sw + 2 * (size_t)gg + half, half ? vb : va);
+    }
+}
+
 // Shared-memory layout of the PRIV sink: unit -> uint32 count[G];
 // weighted -> double2 (sumw, sumw2)[G].
 // With R > 1 replicas (small bin spaces) warp w adds into replica w % R, so hot
@@ -682,10 +716,7 @@ struct PrivSink {
                         a += __shfl_xor_sync(0xffffffffu, a, o);
                         b += __shfl_xor_sync(0xffffffffu, b, o);
                     }
-                    if (ok && sub == 0) {
-                        if (a != 0.0) atomicAdd(p.sumw + i, a);
-                        if (b != 0.0) atomicAdd(p.sumw2 + i, b);
-                    }
+                    if (ok && sub == 0) red_sw(p.sw, i, a, b);
                 } else {
                     uint32_t v = 0;
                     for (int r = sub; ok && r < R; r += S) v += reinterpret_cast<const uint32_t *>(s + r * stride)[i];
@@ -695,16 +726,11 @@ struct PrivSink {
             }
             return;
         }
-        if (W) {
-            for (int i = threadIdx.x; i < G; i += blockDim.x) {
-                double2 v = reinterpret_cast<const double2 *>(s)[i];
-                for (int r = 1; r < R; ++r) {
-                    const double2 u = reinterpret_cast<const double2 *>(s + r * stride)[i];
-                    v.x += u.x;
-                    v.y += u.y;
-                }
-                if (v.x != 0.0) atomicAdd(p.sumw + i, v.x);
-                if (v.y != 0.0) atomicAdd(p.sumw2 + i, v.y);
+        if (W) {        // component-wise: a warp's REDs cover 16 contiguous cells (8 sectors)
+            for (int i = threadIdx.x; i < 2 * G; i += blockDim.x) {
+                double v = reinterpret_cast<const double *>(s)[i];
+                for (int r = 1; r < R; ++r) v += reinterpret_cast<const double *>(s + r * stride)[i];
+                if (v != 0.0) atomicAdd(p.sw + i, v);
             }
         } else {
             for (int i = threadIdx.x; i < G; i += blockDim.x) {
@@ -722,8 +748,8 @@ struct GlobalSink {
     __device__ __forceinline__ void init(unsigned char *, int) {}
     __device__ __forceinline__ void add(int g, double w) {
         if (W) {
-            atomicAdd(pp->sumw + g, w);
-            atomicAdd(pp->sumw2 + g, w * w);
+            const unsigned act = __activemask();
+            red_sw_pairs(act, act, pp->sw, g, w, w * w);
         } else {
             atomicAdd(pp->count + g, 1ull);
         }
@@ -828,34 +854,39 @@ struct CacheSink {
     // a weighted item (a lane cache's (sum w, sum w^2) of bin g, or one event) of the lanes
     // with has=true: equal bins of the warp combine first (match.any + a shuffle walk over
     // the peer mask), then the group leader puts the sums
+    // group sums that miss the slots go to the global cells with paired-lane REDs
     __device__ __forceinline__ void add_item(int g, bool has, double w1, double w2) {
 #if !BH_CACHE_W_AGG
         if (has) put(g, w1, w2);
         return;
 #endif
-        const unsigned act = __ballot_sync(__activemask(), has);
-        if (!has) return;
-        const unsigned peers = __match_any_sync(act, g);
-        const int lane = (int)(threadIdx.x & 31);
-        const int rounds = __reduce_max_sync(act, (unsigned)__popc(peers));
+        const unsigned act0 = __activemask();
+        const unsigned act = __ballot_sync(act0, has);
+        bool glob = false;
         double s1 = 0.0, s2 = 0.0;
-        unsigned m = peers;
-        for (int k = 0; k < rounds; ++k) {
-            const int src = m ? __ffs(m) - 1 : lane;
-            const double v1 = __shfl_sync(act, w1, src), v2 = __shfl_sync(act, w2, src);
-            if (m) { s1 += v1; s2 += v2; m &= m - 1; }
+        if (has) {
+            const unsigned peers = __match_any_sync(act, g);
+            const int lane = (int)(threadIdx.x & 31);
+            const int rounds = __reduce_max_sync(act, (unsigned)__popc(peers));
+            unsigned m = peers;
+            for (int k = 0; k < rounds; ++k) {
+                const int src = m ? __ffs(m) - 1 : lane;
+                const double v1 = __shfl_sync(act, w1, src), v2 = __shfl_sync(act, w2, src);
+                if (m) { s1 += v1; s2 += v2; m &= m - 1; }
+            }
+            if (lane == __ffs(peers) - 1) {
+                const int sl = lookup((uint32_t)g);
+                if (sl >= 0) add2_shared(reinterpret_cast<double2 *>(vals) + sl, s1, s2);   // (sumw, sumw2) cell
+                else glob = true;
+            }
         }
-        if (lane == __ffs(peers) - 1) put(g, s1, s2);
+        red_sw_pairs(act0, __ballot_sync(act0, glob), pp->sw, g, s1, s2);
     }
-    // a weighted group sum into its shared-memory slot, or straight to the global bins
+    // a weighted group sum into its shared-memory slot, or straight to the global cell
     __device__ __forceinline__ void put(int g, double s1, double s2) {
         const int sl = lookup((uint32_t)g);
-        if (sl >= 0) {
-            add2_shared(reinterpret_cast<double2 *>(vals) + sl, s1, s2);     // (sumw, sumw2) cell
-        } else {
-            atomicAdd(pp->sumw + g, s1);
-            atomicAdd(pp->sumw2 + g, s2);
-        }
+        if (sl >= 0) add2_shared(reinterpret_cast<double2 *>(vals) + sl, s1, s2);
+        else red_sw(pp->sw, g, s1, s2);
     }
     __device__ __forceinline__ void drain() {
         if (!W && BH_LANE_CACHE_U && un) {
@@ -876,8 +907,7 @@ struct CacheSink {
             if (k == kEmpty) continue;
             if (W) {
                 const double2 d = reinterpret_cast<const double2 *>(vals)[i];
-                if (d.x != 0.0) atomicAdd(p.sumw + k, d.x);
-                if (d.y != 0.0) atomicAdd(p.sumw2 + k, d.y);
+                red_sw(p.sw, (int)k, d.x, d.y);
             } else {
                 const uint32_t v = reinterpret_cast<const uint32_t *>(vals)[i];
                 if (v) atomicAdd(p.count + k, (unsigned long long)v);
@@ -1297,8 +1327,8 @@ __global__ void __launch_bounds__(512, 2) k_fill_exact(FillP p, long long *limbs
         const double w = valid ? ld_stream(p.w + i) : 0.0, w2 = w * w;
         const bool fin = fabs(w) <= 1.7976931348623157e308 && fabs(w2) <= 1.7976931348623157e308;
         if (valid && !fin) {
-            atomicAdd(p.sumw + g, w);
-            atomicAdd(p.sumw2 + g, w2);
+            atomicAdd(p.sw + 2 * (size_t)g, w);
+            atomicAdd(p.sw + 2 * (size_t)g + 1, w2);
         }
         const bool use = valid && fin;
         const unsigned act = __ballot_sync(0xffffffffu, use);
@@ -1338,12 +1368,12 @@ __device__ __forceinline__ double fold_limbs(long long *l, int e) {
     return ldexp((double)v, e - 96);
 }
 
-__global__ void k_exact_fold(int G, long long *limbs, const unsigned long long *maxbits, double *sumw, double *sumw2) {
+__global__ void k_exact_fold(int G, long long *limbs, const unsigned long long *maxbits, double *sw) {
     const int e1 = exact_exp(*maxbits), e2 = 2 * e1 + 1;
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         long long *l = limbs + 2 * kLimbs * (size_t)g;
-        if (l[0] | l[1] | l[2] | l[3]) sumw[g] += fold_limbs(l, e1);
-        if (l[4] | l[5] | l[6] | l[7]) sumw2[g] += fold_limbs(l + kLimbs, e2);
+        if (l[0] | l[1] | l[2] | l[3]) sw[2 * (size_t)g] += fold_limbs(l, e1);
+        if (l[4] | l[5] | l[6] | l[7]) sw[2 * (size_t)g + 1] += fold_limbs(l + kLimbs, e2);
     }
 }
 
@@ -1374,7 +1404,7 @@ struct MultiH {
     int32_t stat_off;                    // first index of this histogram's stats in the flat list
     int32_t smem_off;                    // byte offset of the privatized bins
     unsigned long long *count;
-    double *sumw, *sumw2, *stats, *partials;
+    double *sw, *stats, *partials;      // sw: interleaved (sum w, sum w^2) [2G]
     unsigned long long *entries;
 };
 
@@ -1501,12 +1531,9 @@ __global__ void __launch_bounds__(1024, 1) k_fill_multi(const __grid_constant__ 
     for (int hh = 0; hh < p.nh; ++hh) {
         const MultiH &H = p.h[hh];
         if (H.weighted) {
-            const double2 *d = reinterpret_cast<const double2 *>(smem + H.smem_off);
-            for (int i = threadIdx.x; i < H.G; i += T) {
-                const double2 v = d[i];
-                if (v.x != 0.0) atomicAdd(H.sumw + i, v.x);
-                if (v.y != 0.0) atomicAdd(H.sumw2 + i, v.y);
-            }
+            const double *d = reinterpret_cast<const double *>(smem + H.smem_off);
+            for (int i = threadIdx.x; i < 2 * H.G; i += T)
+                if (d[i] != 0.0) atomicAdd(H.sw + i, d[i]);
         } else {
             const uint32_t *c = reinterpret_cast<const uint32_t *>(smem + H.smem_off);
             for (int i = threadIdx.x; i < H.G; i += T)
@@ -1621,46 +1648,45 @@ __global__ void k_find_bins(FillP p, int32_t *out) {
 #ifndef BH_FILL_TU
 // bh_reset: bins, sums of w^2, stats and entries to zero in ONE launch (five memsets cost
 // ~2-3 us of launch overhead each, a third of a 1e6-event fill step); 16-byte stores.
-__global__ void k_reset(int G, unsigned long long *count, double *sumw, double *sumw2, double *stats,
+__global__ void k_reset(int G, unsigned long long *count, double *sw, double *stats,
                         unsigned long long *entries) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t h = G / 2;                  // the arrays are 16-byte aligned (cudaMalloc)
     for (int64_t i = t0; i < h; i += stride) {
         reinterpret_cast<ulonglong2 *>(count)[i] = make_ulonglong2(0ull, 0ull);
-        reinterpret_cast<double2 *>(sumw)[i] = make_double2(0.0, 0.0);
-        reinterpret_cast<double2 *>(sumw2)[i] = make_double2(0.0, 0.0);
+        reinterpret_cast<double2 *>(sw)[2 * i] = make_double2(0.0, 0.0);
+        reinterpret_cast<double2 *>(sw)[2 * i + 1] = make_double2(0.0, 0.0);
     }
     if (t0 == 0 && (G & 1)) {
         count[G - 1] = 0ull;
-        sumw[G - 1] = 0.0;
-        sumw2[G - 1] = 0.0;
+        reinterpret_cast<double2 *>(sw)[G - 1] = make_double2(0.0, 0.0);
     }
     if (t0 < 16) stats[t0] = 0.0;
     if (t0 == 0) *entries = 0ull;
 }
 
 // packed = [content | sumw2 | stats | entries], content = count + sumw.
-__global__ void k_pack(int G, int K, const unsigned long long *count, const double *sumw, const double *sumw2,
+__global__ void k_pack(int G, int K, const unsigned long long *count, const double *sw,
                        const double *stats, const unsigned long long *entries, double *out) {
     const int64_t tot = 2 * (int64_t)G + K + 1;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
         double v;
-        if (i < G) v = (double)count[i] + sumw[i];
-        else if (i < 2 * (int64_t)G) v = (double)count[i - G] + sumw2[i - G];
+        if (i < G) v = (double)count[i] + sw[2 * i];
+        else if (i < 2 * (int64_t)G) v = (double)count[i - G] + sw[2 * (i - G) + 1];
         else if (i < 2 * (int64_t)G + K) v = stats[i - 2 * G];
         else v = (double)*entries;
         out[i] = v;
     }
 }
 
-__global__ void k_unpack(int G, int K, unsigned long long *count, double *sumw, double *sumw2, double *stats,
+__global__ void k_unpack(int G, int K, unsigned long long *count, double *sw, double *stats,
                          unsigned long long *entries, const double *in) {
     const int64_t tot = 2 * (int64_t)G + K + 1;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
         const double v = in[i];
-        if (i < G) { count[i] = 0ull; sumw[i] = v; }
-        else if (i < 2 * (int64_t)G) sumw2[i - G] = v;
+        if (i < G) { count[i] = 0ull; sw[2 * i] = v; }
+        else if (i < 2 * (int64_t)G) sw[2 * (i - G) + 1] = v;
         else if (i < 2 * (int64_t)G + K) stats[i - 2 * G] = v;
         else *entries = (unsigned long long)v;
     }
@@ -1673,7 +1699,7 @@ struct PackDesc {
     int64_t off;
     int32_t G, K, unit;
     unsigned long long *count;
-    double *sumw, *sumw2, *stats;
+    double *sw, *stats;                          // sw: interleaved (sum w, sum w^2) [2G]
     unsigned long long *entries;
 };
 constexpr int kMaxPack = 8;
@@ -1695,8 +1721,8 @@ __global__ void k_pack_multi(const __grid_constant__ PackMultiP p, double *out) 
         const int64_t j = i - D.off, G = D.G;
         const int64_t s2 = D.unit ? 0 : G;           // length of the sumw2 section
         double v;
-        if (j < G) v = (double)D.count[j] + D.sumw[j];
-        else if (j < G + s2) v = (double)D.count[j - G] + D.sumw2[j - G];
+        if (j < G) v = (double)D.count[j] + D.sw[2 * j];
+        else if (j < G + s2) v = (double)D.count[j - G] + D.sw[2 * (j - G) + 1];
         else if (j < G + s2 + D.K) v = D.stats[j - G - s2];
         else v = (double)*D.entries;
         out[i] = v;
@@ -1711,9 +1737,9 @@ __global__ void k_unpack_multi(const __grid_constant__ PackMultiP p, const doubl
         const double v = in[i];
         if (j < G) {
             D.count[j] = 0ull;
-            D.sumw[j] = v;
-            if (D.unit) D.sumw2[j] = v;              // unit weights: sum w^2 == count
-        } else if (j < G + s2) D.sumw2[j - G] = v;
+            D.sw[2 * j] = v;
+            if (D.unit) D.sw[2 * j + 1] = v;         // unit weights: sum w^2 == count
+        } else if (j < G + s2) D.sw[2 * (j - G) + 1] = v;
         else if (j < G + s2 + D.K) D.stats[j - G - s2] = v;
         else *D.entries = (unsigned long long)v;
     }

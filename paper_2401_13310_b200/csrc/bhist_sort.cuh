@@ -259,10 +259,12 @@ constexpr int kProbeHash = 4096;
 template <int DIM>
 __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, int samples, unsigned int *out) {
     // out[0]: largest partition count; out[1]: largest count of a hashed bin bucket
-    // (4096 buckets: a single hot bin shows up as one large bucket); out[2]: the decision,
-    // 1 (SORT) when no partition holds > 5% and no bucket > 1% of the samples, else 0
-    // (CACHE) -- read by the gated fills on the device, so AUTO's choice depends on the
-    // data only, never on timing
+    // (4096 buckets: a single hot bin shows up as one large bucket); out[2]: the unit-weight
+    // decision, 1 (SORT) when no partition holds > 5% and no bucket > 1% of the samples, else
+    // 0 (CACHE); out[3]: the weighted decision, 1 (GLOBAL) when no bucket holds > 1/512 of the
+    // samples (a bin with a share f of n events costs f*n serialized same-address REDs, ~0.55
+    // G/s), else 0 (CACHE) -- read by the gated fills on the device, so AUTO's choice depends
+    // on the data only, never on timing
     extern __shared__ unsigned int pc[];
     unsigned int *hc = pc + P;
     for (int i = threadIdx.x; i < P + kProbeHash; i += blockDim.x) pc[i] = 0u;
@@ -290,8 +292,10 @@ __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, 
         atomicMax(out + 1, mh);
     }
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
         out[2] = (20ull * out[0] <= (unsigned long long)samples && 100ull * out[1] <= (unsigned long long)samples) ? 1u : 0u;
+        out[3] = 512ull * out[1] <= (unsigned long long)samples ? 1u : 0u;
+    }
 }
 
 // ------------------------------------------------------------------ plan
@@ -514,12 +518,10 @@ __global__ void __launch_bounds__(kReduceThreads, kReduceCtas) k_part_reduce(Fil
         __syncthreads();
         // merge stage: this CTA's partial bins of the partition -> global
         if (W) {
-            const double2 *d = reinterpret_cast<const double2 *>(smem);
-            for (int i = threadIdx.x; i < nb; i += kReduceThreads) {
-                const double2 vv = d[i];
-                if (vv.x != 0.0) atomicAdd(p.sumw + gb0 + i, vv.x);
-                if (vv.y != 0.0) atomicAdd(p.sumw2 + gb0 + i, vv.y);
-            }
+            const double *d = reinterpret_cast<const double *>(smem);
+            double *o = p.sw + 2 * (size_t)gb0;
+            for (int i = threadIdx.x; i < 2 * nb; i += kReduceThreads)
+                if (d[i] != 0.0) atomicAdd(o + i, d[i]);
         } else {
             const uint32_t *cc = reinterpret_cast<const uint32_t *>(smem);
             for (int i = threadIdx.x; i < nb; i += kReduceThreads)

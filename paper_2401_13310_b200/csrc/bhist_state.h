@@ -29,7 +29,7 @@ struct bh_hist {
     int max_grid = 0;
     // device state
     unsigned long long *count = nullptr;
-    double *sumw = nullptr, *sumw2 = nullptr;
+    double *sw = nullptr;             // interleaved (sum w, sum w^2) per bin [2G]
     double *stats = nullptr;
     unsigned long long *entries = nullptr;
     double *partials = nullptr;

@@ -724,7 +724,8 @@ def test_auto_sort_probe(peaked):
         ref.fill([x, y])
         torch.cuda.synchronize()
     assert h.strategy(False) == (pkg.BH_STRATEGY_CACHE if peaked else pkg.BH_STRATEGY_SORT)
-    assert h.strategy(True) == pkg.BH_STRATEGY_CACHE
+    # the same probe decides weighted fills: GLOBAL (paired-lane REDs) unless a bin is hot
+    assert h.strategy(True) == (pkg.BH_STRATEGY_CACHE if peaked else pkg.BH_STRATEGY_GLOBAL)
     a, b = h.read(), ref.read()
     assert a["entries"] == b["entries"] == 3 * n
     assert np.array_equal(a["content"], b["content"])

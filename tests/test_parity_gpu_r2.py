@@ -448,3 +448,30 @@ def test_auto_sort_decision_is_deterministic_and_matches_oracle():
     ref = oracle_parallel("C3", n)
     ref2 = {k: (2 * v if k != "entries" else 2 * v) for k, v in ref.items()}
     compare(a, ref2, False, "AUTO->SORT x2")
+
+
+# ------------------------------------------------------------------ AUTO's weighted GLOBAL/CACHE decision
+@pytest.mark.slow
+@pytest.mark.parametrize("name,want", [("C3W", "global"), ("C4W", "cache")])
+def test_auto_weighted_global_decision_matches_oracle(name, want):
+    """Weighted fills of a bin space that does not fit PRIV: the device probe picks GLOBAL
+    (paired-lane L2 REDs) on spread-out data and CACHE on a hot bin (C4w: ~43% of the events
+    in one cell), both launched gated; two fresh histograms end bitwise identical in counts
+    and stats, and the result equals the oracle within 1e-12 of sum|term|."""
+    n = 40_000_003
+    wl = bhgen.workload(name, n)
+    hist = wl.hists[0]
+    tc = [_t(wl.column(c, 0, n)) for c in hist.cols]
+    tw = _t(wl.column(wl.wcol, 0, n))
+    axes = oracle.oracle_axes(hist)
+    runs = []
+    for rep in range(2):
+        h = pkg.Histogram(axes)
+        h.fill(tc, tw)
+        runs.append((h.read(), h.strategy(True)))
+        h.close()
+    (a, sa), (b, sb) = runs
+    strat = {"global": pkg.BH_STRATEGY_GLOBAL, "cache": pkg.BH_STRATEGY_CACHE}[want]
+    assert sa == sb == strat
+    assert a["entries"] == b["entries"] == n
+    compare(a, oracle_parallel(name, n), True, f"AUTO weighted {name} -> {want}")

@@ -294,6 +294,24 @@ bh_status bh_jit_compile_check(const char *kernel_expr, int32_t threads, int32_t
 bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *stats, int64_t *entries,
                   bh_stream s);
 
+/* TH1F / TH1I-style contents (the paper's bin type T, PAPER.md:141 `T *histogram`, P:164
+ * `(T) weight`; "different ... data types"), reading R18 of DESIGN.md: the device
+ * state stays exact (u64 counts, float64 sums) and the narrow type is taken once, at read:
+ *   BH_CONTENT_F32  contents[i] = RN_float32(content_i), sumw2[i] = RN_float32(sumw2_i), where
+ *                   content_i / sumw2_i are the float64 values bh_read returns (one rounding,
+ *                   independent of the order of the adds -- unlike float32 atomics);
+ *   BH_CONTENT_I32  contents[i] = sumw2[i] = min(count_i, INT32_MAX) (ROOT's TH1I saturates
+ *                   at INT32_MAX); only for histograms filled with unit weights (a TH1I
+ *                   counts entries) -- BH_EINVAL if any weighted fill or unpack touched it.
+ * contents / sumw2 are caller-owned HOST arrays of G float (F32) or int32_t (I32), either may
+ * be NULL; stats[K] and entries as in bh_read.  The narrowing runs on the device and halves
+ * the bytes copied back.  Synchronizes stream s. */
+#define BH_CONTENT_F64 0
+#define BH_CONTENT_F32 1
+#define BH_CONTENT_I32 2
+bh_status bh_read_as(const bh_hist *h, int32_t content_type, void *contents, void *sumw2, double *stats,
+                     int64_t *entries, bh_stream s);
+
 /* Force a fill strategy (BH_STRATEGY_*); BH_EINVAL if it cannot hold this histogram. */
 bh_status bh_set_strategy(bh_hist *h, int32_t strategy);
 

@@ -22,10 +22,11 @@ BH_DEBUG_SKIP_COPY_WAIT = 1
 BH_DEBUG_FIND_BINS_GLOBAL = 2
 BH_DEBUG_REQUIRE_JIT = 4
 BH_MULTI_PASSES, BH_MULTI_ONE_PASS = 0, 1
+BH_CONTENT_F64, BH_CONTENT_F32, BH_CONTENT_I32 = 0, 1, 2
 
 # every symbol include/bhist.h declares (checked by tests/test_abi.py)
 EXPORTED = ["bh_version", "bh_last_error", "bh_create", "bh_destroy", "bh_reset", "bh_fill", "bh_fill_host",
-            "bh_fill_multi", "bh_fill_expr", "bh_fill_f32", "bh_fill_i32", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_set_strategy",
+            "bh_fill_multi", "bh_fill_expr", "bh_fill_f32", "bh_fill_i32", "bh_find_bins", "bh_info", "bh_packed_size", "bh_pack", "bh_unpack", "bh_read", "bh_read_as", "bh_set_strategy",
             "bh_fill_host_f32", "bh_fill_host_i32", "bh_packed_size_multi", "bh_pack_multi", "bh_unpack_multi",
             "bh_jit_compile_check",
             "bh_get_strategy", "bh_set_chunk", "bh_set_debug", "bh_set_multi_mode", "bh_launch_count",
@@ -97,6 +98,7 @@ def lib(build_if_stale: bool = False):
             "bh_pack": ([_P, _P, _P], _I32),
             "bh_unpack": ([_P, _P, _P], _I32),
             "bh_read": ([_P, _P, _P, _P, _P, _P], _I32),
+            "bh_read_as": ([_P, _I32, _P, _P, _P, _P, _P], _I32),
             "bh_set_strategy": ([_P, _I32], _I32),
             "bh_get_strategy": ([_P, _I32, _P], _I32),
             "bh_set_chunk": ([_P, _I64], _I32),
@@ -342,6 +344,22 @@ def bh_read(h, stream=None) -> dict:
     return {"content": c, "sumw2": s2, "stats": st, "entries": ent.value}
 
 
+def bh_read_as(h, content_type: int, stream=None) -> dict:
+    """bh_read with TH1F / TH1I-style contents (BH_CONTENT_F32: float32, BH_CONTENT_I32: int32)."""
+    if content_type == BH_CONTENT_F64:
+        return bh_read(h, stream)
+    _, G, K = bh_info(h)
+    dt = {BH_CONTENT_F32: np.float32, BH_CONTENT_I32: np.int32}.get(content_type)
+    if dt is None:
+        raise BHistError(f"unknown content type {content_type}")
+    c = np.empty(G, dtype=dt)
+    s2 = np.empty(G, dtype=dt)
+    st = np.empty(K)
+    ent = _I64()
+    _check(lib().bh_read_as(h, content_type, c.ctypes.data, s2.ctypes.data, st.ctypes.data, ctypes.byref(ent), stream))
+    return {"content": c, "sumw2": s2, "stats": st, "entries": ent.value}
+
+
 def bh_set_strategy(h, strategy: int) -> None:
     _check(lib().bh_set_strategy(h, strategy))
 
@@ -563,8 +581,8 @@ class Histogram:
         bh_unpack(self.h, buf.data_ptr(), self._s(stream))
         return self
 
-    def read(self, stream=None) -> dict:
-        return bh_read(self.h, self._s(stream))
+    def read(self, stream=None, content_type: int = BH_CONTENT_F64) -> dict:
+        return bh_read_as(self.h, content_type, self._s(stream))
 
     def strategy(self, weighted: bool) -> int:
         return bh_get_strategy(self.h, weighted)

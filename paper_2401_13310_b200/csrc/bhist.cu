@@ -740,6 +740,8 @@ bh_status bh_destroy(bh_hist *h) {
     cudaFree(h->part_cnt);
     cudaFree(h->part_cp);
     cudaFree(h->probe_dev);
+    cudaFree(h->narrow_buf);
+    if (h->narrow_host) cudaFreeHost(h->narrow_host);
     if (h->pack_host) cudaFreeHost(h->pack_host);
     for (void *p : h->axis_mem) cudaFree(p);
     for (int i = 0; i < kStageSlots; ++i) {
@@ -1520,6 +1522,43 @@ bh_status bh_read(const bh_hist *h, double *contents, double *sumw2, double *sta
     if (sumw2) memcpy(sumw2, h->pack_host + h->G, sizeof(double) * h->G);
     if (stats) memcpy(stats, h->pack_host + 2 * h->G, sizeof(double) * h->K);
     if (entries) *entries = (int64_t)h->pack_host[2 * h->G + h->K];
+    return BH_OK;
+}
+
+bh_status bh_read_as(const bh_hist *h, int32_t type, void *contents, void *sumw2, double *stats, int64_t *entries,
+                     bh_stream s) {
+    if (type == BH_CONTENT_F64)
+        return bh_read(h, static_cast<double *>(contents), static_cast<double *>(sumw2), stats, entries, s);
+    if (type != BH_CONTENT_F32 && type != BH_CONTENT_I32) return fail(BH_EINVAL, "unknown content type %d", type);
+    if (bulk_check(h)) return BH_EINVAL;
+    if (type == BH_CONTENT_I32 && h->weighted_content)
+        return fail(BH_EINVAL, "int32 (TH1I) contents need unit-weight fills only: this histogram holds weighted sums");
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    bh_status r = bh_pack(h, h->pack_buf, s);
+    if (r != BH_OK) return r;
+    const int64_t G = h->G, tot = 2 * G + h->K + 1;
+    // the narrowed [content | sumw2] (8 B per bin) goes to lazily allocated device + pinned buffers
+    bh_hist *hm = const_cast<bh_hist *>(h);
+    if (!hm->narrow_buf) {
+        if (cudaMalloc(reinterpret_cast<void **>(&hm->narrow_buf), 8 * (size_t)G) != cudaSuccess ||
+            cudaMallocHost(reinterpret_cast<void **>(&hm->narrow_host), 8 * (size_t)G) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(BH_ENOMEM, "narrow read buffers (%lld B)", (long long)(8 * G));
+        }
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((2 * G + 255) / 256, (int64_t)h->nsm * 8));
+    k_narrow<<<grid, 256, 0, st>>>((int)G, type, h->pack_buf, hm->narrow_buf);
+    CUDA_TRY(cudaGetLastError());
+    hm->launches++;
+    CUDA_TRY(cudaMemcpyAsync(hm->narrow_host, hm->narrow_buf, 8 * (size_t)G, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(h->pack_host + 2 * G, h->pack_buf + 2 * G, sizeof(double) * (h->K + 1),
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (contents) memcpy(contents, hm->narrow_host, 4 * (size_t)G);
+    if (sumw2) memcpy(sumw2, hm->narrow_host + 4 * (size_t)G, 4 * (size_t)G);
+    if (stats) memcpy(stats, h->pack_host + 2 * G, sizeof(double) * h->K);
+    if (entries) *entries = (int64_t)h->pack_host[tot - 1];
     return BH_OK;
 }
 

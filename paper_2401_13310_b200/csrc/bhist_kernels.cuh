@@ -1692,6 +1692,18 @@ __global__ void k_unpack(int G, int K, unsigned long long *count, double *sw, do
     }
 }
 
+// bh_read_as: the packed float64 [content | sumw2] of bh_pack narrowed once (reading R18):
+// float32 by round-to-nearest, int32 (unit-weight counts) saturated at INT32_MAX.
+// (Unit-weight contents are integers < 2^53, exact in the packed float64.)
+__global__ void k_narrow(int G, int type, const double *packed, void *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * (int64_t)G;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = packed[i];
+        if (type == 1) reinterpret_cast<float *>(out)[i] = __double2float_rn(v);
+        else reinterpret_cast<int32_t *>(out)[i] = v >= 2147483647.0 ? 2147483647 : (int32_t)v;
+    }
+}
+
 // Several histograms packed into one buffer for ONE collective per step:
 // histogram i occupies [off_i, off_i + len_i) with the bh_pack layout, or, when unit_i is
 // set (a unit-weight-only state: sumw2 == content), [content(G) | stats(K) | entries].

@@ -38,6 +38,8 @@ struct bh_hist {
     unsigned long long *maxbits = nullptr;   // EXACT: bit pattern of max|w| of the current launch
     double *pack_buf = nullptr;       // device buffer for bh_read
     double *pack_host = nullptr;      // pinned host buffer for bh_read
+    void *narrow_buf = nullptr;       // bh_read_as: device [content | sumw2] as float32 / int32 [2G]
+    unsigned char *narrow_host = nullptr;   // its pinned host twin
     // SORT strategy scratch (grown on demand): records, segment offsets, partition totals
     uint16_t *part_l = nullptr;
     double *part_w = nullptr;

@@ -475,3 +475,49 @@ def test_auto_weighted_global_decision_matches_oracle(name, want):
     assert sa == sb == strat
     assert a["entries"] == b["entries"] == n
     compare(a, oracle_parallel(name, n), True, f"AUTO weighted {name} -> {want}")
+
+
+# ------------------------------------------------------------------ TH1F / TH1I contents (reading R18)
+@pytest.mark.parametrize("name,weighted", [("C1", False), ("C2", True), ("C3", False)])
+def test_read_as_float32_and_int32_contents(name, weighted):
+    """bh_read_as narrows the exact device state once: float32 = RN_f32(float64 content),
+    int32 = the unit-weight count (TH1I), against the oracle's float64 contents."""
+    n = 1_000_003
+    wl = bhgen.workload(name, n)
+    hist = wl.hists[0]
+    h = pkg.Histogram(oracle.oracle_axes(hist))
+    h.fill([_t(wl.column(c, 0, n)) for c in hist.cols], _t(wl.column(wl.wcol, 0, n)) if weighted else None)
+    d = h.read()
+    f = h.read(content_type=pkg.BH_CONTENT_F32)
+    assert f["content"].dtype == np.float32 and f["sumw2"].dtype == np.float32
+    assert np.array_equal(f["content"], d["content"].astype(np.float32))      # the definition, bin by bin
+    assert np.array_equal(f["sumw2"], d["sumw2"].astype(np.float32))
+    assert f["entries"] == n and np.array_equal(f["stats"], d["stats"])
+    ref = oracle_parallel(name, n)
+    rf = ref["content"].astype(np.float32)
+    # float64 results agree within 1e-12 relative; their float32 roundings within one float32 ulp
+    assert np.all(np.abs(f["content"] - rf) <= np.spacing(np.abs(rf)))
+    if weighted:
+        with pytest.raises(pkg.BHistError):
+            h.read(content_type=pkg.BH_CONTENT_I32)
+    else:
+        i = h.read(content_type=pkg.BH_CONTENT_I32)
+        assert i["content"].dtype == np.int32
+        assert np.array_equal(i["content"], ref["content"].astype(np.int64))
+        assert np.array_equal(i["sumw2"], i["content"])
+    h.close()
+
+
+def test_read_as_int32_saturates():
+    """A TH1I bin saturates at INT32_MAX (ROOT's TH1I); the float32 content is RN_f32 of the
+    exact count: 9 fills of 2^28 events into one bin = 2415919104 > 2^31 - 1."""
+    m = 1 << 28
+    x = torch.full((m,), 0.5, dtype=torch.float64, device=DEV)
+    h = pkg.Histogram([(1, 0.0, 1.0)])
+    for _ in range(9):
+        h.fill([x])
+    i = h.read(content_type=pkg.BH_CONTENT_I32)
+    f = h.read(content_type=pkg.BH_CONTENT_F32)
+    assert i["content"].tolist() == [0, 2147483647, 0] and i["entries"] == 9 * m
+    assert f["content"].tolist() == [0.0, 2415919104.0, 0.0]
+    h.close()

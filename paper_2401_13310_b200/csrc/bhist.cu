@@ -107,10 +107,10 @@ int cache_slots_for(bool weighted) {
 
 size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
 
-size_t sink_bytes(const bh_hist *h, int strategy, bool weighted) {
+size_t sink_bytes(const bh_hist *h, int strategy, bool weighted, int slots = 0) {
     if (strategy == BH_STRATEGY_PRIV) return align16(weighted ? 16 * (size_t)h->G : 4 * (size_t)h->G);
     if (strategy == BH_STRATEGY_CACHE) {
-        const size_t S = cache_slots_for(weighted);
+        const size_t S = slots > 0 ? slots : cache_slots_for(weighted);
         return S * 4 + (weighted ? 16 * S : 4 * S);
     }
     return 0;
@@ -141,6 +141,10 @@ FillP make_params(const bh_hist *h, int64_t n, const double *const *coords, cons
     p.entries = h->entries;
     p.entries_add = n;
     p.wc_off = -1;
+    p.hot = nullptr;
+    p.hot_off = -1;
+    p.win = nullptr;
+    p.win_off = -1;
     return p;
 }
 
@@ -163,14 +167,15 @@ struct FillPlan {
 // through CACHE (warp-aggregated, hot-bin safe) instead.
 bool small_fill(const bh_hist *h, int64_t n) { return n < 2 * h->G * (int64_t)h->nsm; }
 
-bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n, size_t reserve = 0, int force = -1) {
+bh_status plan_fill(const bh_hist *h, bool weighted, FillPlan &pl, int64_t n, size_t reserve = 0, int force = -1,
+                    int slots = 0) {
     LaunchCfg &c = pl.c;
     c.weighted = weighted;
     c.strategy = force >= 0 ? force : resolve_one_pass(h, c.weighted);
     if (force < 0 && c.strategy == BH_STRATEGY_PRIV && (h->strategy == BH_STRATEGY_AUTO || h->strategy == BH_STRATEGY_EXACT) &&
         small_fill(h, n))
         c.strategy = BH_STRATEGY_CACHE;
-    size_t sink = sink_bytes(h, c.strategy, c.weighted);
+    size_t sink = sink_bytes(h, c.strategy, c.weighted, slots);
     // variable-axis tables go to shared memory behind the sink when they fit
     size_t tabs = 0;
     for (int a = 0; a < h->dim; ++a) {
@@ -406,31 +411,90 @@ bh_status fill_sort(bh_hist *h, int64_t n, const double *const *coords, const do
 // never on host timing, and the host never waits for it.  Returns the device flag of this
 // fill's choice (1: SORT / GLOBAL), or nullptr (plain CACHE).
 constexpr int kProbeSamples = 1 << 14;     // one CTA: ~40 us, once per histogram and reset
+
+// Unit-weight WINDOW plan (probe decision 2, see k_part_probe): CACHE with kWinSlots slots,
+// its tables, then the box counts at `off`, as many as the rest of shared memory holds (amax).
+constexpr int kWinSlots = 1024;
+bool win_plan(const bh_hist *h, int64_t n, FillPlan &pw, size_t &off, int &amax) {
+    if (h->dim > 2 || plan_fill(h, false, pw, n, 0, BH_STRATEGY_CACHE, kWinSlots) != BH_OK) {
+        g_err.clear();
+        return false;
+    }
+    off = align16(pw.c.smem);
+    const size_t room = h->smem_optin > off + kStaticSmemReserve ? h->smem_optin - off - kStaticSmemReserve : 0;
+    amax = (int)std::min<size_t>(room / 4, (size_t)1 << 20);
+    return amax >= 1024;
+}
+
 const int32_t *auto_gate(bh_hist *h, int64_t n, const double *const *coords, bool weighted, cudaStream_t s) {
     if (h->strategy != BH_STRATEGY_AUTO || resolve_strategy(h, weighted) != BH_STRATEGY_CACHE) return nullptr;
     const int P = (int)sort_partitions(h, false);
     if (P > kPartMaxP || n < 8LL * h->nsm * (1LL << sort_pb(false))) return nullptr;
     if (getenv(weighted ? "BHIST_NO_AUTO_GLOBAL" : "BHIST_NO_AUTO_SORT")) return nullptr;
     if (!h->probe_dev) {
-        if (cudaMalloc(reinterpret_cast<void **>(&h->probe_dev), 4 * sizeof(unsigned int)) != cudaSuccess) {
+        if (cudaMalloc(reinterpret_cast<void **>(&h->probe_dev), 8 * sizeof(unsigned int)) != cudaSuccess) {
             cudaGetLastError();
             return nullptr;                                  // no probe: stay on CACHE
         }
     }
     if (h->probe_state == 0) {
         FillP p = make_params(h, n, coords, nullptr);
-        if (cudaMemsetAsync(h->probe_dev, 0, 4 * sizeof(unsigned int), s) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-        const size_t sm = sizeof(unsigned int) * (P + kProbeHash);
+        if (cudaMemsetAsync(h->probe_dev, 0, 8 * sizeof(unsigned int), s) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        FillPlan pw;
+        size_t woff = 0;
+        int amax = 0;
+        if (getenv("BHIST_NO_AUTO_WINDOW") || !win_plan(h, n, pw, woff, amax)) amax = 0;
+        const size_t sm = sizeof(unsigned int) * (P + kProbeHash + 2 * kProbeMarg + kProbeSamples);
+        cudaError_t e;
         switch (h->dim) {
-        case 1: k_part_probe<1><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, h->probe_dev); break;
-        case 2: k_part_probe<2><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, h->probe_dev); break;
-        default: k_part_probe<3><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, h->probe_dev); break;
+        case 1:
+            e = cudaFuncSetAttribute(k_part_probe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e == cudaSuccess) k_part_probe<1><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, amax, h->probe_dev);
+            break;
+        case 2:
+            e = cudaFuncSetAttribute(k_part_probe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e == cudaSuccess) k_part_probe<2><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, amax, h->probe_dev);
+            break;
+        default:
+            e = cudaFuncSetAttribute(k_part_probe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e == cudaSuccess) k_part_probe<3><<<1, 1024, sm, s>>>(p, sort_pb(false), P, kProbeSamples, 0, h->probe_dev);
+            break;
         }
+        if (e != cudaSuccess) { cudaGetLastError(); return nullptr; }
         if (cudaGetLastError() != cudaSuccess) return nullptr;
         h->launches++;
         h->probe_state = 1;                                   // decided (on the device)
     }
     return reinterpret_cast<const int32_t *>(h->probe_dev + (weighted ? 3 : 2));
+}
+
+// AUTO's lane-private window of hot cells (see HotTab) for large weighted PRIVA fills: the
+// first such fill after create/reset launches k_hot_probe on a strided sample of its events;
+// that fill and every later one launch the window kernel and the plain one, gated on the
+// probe's device flag.  Returns the device table, or nullptr (plain PRIVA).
+constexpr int64_t kHotMinEvents = int64_t(1) << 22;
+const HotTab *auto_hot(bh_hist *h, int64_t n, const double *const *coords, const FillPlan &pl, cudaStream_t s) {
+    if (h->strategy != BH_STRATEGY_AUTO || pl.c.strategy != BH_STRATEGY_PRIV || pl.wc_off < 0 || n < kHotMinEvents ||
+        getenv("BHIST_NO_HOT_WINDOW"))
+        return nullptr;
+    if (!h->hot_dev) {
+        if (cudaMalloc(reinterpret_cast<void **>(&h->hot_dev), sizeof(HotTab)) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+    }
+    if (h->hot_state == 0) {
+        FillP p = make_params(h, n, coords, nullptr);
+        switch (h->dim) {
+        case 1: k_hot_probe<1><<<1, 1024, 0, s>>>(p, kProbeSamples, h->hot_dev); break;
+        case 2: k_hot_probe<2><<<1, 1024, 0, s>>>(p, kProbeSamples, h->hot_dev); break;
+        default: k_hot_probe<3><<<1, 1024, 0, s>>>(p, kProbeSamples, h->hot_dev); break;
+        }
+        if (cudaGetLastError() != cudaSuccess) return nullptr;
+        h->launches++;
+        h->hot_state = 1;
+    }
+    return h->hot_dev;
 }
 
 // One fill over device-resident columns, split into launches of <= 2^30 events.
@@ -445,6 +509,19 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
     if (bh_status r = plan_fill(h, w != nullptr, pl, n)) return r;
     if (gate && w)
         if (bh_status r = plan_fill(h, true, pg, n, 0, BH_STRATEGY_GLOBAL)) return r;
+    // unit weights: the WINDOW variant of CACHE (probe decision 2)
+    FillPlan pwin;
+    size_t win_off = 0;
+    int win_amax = 0;
+    const bool winp = gate && !w && !getenv("BHIST_NO_AUTO_WINDOW") && win_plan(h, n, pwin, win_off, win_amax);
+    // weighted PRIVA: the hot-cell window variant, run iff the probe's flag says so
+    const HotTab *hot = w ? auto_hot(h, n, coords, pl, s) : nullptr;
+    FillPlan phot;
+    const size_t hot_bytes = hot_smem_bytes(threads_of(BH_STRATEGY_PRIV, true));
+    if (hot && (plan_fill(h, true, phot, n, hot_bytes) != BH_OK || phot.c.strategy != BH_STRATEGY_PRIV || phot.wc_off < 0)) {
+        hot = nullptr;
+        g_err.clear();
+    }
     LaunchCfg &c = pl.c;
     const int64_t kMaxLaunch = int64_t(1) << 30;   // in-kernel event indices are int32
     for (int64_t off = 0; off < n; off += kMaxLaunch) {
@@ -468,6 +545,44 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         p.wc_off = pl.wc_off;
         c.grid = grid_for(h, c, m);
         cudaError_t e;
+        if (winp) {                                           // unit: the gated WINDOW kernel
+            FillP pq = p;
+            for (int a = 0; a < h->dim; ++a) pq.ax[a] = pwin.ax[a];
+            pq.cache_slots = kWinSlots;
+            pq.win = h->probe_dev + 4;
+            pq.win_off = (int32_t)win_off;
+            pq.gate_run = 2;
+            LaunchCfg cw = pwin.c;
+            cw.smem = win_off + 4 * (size_t)win_amax;
+            cw.vec = c.vec;
+            cw.grid = grid_for(h, cw, m);
+            e = h->dim == 1 ? fill_launch<1, false>(pq, cw, s) : fill_launch<2, false>(pq, cw, s);
+            if (e != cudaSuccess) return fail(BH_ECUDA, "fill launch: %s", cudaGetErrorString(e));
+            ++h->launches;
+        }
+        if (hot) {                                            // gated window kernel, then the plain one
+            FillP pq = p;
+            for (int a = 0; a < h->dim; ++a) pq.ax[a] = phot.ax[a];
+            pq.replicas = phot.replicas;
+            pq.wc_off = phot.wc_off;
+            pq.hot = hot;
+            pq.hot_off = (int32_t)align16(phot.c.smem);
+            pq.gate = &hot->flag;
+            pq.gate_run = 1;
+            LaunchCfg ch = phot.c;
+            ch.smem = pq.hot_off + hot_bytes;
+            ch.vec = c.vec;
+            ch.grid = grid_for(h, ch, m);
+            switch (h->dim) {
+            case 1: e = fill_launch<1, true>(pq, ch, s); break;
+            case 2: e = fill_launch<2, true>(pq, ch, s); break;
+            default: e = fill_launch<3, true>(pq, ch, s); break;
+            }
+            if (e != cudaSuccess) return fail(BH_ECUDA, "fill launch: %s", cudaGetErrorString(e));
+            ++h->launches;
+            p.gate = &hot->flag;
+            p.gate_run = 0;
+        }
         if (gate && w) {                                      // weighted AUTO: the gated GLOBAL fill first
             FillP pq = p;
             for (int a = 0; a < h->dim; ++a) pq.ax[a] = pg.ax[a];
@@ -740,6 +855,7 @@ bh_status bh_destroy(bh_hist *h) {
     cudaFree(h->part_cnt);
     cudaFree(h->part_cp);
     cudaFree(h->probe_dev);
+    cudaFree(h->hot_dev);
     cudaFree(h->narrow_buf);
     if (h->narrow_host) cudaFreeHost(h->narrow_host);
     if (h->pack_host) cudaFreeHost(h->pack_host);
@@ -764,6 +880,7 @@ bh_status bh_reset(bh_hist *h, bh_stream s) {
     ++h->launches;
     h->weighted_content = false;
     h->probe_state = 0;                  // AUTO re-decides SORT vs CACHE on the next large fill
+    h->hot_state = 0;                    // and re-probes the hot-cell window
     return BH_OK;
 }
 

@@ -95,6 +95,10 @@ struct FillP {
     double *stats;               // [K], running totals
     unsigned long long *entries; // running entries
     int64_t entries_add;         // added to *entries by the last CTA
+    const unsigned int *win;     // unit CACHE: the probe's dense box (x0, wx, y0, wy) of bins kept as
+    int32_t win_off;             // shared-memory u32 counts at byte win_off (nullptr: none)
+    const struct HotTab *hot;    // weighted PRIVA: lane-private window of hot cells (nullptr: none)
+    int32_t hot_off;             // its byte offset in shared memory (table, cell list, lane cells)
     const int32_t *gate;         // AUTO's device-side strategy decision: the kernel runs only if
     int32_t gate_run;            // gate == nullptr or *gate == gate_run (otherwise every CTA exits)
 };
@@ -617,11 +621,37 @@ struct RegHot {
 #ifndef BH_AGG_STAY
 #define BH_AGG_STAY 4        // keep aggregating while some bin holds this many lanes
 #endif
+// Lane-private window of hot cells (weighted PRIVA; AUTO's hot-cell probe k_hot_probe).  A
+// peaked weighted histogram (C5's H7: 50x50 on a Cauchy x Gaussian, ~75% of the events in 8
+// cells) serializes every sink on a few shared-memory cells: exchanges collide, the warp
+// aggregation walks long peer groups.  With the window, each THREAD owns a private (sum w,
+// sum w^2) copy of up to kHotW hot cells in shared memory (cell k of thread t at
+// [k * blockDim + t]: consecutive lanes, conflict-free LDS.128/STS.128) and adds its events of
+// those cells with plain read-modify-writes -- no atomic, no collision; the other events take
+// the PRIVA sink.  A direct-mapped table of kHotSlots slots maps a global bin to its window
+// index (one LDS.64 per event).  At the end each warp sums its lanes' copies (shuffles) into
+// its replica, before the usual merge.  The probe picks the cells from a sample on the device
+// and writes `flag` (1: use the window); the fill launches both kernels gated on it.
+constexpr int kHotW = 8;                 // window cells per thread (8 x 16 B x 1024 threads = 128 KB)
+constexpr int kHotSlots = 64;
+struct HotTab {
+    int32_t flag, nwin;                  // flag: window worth using (gate); nwin: cells chosen
+    int32_t cell[kHotW];                 // global bin of window cell k (-1: none)
+    int2 tab[kHotSlots];                 // slot -> {global bin, k}; x = -1 empty
+};
+constexpr int kHotTabSmem = kHotSlots * 8 + kHotW * 4;     // staged table + cell list (16-byte multiple)
+__host__ __device__ constexpr size_t hot_smem_bytes(int threads) { return kHotTabSmem + (size_t)kHotW * 16 * threads; }
+__host__ __device__ __forceinline__ int hot_slot(int g) { return (int)(((uint32_t)g * 2654435761u) >> 26); }
+
 template <bool W, bool ADAPT>
 struct PrivSink {
     uint32_t sm;         // shared-memory address of this warp's replica
     bool agg;            // ADAPT: the warp's previous add collided -> aggregate this one first
     WarpHot hot;         // ADAPT && W: this warp's hot-bin cache
+    const int2 *htab = nullptr;          // lane-private window (see HotTab): staged slot table,
+    const int32_t *hcell = nullptr;      // window cell -> global bin,
+    double2 *hlane = nullptr;            // this thread's copy of window cell 0 (stride blockDim)
+    int hn = 0;                          // window cells (0: no window)
     static constexpr int kCell = W ? 16 : 4;
     static __device__ __forceinline__ size_t stride_of(int G) { return ((size_t)G * kCell + 15) & ~size_t(15); }
     __device__ __forceinline__ void init(unsigned char *s, int G, int R, int wc_off = -1) {
@@ -637,7 +667,32 @@ struct PrivSink {
                 reinterpret_cast<uint32_t *>(s)[i] = 0u;
         }
     }
+    // weighted PRIVA with a hot-cell window (k_fill, p.hot set): stage the table, zero the lane cells
+    __device__ __forceinline__ void init_hot(const FillP &p, unsigned char *smem) {
+        if (!(W && ADAPT) || !p.hot) return;
+        unsigned char *b = smem + p.hot_off;
+        int2 *t = reinterpret_cast<int2 *>(b);
+        int32_t *c = reinterpret_cast<int32_t *>(b + kHotSlots * 8);
+        for (int i = threadIdx.x; i < kHotSlots; i += blockDim.x) t[i] = p.hot->tab[i];
+        if (threadIdx.x < kHotW) c[threadIdx.x] = p.hot->cell[threadIdx.x];
+        hn = p.hot->nwin;
+        htab = t;
+        hcell = c;
+        hlane = reinterpret_cast<double2 *>(b + kHotTabSmem) + threadIdx.x;
+        for (int k = 0; k < kHotW; ++k) hlane[k * blockDim.x] = make_double2(0.0, 0.0);
+    }
     __device__ __forceinline__ void add(int g, double w) {
+        if (W && ADAPT && hn) {          // a window cell: this thread's private copy
+            const int2 e = htab[hot_slot(g)];
+            if (e.x == g) {
+                double2 *c = hlane + e.y * blockDim.x;
+                double2 v = *c;
+                v.x += w;
+                v.y = fma(w, w, v.y);
+                *c = v;
+                return;
+            }
+        }
         if (W) {
             double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
 #ifdef BH_EXP_NOCAS   // experiment only (wrong results): plain read-modify-write instead of CAS
@@ -685,6 +740,21 @@ struct PrivSink {
     }
     // Before the block barrier of the merge stage: hot-bin caches -> this warp's replica.
     __device__ __forceinline__ void drain() {
+        if (ADAPT && W && hn) {          // window: the warp's lane copies -> its replica
+            double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
+            __syncwarp();
+            for (int k = 0; k < kHotW; ++k) {
+                const int g = hcell[k];
+                if (g < 0) continue;     // (uniform)
+                double2 v = hlane[k * blockDim.x];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+                    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+                }
+                if ((threadIdx.x & 31) == 0 && (v.x != 0.0 || v.y != 0.0)) add2_shared(base + g, v.x, v.y);
+            }
+        }
         if (ADAPT && W) {
             double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
             hot.drain([&](int t, double a1, double a2) { add2_shared(base + t, a1, a2); });
@@ -799,7 +869,36 @@ struct CacheSink {
     // the other events go one by one to their slot or the global count, no warp aggregation
     int ug = -1;
     uint32_t un = 0, umiss = 0;
+    // unit weights, AUTO's WINDOW decision (k_part_probe): a dense box of the bin space (1-D: an
+    // interval; 2-D: x0 <= b0 < x0+wx, y0 <= b1 < y0+wy) kept as private u32 counts in shared
+    // memory, the PAPER.md:138 per-block copy for the part of a large bin space where the
+    // events are; the bins outside go through the slots / L2 as before.  C5's H6 (1000x1000 on
+    // two Gaussians): a 55K-bin box holds ~2/3 of the events.
+    uint32_t wsm = 0;                    // shared-memory address of the box counts (0: none)
+    int wx0 = 0, wx = 0, wy0 = 0, wy = 0, wst = 1;
+    unsigned long long wmag = 0;         // ceil(2^40 / st1): b1 = (g * wmag) >> 40 exactly (g < 2^24)
+    __device__ __forceinline__ void init_win(const FillP &p, unsigned char *smem, int dim) {
+        if (W || !p.win) return;
+        wx0 = (int)__ldcg(p.win);
+        wx = (int)__ldcg(p.win + 1);
+        wy0 = (int)__ldcg(p.win + 2);
+        wy = (int)__ldcg(p.win + 3);
+        if (wx <= 0) return;
+        wst = p.st1;
+        wmag = dim >= 2 ? ((1ull << 40) + (unsigned long long)p.st1 - 1) / (unsigned long long)p.st1 : 0ull;
+        uint32_t *c = reinterpret_cast<uint32_t *>(smem + p.win_off);
+        for (int i = threadIdx.x; i < wx * wy; i += blockDim.x) c[i] = 0u;
+        wsm = (uint32_t)__cvta_generic_to_shared(c);
+    }
     __device__ __forceinline__ void put_count(int g, uint32_t c) {
+        if (wsm) {
+            const uint32_t by = wmag ? (uint32_t)(((unsigned long long)(uint32_t)g * wmag) >> 40) : 0u;
+            const uint32_t ux = (uint32_t)g - by * (uint32_t)wst - (uint32_t)wx0, uy = by - (uint32_t)wy0;
+            if (ux < (uint32_t)wx && uy < (uint32_t)wy) {
+                asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(wsm + 4u * (ux + (uint32_t)wx * uy)), "r"(c) : "memory");
+                return;
+            }
+        }
         const int sl = lookup((uint32_t)g);
         if (sl >= 0) atomicAdd(reinterpret_cast<uint32_t *>(vals) + sl, c);
         else atomicAdd(pp->count + g, (unsigned long long)c);
@@ -902,6 +1001,11 @@ struct CacheSink {
         }
     }
     __device__ __forceinline__ void flush(const FillP &p, const unsigned char *) {
+        if (wsm) {                       // the box -> global, once per CTA
+            const uint32_t *wc = reinterpret_cast<const uint32_t *>(__cvta_shared_to_generic(wsm));
+            for (int i = threadIdx.x; i < wx * wy; i += blockDim.x)
+                if (wc[i]) atomicAdd(p.count + (wx0 + i % wx) + (size_t)wst * (wy0 + i / wx), (unsigned long long)wc[i]);
+        }
         for (int i = threadIdx.x; i < S; i += blockDim.x) {
             const uint32_t k = keys[i];
             if (k == kEmpty) continue;
@@ -972,6 +1076,8 @@ __global__ void __launch_bounds__((FillThreads<SINK, DIM, W>::v), SINK == SINK_G
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
     else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas, p.wc_off);
     else sink.init(smem, p.G);
+    if constexpr (SINK == SINK_PRIVA && W) sink.init_hot(p, smem);
+    if constexpr (SINK == SINK_CACHE && !W && DIM <= 2) sink.init_win(p, smem, DIM);
     if constexpr (VM == 1 || VM == 3) stage_axes<DIM>(p.ax, smem);
     if constexpr (SINK != SINK_GLOBAL || VM == 1 || VM == 3) __syncthreads();
 

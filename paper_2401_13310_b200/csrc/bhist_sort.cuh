@@ -255,31 +255,63 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_part_scatter(FillP p, PartP
 // writes the largest partition's count: AUTO uses SORT for later large unit-weight fills
 // only when no partition is hot (a hot partition serializes pass 1's rank atomics).
 constexpr int kProbeHash = 4096;
+constexpr int kProbeMarg = 4096;                  // window: bins per axis (flow included) the probe histograms
+
+// Shortest run of consecutive bins of m[0..n) holding >= T samples (two pointers); len = n+1
+// when none does.
+__device__ inline void shortest_cover(const unsigned int *m, int n, unsigned int T, int &lo, int &len) {
+    lo = 0;
+    len = n + 1;
+    unsigned int sum = 0;
+    int r = 0;
+    for (int l = 0; l < n; ++l) {
+        while (r < n && sum < T) sum += m[r++];
+        if (sum < T) break;
+        if (r - l < len) { len = r - l; lo = l; }
+        sum -= m[l];
+    }
+}
 
 template <int DIM>
-__global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, int samples, unsigned int *out) {
+__global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, int samples, int amax, unsigned int *out) {
     // out[0]: largest partition count; out[1]: largest count of a hashed bin bucket
     // (4096 buckets: a single hot bin shows up as one large bucket); out[2]: the unit-weight
-    // decision, 1 (SORT) when no partition holds > 5% and no bucket > 1% of the samples, else
-    // 0 (CACHE); out[3]: the weighted decision, 1 (GLOBAL) when no bucket holds > 1/512 of the
-    // samples (a bin with a share f of n events costs f*n serialized same-address REDs, ~0.55
-    // G/s), else 0 (CACHE) -- read by the gated fills on the device, so AUTO's choice depends
-    // on the data only, never on timing
+    // decision, 2 (WINDOW) when a box of <= amax bins (per-axis shortest intervals holding
+    // the same share q of the sample's marginals, the largest q that fits) holds >= 50% of
+    // the samples, else 1 (SORT) when no partition holds > 5% and no bucket > 1% of the
+    // samples, else 0 (CACHE); out[3]: the weighted decision, 1 (GLOBAL) when no bucket holds
+    // > 1/512 of the samples (a bin with a share f of n events costs f*n serialized
+    // same-address REDs, ~0.55 G/s), else 0 (CACHE); out[4..7]: the box (x0, wx, y0, wy) --
+    // read by the gated fills on the device, so AUTO's choice depends on the data only, never
+    // on timing.  Window: DIM <= 2, axes of <= kProbeMarg bins each (flow included).
     extern __shared__ unsigned int pc[];
     unsigned int *hc = pc + P;
-    for (int i = threadIdx.x; i < P + kProbeHash; i += blockDim.x) pc[i] = 0u;
+    unsigned int *m0 = hc + kProbeHash, *m1 = m0 + kProbeMarg;
+    int *gs = reinterpret_cast<int *>(m1 + kProbeMarg);          // [samples] axis bins, packed
+    __shared__ int box[4];
+    __shared__ unsigned int inbox;
+    const int n0 = p.ax[0].n + 2, n1 = DIM >= 2 ? p.ax[1].n + 2 : 1;
+    const bool win = DIM <= 2 && amax > 0 && n0 <= kProbeMarg && n1 <= kProbeMarg;
+    for (int i = threadIdx.x; i < P + kProbeHash + 2 * kProbeMarg; i += blockDim.x) pc[i] = 0u;
+    if (threadIdx.x == 0) inbox = 0u;
     __syncthreads();
     const int64_t stride = p.n / samples;
     for (int k = threadIdx.x; k < samples; k += blockDim.x) {
         const int64_t e = (int64_t)k * stride;
-        int g = 0, mul = 1;
+        int g = 0, mul = 1, bb[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
-            g += find_bin(p.ax[a], p.x[a][e]) * mul;
+            bb[a] = find_bin(p.ax[a], p.x[a][e]);
+            g += bb[a] * mul;
             if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
         }
         atomicAdd(pc + ((uint32_t)g >> pb), 1u);
         atomicAdd(hc + (((uint32_t)g * 2654435761u) >> 20), 1u);
+        if (win) {
+            atomicAdd(m0 + bb[0], 1u);
+            if (DIM >= 2) atomicAdd(m1 + bb[DIM >= 2 ? 1 : 0], 1u);
+            gs[k] = bb[0] | (DIM >= 2 ? bb[DIM >= 2 ? 1 : 0] << 16 : 0);
+        }
     }
     __syncthreads();
     unsigned int m = 0, mh = 0;
@@ -291,10 +323,115 @@ __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, 
         atomicMax(out, m);
         atomicMax(out + 1, mh);
     }
+    if (threadIdx.x == 0) {                                       // the box: bisection on q
+        box[0] = 0; box[1] = 0; box[2] = 0; box[3] = 0;
+        if (win) {
+            unsigned int qlo = 0, qhi = (unsigned int)samples;       // covers qlo fits, qhi does not
+            int lo0, len0, lo1 = 0, len1 = 1;
+            shortest_cover(m0, n0, qhi, lo0, len0);
+            if (DIM >= 2) shortest_cover(m1, n1, qhi, lo1, len1);
+            if ((int64_t)len0 * len1 <= amax) qlo = qhi;
+            while (qhi - qlo > 1 && qlo < (unsigned int)samples) {
+                const unsigned int q = (qlo + qhi) / 2;
+                shortest_cover(m0, n0, q, lo0, len0);
+                if (DIM >= 2) shortest_cover(m1, n1, q, lo1, len1);
+                if (len0 <= n0 && len1 <= n1 && (int64_t)len0 * len1 <= amax) qlo = q; else qhi = q;
+            }
+            if (qlo > 0) {
+                shortest_cover(m0, n0, qlo, lo0, len0);
+                if (DIM >= 2) shortest_cover(m1, n1, qlo, lo1, len1);
+                box[0] = lo0; box[1] = len0; box[2] = lo1; box[3] = len1;
+            }
+        }
+    }
+    __syncthreads();
+    if (win && box[1] > 0) {
+        unsigned int c = 0;
+        for (int k = threadIdx.x; k < samples; k += blockDim.x) {
+            const int b0 = gs[k] & 0xffff, b1 = gs[k] >> 16;
+            c += (unsigned)(b0 - box[0]) < (unsigned)box[1] && (unsigned)(b1 - box[2]) < (unsigned)box[3];
+        }
+        c = __reduce_add_sync(0xffffffffu, c);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&inbox, c);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        out[2] = (20ull * out[0] <= (unsigned long long)samples && 100ull * out[1] <= (unsigned long long)samples) ? 1u : 0u;
-        out[3] = 512ull * out[1] <= (unsigned long long)samples ? 1u : 0u;
+        const unsigned long long S = (unsigned long long)samples;
+        out[2] = 2ull * inbox >= S && box[1] > 0 ? 2u : (20ull * out[0] <= S && 100ull * out[1] <= S) ? 1u : 0u;
+        out[3] = 512ull * out[1] <= S ? 1u : 0u;
+        for (int i = 0; i < 4; ++i) out[4 + i] = (unsigned int)box[i];
+    }
+}
+
+// ------------------------------------------------------------------ hot-cell probe (AUTO, weighted PRIVA)
+// One CTA counts the global bins of an evenly strided sample in a shared-memory hash table,
+// picks up to kHotW cells holding >= 1/64 of the sample each (hottest first), maps them
+// into the direct-mapped slot table (a colliding colder cell is dropped), and sets flag = 1
+// when the mapped cells hold >= 20% of the sample (then the lane-private window pays for the
+// 128 KB it takes from the replicas).  Deterministic: a fixed sample, fixed tie-breaks.
+constexpr int kHotHash = 4096;
+template <int DIM>
+__global__ void __launch_bounds__(1024, 1) k_hot_probe(FillP p, int samples, HotTab *out) {
+    __shared__ int32_t key[kHotHash];
+    __shared__ uint32_t cnt[kHotHash];
+    __shared__ int32_t pick[kHotW];
+    __shared__ uint32_t pickc[kHotW];
+    for (int i = threadIdx.x; i < kHotHash; i += blockDim.x) { key[i] = -1; cnt[i] = 0u; }
+    __syncthreads();
+    const int64_t stride = p.n / samples;
+    for (int k = threadIdx.x; k < samples; k += blockDim.x) {
+        const int64_t e = (int64_t)k * stride;
+        int g = 0, mul = 1;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            g += find_bin(p.ax[a], p.x[a][e]) * mul;
+            if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
+        }
+        int hs = (int)(((uint32_t)g * 2654435761u) >> 20);
+        for (int t = 0; t < 32; ++t, hs = (hs + 1) & (kHotHash - 1)) {      // a sparse cell may be dropped
+            const int old = atomicCAS(key + hs, -1, g);
+            if (old == -1 || old == g) { atomicAdd(cnt + hs, 1u); break; }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {                                   // warp 0: the hottest cells, in order
+        const int lane = threadIdx.x;
+        for (int r = 0; r < kHotW; ++r) {
+            uint32_t best = 0;
+            int bi = kHotHash;
+            for (int i = lane; i < kHotHash; i += 32)
+                if (cnt[i] > best) { best = cnt[i]; bi = i; }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint32_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            const bool ok = 64ull * best >= (unsigned long long)samples && bi < kHotHash;
+            if (lane == 0) {
+                pick[r] = ok ? key[bi] : -1;
+                pickc[r] = ok ? best : 0u;
+                if (ok) cnt[bi] = 0u;
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            for (int i = 0; i < kHotSlots; ++i) out->tab[i] = make_int2(-1, 0);
+            unsigned long long covered = 0;
+            int nwin = 0;
+            for (int r = 0; r < kHotW; ++r) {
+                out->cell[r] = -1;
+                if (pick[r] < 0) continue;
+                int2 &slot = out->tab[hot_slot(pick[r])];
+                if (slot.x != -1) continue;                   // collides with a hotter cell
+                slot = make_int2(pick[r], r);
+                out->cell[r] = pick[r];
+                covered += pickc[r];
+                nwin = r + 1;
+            }
+            out->nwin = nwin;
+            out->flag = 5ull * covered >= (unsigned long long)samples ? 1 : 0;
+        }
     }
 }
 

@@ -50,6 +50,10 @@ struct bh_hist {
     // AUTO's SORT decision for large unit-weight fills: 0 not probed since create/reset,
     // 1 probed (probe_dev[2] on the device: 1 SORT, 0 CACHE; both paths are launched gated)
     int probe_state = 0;
+    // AUTO's lane-private hot-cell window for large weighted PRIVA fills (k_hot_probe):
+    // 0 not probed since create/reset, 1 probed (hot_dev->flag on the device gates the kernels)
+    bh::HotTab *hot_dev = nullptr;
+    int hot_state = 0;
     unsigned int *probe_dev = nullptr;
     std::vector<void *> axis_mem;     // edges and guide tables
     // host->device double buffer

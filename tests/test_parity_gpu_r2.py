@@ -521,3 +521,57 @@ def test_read_as_int32_saturates():
     assert i["content"].tolist() == [0, 2147483647, 0] and i["entries"] == 9 * m
     assert f["content"].tolist() == [0.0, 2415919104.0, 0.0]
     h.close()
+
+
+# ------------------------------------------------------------------ hot-cell window (weighted PRIVA)
+@pytest.mark.parametrize("hidx,n", [(7, 1 << 23), (7, (1 << 22) + 7), (5, 1 << 23), (1, 1 << 23)])
+def test_hot_window_weighted_priva_matches_oracle(hidx, n):
+    """C5's peaked weighted H7 (50x50, ~75% of the events in 8 cells) takes the lane-private
+    window (device probe, gated kernels); H5/H1 (spread out) take plain PRIVA.  Both equal the
+    oracle; a second fill and a reset re-probe keep the result exact."""
+    wl = bhgen.workload("C5", n)
+    hist = wl.hists[hidx]
+    cols = [_t(wl.column(c, 0, n)) for c in hist.cols]
+    w = _t(wl.column(wl.wcol, 0, n))
+    h = pkg.Histogram(oracle.oracle_axes(hist))
+    h.fill(cols, w)
+    h.fill(cols, w)
+    got = h.read()
+    ref = oracle_parallel("C5", n, hidx=hidx)
+    compare(got, {k: 2 * v for k, v in ref.items()}, True, f"C5 H{hidx} x2 (hot window)")
+    h.reset()
+    h.fill(cols, w)
+    compare(h.read(), ref, True, f"C5 H{hidx} after reset")
+    h.close()
+
+
+# ------------------------------------------------------------------ unit-weight WINDOW (AUTO probe decision 2)
+@pytest.mark.slow
+@pytest.mark.parametrize("case", ["C5 H6", "1D 200k gauss"])
+def test_auto_window_unit_matches_oracle(case):
+    """Large unit-weight bin spaces whose events concentrate in a box (C5's H6: 1000x1000 on
+    two Gaussians; a 200,000-bin 1-D Gaussian) take CACHE with the probe's dense box of
+    private shared-memory counts: counts bit-exact vs the oracle, fresh histograms identical."""
+    n = 40_000_001
+    if case == "C5 H6":
+        wl = bhgen.workload("C5", n)
+        hist = wl.hists[6]
+        cols = [wl.column(c, 0, n) for c in hist.cols]
+        axes = oracle.oracle_axes(hist)
+        ref = oracle_parallel("C5", n, hidx=6)
+    else:
+        wl = bhgen.workload("C2", n)                  # N(0.5, 0.15) column
+        cols = [wl.column(wl.hists[0].cols[0], 0, n)]
+        axes = [(200_000, 0.0, 1.0)]
+        ref = oracle.OracleHist(axes).fill(cols).read()
+    tc = [_t(c) for c in cols]
+    outs = []
+    for rep in range(2):
+        h = pkg.Histogram(axes)
+        h.fill(tc)
+        h.fill(tc)
+        outs.append(h.read())
+        h.close()
+    a, b = outs
+    assert np.array_equal(a["content"], b["content"]) and a["stats"].tobytes() == b["stats"].tobytes()
+    compare(a, {k: 2 * v for k, v in ref.items()}, False, f"AUTO window {case}")

@@ -444,7 +444,7 @@ const int32_t *auto_gate(bh_hist *h, int64_t n, const double *const *coords, boo
         size_t woff = 0;
         int amax = 0;
         if (getenv("BHIST_NO_AUTO_WINDOW") || !win_plan(h, n, pw, woff, amax)) amax = 0;
-        const size_t sm = sizeof(unsigned int) * (P + kProbeHash + 2 * kProbeMarg + kProbeSamples);
+        const size_t sm = sizeof(unsigned int) * (P + kProbeHash + 4 * kProbeMarg + 2 + kProbeSamples);
         cudaError_t e;
         switch (h->dim) {
         case 1:
@@ -468,13 +468,17 @@ const int32_t *auto_gate(bh_hist *h, int64_t n, const double *const *coords, boo
     return reinterpret_cast<const int32_t *>(h->probe_dev + (weighted ? 3 : 2));
 }
 
-// AUTO's lane-private window of hot cells (see HotTab) for large weighted PRIVA fills: the
-// first such fill after create/reset launches k_hot_probe on a strided sample of its events;
-// that fill and every later one launch the window kernel and the plain one, gated on the
-// probe's device flag.  Returns the device table, or nullptr (plain PRIVA).
+// AUTO's lane-private window of hot cells (see HotTab) for large weighted PRIVA and CACHE
+// fills: the first such fill after create/reset launches k_hot_probe on a strided sample of
+// its events; that fill and every later one launch the window kernel and the plain one (and,
+// for CACHE, the GLOBAL one of k_part_probe's decision `gdec`), gated on the probe's device
+// word.  Returns the device table, or nullptr (no window).
 constexpr int64_t kHotMinEvents = int64_t(1) << 22;
-const HotTab *auto_hot(bh_hist *h, int64_t n, const double *const *coords, const FillPlan &pl, cudaStream_t s) {
-    if (h->strategy != BH_STRATEGY_AUTO || pl.c.strategy != BH_STRATEGY_PRIV || pl.wc_off < 0 || n < kHotMinEvents ||
+constexpr int kHotCacheSlots = 4096;       // CACHE's slots next to the lane window
+const HotTab *auto_hot(bh_hist *h, int64_t n, const double *const *coords, const FillPlan &pl,
+                       const int32_t *gdec, cudaStream_t s) {
+    const bool priva = pl.c.strategy == BH_STRATEGY_PRIV && pl.wc_off >= 0;
+    if (h->strategy != BH_STRATEGY_AUTO || !(priva || pl.c.strategy == BH_STRATEGY_CACHE) || n < kHotMinEvents ||
         getenv("BHIST_NO_HOT_WINDOW"))
         return nullptr;
     if (!h->hot_dev) {
@@ -485,10 +489,11 @@ const HotTab *auto_hot(bh_hist *h, int64_t n, const double *const *coords, const
     }
     if (h->hot_state == 0) {
         FillP p = make_params(h, n, coords, nullptr);
+        const unsigned int *gd = reinterpret_cast<const unsigned int *>(gdec);
         switch (h->dim) {
-        case 1: k_hot_probe<1><<<1, 1024, 0, s>>>(p, kProbeSamples, h->hot_dev); break;
-        case 2: k_hot_probe<2><<<1, 1024, 0, s>>>(p, kProbeSamples, h->hot_dev); break;
-        default: k_hot_probe<3><<<1, 1024, 0, s>>>(p, kProbeSamples, h->hot_dev); break;
+        case 1: k_hot_probe<1><<<1, 1024, 0, s>>>(p, kProbeSamples, gd, h->hot_dev); break;
+        case 2: k_hot_probe<2><<<1, 1024, 0, s>>>(p, kProbeSamples, gd, h->hot_dev); break;
+        default: k_hot_probe<3><<<1, 1024, 0, s>>>(p, kProbeSamples, gd, h->hot_dev); break;
         }
         if (cudaGetLastError() != cudaSuccess) return nullptr;
         h->launches++;
@@ -514,11 +519,14 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
     size_t win_off = 0;
     int win_amax = 0;
     const bool winp = gate && !w && !getenv("BHIST_NO_AUTO_WINDOW") && win_plan(h, n, pwin, win_off, win_amax);
-    // weighted PRIVA: the hot-cell window variant, run iff the probe's flag says so
-    const HotTab *hot = w ? auto_hot(h, n, coords, pl, s) : nullptr;
+    // weighted PRIVA / CACHE: the hot-cell window variant, run iff the probe's word says 2
+    const HotTab *hot = w ? auto_hot(h, n, coords, pl, gate, s) : nullptr;
     FillPlan phot;
-    const size_t hot_bytes = hot_smem_bytes(threads_of(BH_STRATEGY_PRIV, true));
-    if (hot && (plan_fill(h, true, phot, n, hot_bytes) != BH_OK || phot.c.strategy != BH_STRATEGY_PRIV || phot.wc_off < 0)) {
+    const bool hot_cache = pl.c.strategy == BH_STRATEGY_CACHE;
+    const size_t hot_bytes = hot_smem_bytes(threads_of(pl.c.strategy, true, h->dim));
+    if (hot && (hot_cache ? plan_fill(h, true, phot, n, hot_bytes, BH_STRATEGY_CACHE, kHotCacheSlots) != BH_OK
+                          : plan_fill(h, true, phot, n, hot_bytes) != BH_OK || phot.c.strategy != BH_STRATEGY_PRIV ||
+                                phot.wc_off < 0)) {
         hot = nullptr;
         g_err.clear();
     }
@@ -565,10 +573,11 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
             for (int a = 0; a < h->dim; ++a) pq.ax[a] = phot.ax[a];
             pq.replicas = phot.replicas;
             pq.wc_off = phot.wc_off;
+            if (hot_cache) pq.cache_slots = kHotCacheSlots;
             pq.hot = hot;
             pq.hot_off = (int32_t)align16(phot.c.smem);
             pq.gate = &hot->flag;
-            pq.gate_run = 1;
+            pq.gate_run = 2;
             LaunchCfg ch = phot.c;
             ch.smem = pq.hot_off + hot_bytes;
             ch.vec = c.vec;

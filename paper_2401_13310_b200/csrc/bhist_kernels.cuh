@@ -635,7 +635,7 @@ struct RegHot {
 constexpr int kHotW = 8;                 // window cells per thread (8 x 16 B x 1024 threads = 128 KB)
 constexpr int kHotSlots = 64;
 struct HotTab {
-    int32_t flag, nwin;                  // flag: window worth using (gate); nwin: cells chosen
+    int32_t flag, nwin;                  // flag (gate word): 2 window kernel, 1 GLOBAL, 0 plain; nwin: cells
     int32_t cell[kHotW];                 // global bin of window cell k (-1: none)
     int2 tab[kHotSlots];                 // slot -> {global bin, k}; x = -1 empty
 };
@@ -643,15 +643,60 @@ constexpr int kHotTabSmem = kHotSlots * 8 + kHotW * 4;     // staged table + cel
 __host__ __device__ constexpr size_t hot_smem_bytes(int threads) { return kHotTabSmem + (size_t)kHotW * 16 * threads; }
 __host__ __device__ __forceinline__ int hot_slot(int g) { return (int)(((uint32_t)g * 2654435761u) >> 26); }
 
+struct LaneWindow {
+    const int2 *htab = nullptr;          // staged slot table
+    const int32_t *hcell = nullptr;      // window cell -> global bin (-1: none)
+    double2 *hlane = nullptr;            // this thread's copy of window cell 0 (stride blockDim)
+    int hn = 0;                          // window cells (0: no window)
+    __device__ __forceinline__ void init(const HotTab *hot, unsigned char *b) {
+        int2 *t = reinterpret_cast<int2 *>(b);
+        int32_t *c = reinterpret_cast<int32_t *>(b + kHotSlots * 8);
+        for (int i = threadIdx.x; i < kHotSlots; i += blockDim.x) t[i] = hot->tab[i];
+        if (threadIdx.x < kHotW) c[threadIdx.x] = hot->cell[threadIdx.x];
+        hn = hot->nwin;
+        htab = t;
+        hcell = c;
+        hlane = reinterpret_cast<double2 *>(b + kHotTabSmem) + threadIdx.x;
+        for (int k = 0; k < kHotW; ++k) hlane[k * blockDim.x] = make_double2(0.0, 0.0);
+    }
+    // (g, w) of a window cell goes to this thread's private copy: plain read-modify-write
+    __device__ __forceinline__ bool add(int g, double w) {
+        if (!hn) return false;
+        const int2 e = htab[hot_slot(g)];
+        if (e.x != g) return false;
+        double2 *c = hlane + e.y * blockDim.x;
+        double2 v = *c;
+        v.x += w;
+        v.y = fma(w, w, v.y);
+        *c = v;
+        return true;
+    }
+    // every lane of every warp: the warp's lane copies summed by shuffles, lane 0 spills them
+    template <typename Spill>
+    __device__ __forceinline__ void drain(Spill spill) {
+        if (!hn) return;
+        __syncwarp();
+        for (int k = 0; k < kHotW; ++k) {
+            const int g = hcell[k];
+            if (g < 0) continue;         // (uniform)
+            double2 v = hlane[k * blockDim.x];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+                v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+            }
+            if ((threadIdx.x & 31) == 0 && (v.x != 0.0 || v.y != 0.0)) spill(g, v.x, v.y);
+        }
+        __syncwarp();
+    }
+};
+
 template <bool W, bool ADAPT>
 struct PrivSink {
     uint32_t sm;         // shared-memory address of this warp's replica
     bool agg;            // ADAPT: the warp's previous add collided -> aggregate this one first
     WarpHot hot;         // ADAPT && W: this warp's hot-bin cache
-    const int2 *htab = nullptr;          // lane-private window (see HotTab): staged slot table,
-    const int32_t *hcell = nullptr;      // window cell -> global bin,
-    double2 *hlane = nullptr;            // this thread's copy of window cell 0 (stride blockDim)
-    int hn = 0;                          // window cells (0: no window)
+    LaneWindow lw;                       // lane-private window of hot cells (see HotTab)
     static constexpr int kCell = W ? 16 : 4;
     static __device__ __forceinline__ size_t stride_of(int G) { return ((size_t)G * kCell + 15) & ~size_t(15); }
     __device__ __forceinline__ void init(unsigned char *s, int G, int R, int wc_off = -1) {
@@ -670,29 +715,10 @@ struct PrivSink {
     // weighted PRIVA with a hot-cell window (k_fill, p.hot set): stage the table, zero the lane cells
     __device__ __forceinline__ void init_hot(const FillP &p, unsigned char *smem) {
         if (!(W && ADAPT) || !p.hot) return;
-        unsigned char *b = smem + p.hot_off;
-        int2 *t = reinterpret_cast<int2 *>(b);
-        int32_t *c = reinterpret_cast<int32_t *>(b + kHotSlots * 8);
-        for (int i = threadIdx.x; i < kHotSlots; i += blockDim.x) t[i] = p.hot->tab[i];
-        if (threadIdx.x < kHotW) c[threadIdx.x] = p.hot->cell[threadIdx.x];
-        hn = p.hot->nwin;
-        htab = t;
-        hcell = c;
-        hlane = reinterpret_cast<double2 *>(b + kHotTabSmem) + threadIdx.x;
-        for (int k = 0; k < kHotW; ++k) hlane[k * blockDim.x] = make_double2(0.0, 0.0);
+        lw.init(p.hot, smem + p.hot_off);
     }
     __device__ __forceinline__ void add(int g, double w) {
-        if (W && ADAPT && hn) {          // a window cell: this thread's private copy
-            const int2 e = htab[hot_slot(g)];
-            if (e.x == g) {
-                double2 *c = hlane + e.y * blockDim.x;
-                double2 v = *c;
-                v.x += w;
-                v.y = fma(w, w, v.y);
-                *c = v;
-                return;
-            }
-        }
+        if (W && ADAPT && lw.add(g, w)) return;     // a window cell: this thread's private copy
         if (W) {
             double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
 #ifdef BH_EXP_NOCAS   // experiment only (wrong results): plain read-modify-write instead of CAS
@@ -740,20 +766,9 @@ struct PrivSink {
     }
     // Before the block barrier of the merge stage: hot-bin caches -> this warp's replica.
     __device__ __forceinline__ void drain() {
-        if (ADAPT && W && hn) {          // window: the warp's lane copies -> its replica
+        if (ADAPT && W) {                // window: the warp's lane copies -> its replica
             double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
-            __syncwarp();
-            for (int k = 0; k < kHotW; ++k) {
-                const int g = hcell[k];
-                if (g < 0) continue;     // (uniform)
-                double2 v = hlane[k * blockDim.x];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-                    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
-                }
-                if ((threadIdx.x & 31) == 0 && (v.x != 0.0 || v.y != 0.0)) add2_shared(base + g, v.x, v.y);
-            }
+            lw.drain([&](int g, double a1, double a2) { add2_shared(base + g, a1, a2); });
         }
         if (ADAPT && W) {
             double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
@@ -865,6 +880,10 @@ struct CacheSink {
         return k == g ? sl : -1;
     }
     RegHot lc;        // W: this thread's hot bin (in front of the warp aggregation)
+    LaneWindow lw;    // W, AUTO's hot-cell window (k_hot_probe): lane-private copies of the hot cells
+    __device__ __forceinline__ void init_hot(const FillP &p, unsigned char *smem) {
+        if (W && p.hot) lw.init(p.hot, smem + p.hot_off);
+    }
     // unit weights: the thread's hot bin as a register count (same stickiness rule as RegHot);
     // the other events go one by one to their slot or the global count, no warp aggregation
     int ug = -1;
@@ -904,6 +923,7 @@ struct CacheSink {
         else atomicAdd(pp->count + g, (unsigned long long)c);
     }
     __device__ __forceinline__ void add(int g, double w) {
+        if (W && lw.add(g, w)) return;
 #if BH_LANE_CACHE
         if (W) {
             uint32_t on;
@@ -999,6 +1019,7 @@ struct CacheSink {
             double o1, o2;
             if (lc.take(og, on, o1, o2)) put(og, o1, o2);
         }
+        if (W) lw.drain([&](int g, double a1, double a2) { put(g, a1, a2); });
     }
     __device__ __forceinline__ void flush(const FillP &p, const unsigned char *) {
         if (wsm) {                       // the box -> global, once per CTA
@@ -1078,6 +1099,7 @@ __global__ void __launch_bounds__((FillThreads<SINK, DIM, W>::v), SINK == SINK_G
     else sink.init(smem, p.G);
     if constexpr (SINK == SINK_PRIVA && W) sink.init_hot(p, smem);
     if constexpr (SINK == SINK_CACHE && !W && DIM <= 2) sink.init_win(p, smem, DIM);
+    if constexpr (SINK == SINK_CACHE && W) sink.init_hot(p, smem);
     if constexpr (VM == 1 || VM == 3) stage_axes<DIM>(p.ax, smem);
     if constexpr (SINK != SINK_GLOBAL || VM == 1 || VM == 3) __syncthreads();
 

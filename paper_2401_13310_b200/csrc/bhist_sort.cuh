@@ -251,25 +251,74 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_part_scatter(FillP p, PartP
 
 #ifndef BH_FILL_TU
 // ------------------------------------------------------------------ hotness probe (AUTO)
-// One CTA bins an evenly strided sample of a fill's events (global-memory FindBin) and
+// One CTA bins a sample of a fill's events (probe_load; global-memory FindBin) and
 // writes the largest partition's count: AUTO uses SORT for later large unit-weight fills
 // only when no partition is hot (a hot partition serializes pass 1's rank atomics).
 constexpr int kProbeHash = 4096;
 constexpr int kProbeMarg = 4096;                  // window: bins per axis (flow included) the probe histograms
 
-// Shortest run of consecutive bins of m[0..n) holding >= T samples (two pointers); len = n+1
-// when none does.
-__device__ inline void shortest_cover(const unsigned int *m, int n, unsigned int T, int &lo, int &len) {
-    lo = 0;
-    len = n + 1;
-    unsigned int sum = 0;
-    int r = 0;
-    for (int l = 0; l < n; ++l) {
-        while (r < n && sum < T) sum += m[r++];
-        if (sum < T) break;
-        if (r - l < len) { len = r - l; lo = l; }
-        sum -= m[l];
+// The probes' sample: kProbeRuns runs of consecutive events spread evenly over the fill
+// (sample k = event (k / run) * (n / kProbeRuns) + k % run): a warp reads 32 consecutive
+// events per column, not 32 scattered 32-byte sectors; a batch of kProbeBatch samples per
+// thread is loaded before any is binned.  (Strided single events cost ~70 us per probe.)
+constexpr int kProbeBatch = 4;
+constexpr int kProbeRuns = 64;
+template <int DIM>
+__device__ __forceinline__ void probe_load(const FillP &p, int k0, int samples, double (&xv)[kProbeBatch][DIM]) {
+    const int run = samples / kProbeRuns;
+    const int64_t gap = p.n / kProbeRuns;
+#pragma unroll
+    for (int j = 0; j < kProbeBatch; ++j) {
+        const int k = k0 + j * (int)blockDim.x;
+        const int64_t e = (int64_t)(k / run) * gap + (k % run);
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) xv[j][a] = k < samples ? __ldg(p.x[a] + e) : 0.0;
     }
+}
+
+// Block-wide: shortest run of consecutive bins holding >= T samples, from the inclusive-
+// exclusive prefix sums ps[0..n] (ps[0] = 0): each thread takes starts l, finds the first end
+// r with ps[r] - ps[l] >= T by binary search, and the block keeps the minimum (len, l).
+// Returns (len << 16) | lo, or 0xffffffff when no run holds T.  All threads call it.
+__device__ inline unsigned int shortest_cover(const unsigned int *ps, int n, unsigned int T, unsigned int *red) {
+    if (threadIdx.x == 0) *red = 0xffffffffu;
+    __syncthreads();
+    unsigned int bestv = 0xffffffffu;
+    for (int l = threadIdx.x; l < n; l += blockDim.x) {
+        const unsigned int need = ps[l] + T;
+        if (ps[n] < need) continue;
+        int lo = l + 1, hi = n;                      // first r in [l+1, n] with ps[r] >= need
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ps[mid] >= need) hi = mid; else lo = mid + 1;
+        }
+        bestv = min(bestv, ((unsigned int)(lo - l) << 16) | (unsigned int)l);
+    }
+    bestv = __reduce_min_sync(0xffffffffu, bestv);
+    if ((threadIdx.x & 31) == 0) atomicMin(red, bestv);
+    __syncthreads();
+    const unsigned int v = *red;
+    __syncthreads();
+    return v;
+}
+
+// in-place exclusive prefix sums of m[0..n) into ps[0..n] (warp 0; n <= kProbeMarg)
+__device__ inline void prefix_sums(const unsigned int *m, int n, unsigned int *ps) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x, per = (n + 31) / 32, b = lane * per;
+        unsigned int loc = 0;
+        for (int i = b; i < min(n, b + per); ++i) loc += m[i];
+        unsigned int inc = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        unsigned int run = inc - loc;
+        for (int i = b; i < min(n, b + per); ++i) { ps[i] = run; run += m[i]; }
+        if (lane == 31) ps[n] = inc;
+    }
+    __syncthreads();
 }
 
 template <int DIM>
@@ -287,7 +336,9 @@ __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, 
     extern __shared__ unsigned int pc[];
     unsigned int *hc = pc + P;
     unsigned int *m0 = hc + kProbeHash, *m1 = m0 + kProbeMarg;
-    int *gs = reinterpret_cast<int *>(m1 + kProbeMarg);          // [samples] axis bins, packed
+    unsigned int *ps0 = m1 + kProbeMarg, *ps1 = ps0 + kProbeMarg + 1;    // prefix sums [n + 1]
+    int *gs = reinterpret_cast<int *>(ps1 + kProbeMarg + 1);     // [samples] axis bins, packed
+    __shared__ unsigned int red;
     __shared__ int box[4];
     __shared__ unsigned int inbox;
     const int n0 = p.ax[0].n + 2, n1 = DIM >= 2 ? p.ax[1].n + 2 : 1;
@@ -295,16 +346,22 @@ __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, 
     for (int i = threadIdx.x; i < P + kProbeHash + 2 * kProbeMarg; i += blockDim.x) pc[i] = 0u;
     if (threadIdx.x == 0) inbox = 0u;
     __syncthreads();
-    const int64_t stride = p.n / samples;
-    for (int k = threadIdx.x; k < samples; k += blockDim.x) {
-        const int64_t e = (int64_t)k * stride;
+    double xv[kProbeBatch][DIM];
+    for (int base = 0; base < samples; base += kProbeBatch * (int)blockDim.x) {     // warp-uniform trips
+      const int k0 = base + (int)threadIdx.x;
+      probe_load<DIM>(p, k0, samples, xv);       // the batch's (random) loads first
+#pragma unroll
+      for (int j = 0; j < kProbeBatch; ++j) {
+        const int k = k0 + j * (int)blockDim.x;
+        const bool ok = k < samples;
         int g = 0, mul = 1, bb[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
-            bb[a] = find_bin(p.ax[a], p.x[a][e]);
+            bb[a] = find_bin(p.ax[a], xv[j][a]);
             g += bb[a] * mul;
             if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
         }
+        if (!ok) continue;
         atomicAdd(pc + ((uint32_t)g >> pb), 1u);
         atomicAdd(hc + (((uint32_t)g * 2654435761u) >> 20), 1u);
         if (win) {
@@ -312,6 +369,7 @@ __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, 
             if (DIM >= 2) atomicAdd(m1 + bb[DIM >= 2 ? 1 : 0], 1u);
             gs[k] = bb[0] | (DIM >= 2 ? bb[DIM >= 2 ? 1 : 0] << 16 : 0);
         }
+      }
     }
     __syncthreads();
     unsigned int m = 0, mh = 0;
@@ -323,25 +381,27 @@ __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, 
         atomicMax(out, m);
         atomicMax(out + 1, mh);
     }
-    if (threadIdx.x == 0) {                                       // the box: bisection on q
-        box[0] = 0; box[1] = 0; box[2] = 0; box[3] = 0;
-        if (win) {
-            unsigned int qlo = 0, qhi = (unsigned int)samples;       // covers qlo fits, qhi does not
-            int lo0, len0, lo1 = 0, len1 = 1;
-            shortest_cover(m0, n0, qhi, lo0, len0);
-            if (DIM >= 2) shortest_cover(m1, n1, qhi, lo1, len1);
-            if ((int64_t)len0 * len1 <= amax) qlo = qhi;
-            while (qhi - qlo > 1 && qlo < (unsigned int)samples) {
-                const unsigned int q = (qlo + qhi) / 2;
-                shortest_cover(m0, n0, q, lo0, len0);
-                if (DIM >= 2) shortest_cover(m1, n1, q, lo1, len1);
-                if (len0 <= n0 && len1 <= n1 && (int64_t)len0 * len1 <= amax) qlo = q; else qhi = q;
+    // the box: bisection on the sample share q (the largest q whose per-axis shortest
+    // intervals fit amax bins), each interval found block-parallel on prefix sums
+    if (threadIdx.x == 0) { box[0] = 0; box[1] = 0; box[2] = 0; box[3] = 0; }
+    if (win) {
+        prefix_sums(m0, n0, ps0);
+        if (DIM >= 2) prefix_sums(m1, n1, ps1);
+        unsigned int qlo = 0, qhi = (unsigned int)samples + 1;        // qlo fits, qhi does not
+        unsigned int b0 = 0, b1 = 1u << 16;
+        while (qhi - qlo > 1u + (unsigned int)samples / 1024) {
+            const unsigned int q = (qlo + qhi) / 2;
+            const unsigned int c0 = shortest_cover(ps0, n0, q, &red);
+            const unsigned int c1 = DIM >= 2 ? shortest_cover(ps1, n1, q, &red) : (1u << 16);
+            if (c0 != 0xffffffffu && c1 != 0xffffffffu && (int64_t)(c0 >> 16) * (c1 >> 16) <= amax) {
+                qlo = q; b0 = c0; b1 = c1;
+            } else {
+                qhi = q;
             }
-            if (qlo > 0) {
-                shortest_cover(m0, n0, qlo, lo0, len0);
-                if (DIM >= 2) shortest_cover(m1, n1, qlo, lo1, len1);
-                box[0] = lo0; box[1] = len0; box[2] = lo1; box[3] = len1;
-            }
+        }
+        if (threadIdx.x == 0 && qlo > 0) {
+            box[0] = (int)(b0 & 0xffffu); box[1] = (int)(b0 >> 16);
+            box[2] = (int)(b1 & 0xffffu); box[3] = (int)(b1 >> 16);
         }
     }
     __syncthreads();
@@ -364,34 +424,43 @@ __global__ void __launch_bounds__(1024, 1) k_part_probe(FillP p, int pb, int P, 
 }
 
 // ------------------------------------------------------------------ hot-cell probe (AUTO, weighted PRIVA)
-// One CTA counts the global bins of an evenly strided sample in a shared-memory hash table,
+// One CTA counts the global bins of a sample (probe_load) in a shared-memory hash table,
 // picks up to kHotW cells holding >= 1/64 of the sample each (hottest first), maps them
-// into the direct-mapped slot table (a colliding colder cell is dropped), and sets flag = 1
+// into the direct-mapped slot table (a colliding colder cell is dropped), and sets flag = 2
 // when the mapped cells hold >= 20% of the sample (then the lane-private window pays for the
-// 128 KB it takes from the replicas).  Deterministic: a fixed sample, fixed tie-breaks.
+// shared memory it takes from the replicas / slots); flag = 1 passes on k_part_probe's GLOBAL
+// decision (weighted CACHE fills).  Deterministic: a fixed sample, fixed tie-breaks.
 constexpr int kHotHash = 4096;
 template <int DIM>
-__global__ void __launch_bounds__(1024, 1) k_hot_probe(FillP p, int samples, HotTab *out) {
+__global__ void __launch_bounds__(1024, 1) k_hot_probe(FillP p, int samples, const unsigned int *gdec, HotTab *out) {
     __shared__ int32_t key[kHotHash];
     __shared__ uint32_t cnt[kHotHash];
     __shared__ int32_t pick[kHotW];
     __shared__ uint32_t pickc[kHotW];
     for (int i = threadIdx.x; i < kHotHash; i += blockDim.x) { key[i] = -1; cnt[i] = 0u; }
     __syncthreads();
-    const int64_t stride = p.n / samples;
-    for (int k = threadIdx.x; k < samples; k += blockDim.x) {
-        const int64_t e = (int64_t)k * stride;
+    double xv[kProbeBatch][DIM];
+    for (int base = 0; base < samples; base += kProbeBatch * (int)blockDim.x) {     // warp-uniform trips
+      const int k0 = base + (int)threadIdx.x;
+      probe_load<DIM>(p, k0, samples, xv);
+#pragma unroll
+      for (int j = 0; j < kProbeBatch; ++j) {
+        const bool ok = k0 + j * (int)blockDim.x < samples;
         int g = 0, mul = 1;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
-            g += find_bin(p.ax[a], p.x[a][e]) * mul;
+            g += find_bin(p.ax[a], xv[j][a]) * mul;
             if (a + 1 < DIM) mul = (a == 0) ? p.st1 : p.st2;
         }
+        // equal cells of the warp first (hot cells would serialize the table's atomics)
+        const unsigned m = __match_any_sync(0xffffffffu, ok ? g : -1 - (int)(threadIdx.x & 31));
+        if (!ok || (int)(threadIdx.x & 31) != __ffs(m) - 1) continue;
         int hs = (int)(((uint32_t)g * 2654435761u) >> 20);
-        for (int t = 0; t < 32; ++t, hs = (hs + 1) & (kHotHash - 1)) {      // a sparse cell may be dropped
+        for (int t = 0; t < 8; ++t, hs = (hs + 1) & (kHotHash - 1)) {       // a sparse cell may be dropped
             const int old = atomicCAS(key + hs, -1, g);
-            if (old == -1 || old == g) { atomicAdd(cnt + hs, 1u); break; }
+            if (old == -1 || old == g) { atomicAdd(cnt + hs, (unsigned)__popc(m)); break; }
         }
+      }
     }
     __syncthreads();
     if (threadIdx.x < 32) {                                   // warp 0: the hottest cells, in order
@@ -430,7 +499,9 @@ __global__ void __launch_bounds__(1024, 1) k_hot_probe(FillP p, int samples, Hot
                 nwin = r + 1;
             }
             out->nwin = nwin;
-            out->flag = 5ull * covered >= (unsigned long long)samples ? 1 : 0;
+            // the gate word of the weighted fill: 1 GLOBAL (k_part_probe's decision, when given),
+            // else 2 (window kernel) or 0 (plain sink)
+            out->flag = gdec && __ldcg(gdec) == 1u ? 1 : 5ull * covered >= (unsigned long long)samples ? 2 : 0;
         }
     }
 }

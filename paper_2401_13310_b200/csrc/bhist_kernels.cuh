@@ -95,12 +95,12 @@ struct FillP {
     double *stats;               // [K], running totals
     unsigned long long *entries; // running entries
     int64_t entries_add;         // added to *entries by the last CTA
-    const unsigned int *win;     // unit CACHE: the probe's dense box (x0, wx, y0, wy) of bins kept as
-    int32_t win_off;             // shared-memory u32 counts at byte win_off (nullptr: none)
-    const struct HotTab *hot;    // weighted PRIVA: lane-private window of hot cells (nullptr: none)
-    int32_t hot_off;             // its byte offset in shared memory (table, cell list, lane cells)
     const int32_t *gate;         // AUTO's device-side strategy decision: the kernel runs only if
     int32_t gate_run;            // gate == nullptr or *gate == gate_run (otherwise every CTA exits)
+    const unsigned int *win;     // unit CACHE: the probe's dense box (x0, wx, y0, wy) of bins kept as
+    int32_t win_off;             // shared-memory u32 counts at byte win_off (nullptr: none)
+    int32_t hot_off;             // weighted PRIVA / CACHE: byte offset of the lane window in shared memory
+    const struct HotTab *hot;    // the lane-private window of hot cells (nullptr: none)
 };
 
 __device__ __forceinline__ bool gated_off(const int32_t *gate, int32_t run) { return gate && __ldcg(gate) != run; }
@@ -211,13 +211,15 @@ __device__ __forceinline__ int compact_cell(const AxisP &a, double x, int &q) {
     return c;
 }
 
-static __device__ __noinline__ int compact_slow(const AxisP &a, double x, const uint32_t *tab, int c, int lo, int cnt) {
+// (the edges by pointer, not the AxisP by reference: a reference into the kernel parameters
+// makes nvcc copy the whole FillP to local memory -- measured +9% instructions on C2)
+static __device__ __noinline__ int compact_slow(const double *e, double x, const uint32_t *tab, int c, int lo, int cnt) {
     // count the cell's interior edges e[lo+1 .. hi] <= x exactly (ties / >= 3 edges)
     int hi = cnt < 3 ? lo + cnt : (int)(tab[c + 1] & 0x3fffu);
     int l = lo;                                      // largest l in [lo, hi] with l == lo or e[l] <= x
     while (l < hi) {
         const int m = (l + hi + 1) >> 1;
-        if (__ldg(a.e + m) <= x) l = m; else hi = m - 1;
+        if (__ldg(e + m) <= x) l = m; else hi = m - 1;
     }
     return 1 + l;
 }
@@ -233,7 +235,7 @@ __device__ __forceinline__ int find_bin_var_compact(const AxisP &a, double x, co
     const int lo = (int)(v & 0x3fffu), cnt = (int)((v >> 14) & 3u);
     const int p1 = (int)((v >> 16) & 255u), p2 = (int)(v >> 24);
     const bool tie = (cnt >= 1 && q == p1) || (cnt >= 2 && q == p2);
-    if (tie || cnt == 3) return compact_slow(a, x, tab, c, lo, cnt);
+    if (tie || cnt == 3) return compact_slow(a.e, x, tab, c, lo, cnt);
     return 1 + lo + (int)(cnt >= 1 && q > p1) + (int)(cnt >= 2 && q > p2);
 }
 
@@ -643,6 +645,12 @@ constexpr int kHotTabSmem = kHotSlots * 8 + kHotW * 4;     // staged table + cel
 __host__ __device__ constexpr size_t hot_smem_bytes(int threads) { return kHotTabSmem + (size_t)kHotW * 16 * threads; }
 __host__ __device__ __forceinline__ int hot_slot(int g) { return (int)(((uint32_t)g * 2654435761u) >> 26); }
 
+template <bool B, class T, class F> struct PickT { using type = T; };   // (NVRTC: no <type_traits>)
+template <class T, class F> struct PickT<false, T, F> { using type = F; };
+struct NoLaneWindow {
+    __device__ __forceinline__ bool add(int, double) { return false; }
+    template <typename Spill> __device__ __forceinline__ void drain(Spill) {}
+};
 struct LaneWindow {
     const int2 *htab = nullptr;          // staged slot table
     const int32_t *hcell = nullptr;      // window cell -> global bin (-1: none)
@@ -696,7 +704,9 @@ struct PrivSink {
     uint32_t sm;         // shared-memory address of this warp's replica
     bool agg;            // ADAPT: the warp's previous add collided -> aggregate this one first
     WarpHot hot;         // ADAPT && W: this warp's hot-bin cache
-    LaneWindow lw;                       // lane-private window of hot cells (see HotTab)
+    // lane-private window of hot cells (see HotTab); an empty member unless W && ADAPT (a
+    // LaneWindow in the plain sink made nvcc keep the kernel parameters in local memory)
+    typename PickT<W && ADAPT, LaneWindow, NoLaneWindow>::type lw;
     static constexpr int kCell = W ? 16 : 4;
     static __device__ __forceinline__ size_t stride_of(int G) { return ((size_t)G * kCell + 15) & ~size_t(15); }
     __device__ __forceinline__ void init(unsigned char *s, int G, int R, int wc_off = -1) {

@@ -210,8 +210,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     constexpr int NCOL = DIM + (W ? 1 : 0);
     using Sink_t = typename SinkOf<SINK, W>::T;
     Sink_t sink;
-    if constexpr (SINK == SINK_GLOBAL) sink.pp = &p;
-    if constexpr (SINK == SINK_CACHE) sink.pp = &p;
+    if constexpr (SINK == SINK_GLOBAL || SINK == SINK_CACHE) sink.bind(p);
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
     else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas, p.wc_off);
     else sink.init(smem, p.G);

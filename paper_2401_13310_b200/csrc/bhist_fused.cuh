@@ -200,7 +200,7 @@ __device__ __forceinline__ void fused_sink(const FusedH &F, int g, double w, boo
             if constexpr (H::W) add2_shared(reinterpret_cast<double2 *>(smem + F.smem_off) + g, s1, s2);
             else atomicAdd(reinterpret_cast<uint32_t *>(smem + F.smem_off) + g, cnt);
         } else if constexpr (!H::W) {
-            atomicAdd(F.count + g, (unsigned long long)cnt);
+            red_u64(F.count + g, (unsigned long long)cnt);
         }
     }
 }
@@ -270,11 +270,11 @@ template <class H, class... Rest> struct Proc<H, Rest...> {
             if constexpr (H::W) {
                 const double *d = reinterpret_cast<const double *>(smem + F.smem_off);
                 for (int i = tig; i < 2 * F.G; i += ntg)
-                    if (d[i] != 0.0) atomicAdd(F.sw + i, d[i]);
+                    if (d[i] != 0.0) red_f64(F.sw + i, d[i]);
             } else {
                 const uint32_t *c = reinterpret_cast<const uint32_t *>(smem + F.smem_off);
                 for (int i = tig; i < F.G; i += ntg)
-                    if (c[i]) atomicAdd(F.count + i, (unsigned long long)c[i]);
+                    if (c[i]) red_u64(F.count + i, (unsigned long long)c[i]);
             }
         }
         Proc<Rest...>::flush(p, smem, tig, ntg);

@@ -453,9 +453,17 @@ __device__ __forceinline__ void add2_shared(double2 *cell, double w, double w2) 
 // one cell in the SAME warp RED instruction cost one request, the same as one u64 RED
 // (tools/microbench/mb6.cu on 1M random cells: 193 G (w, w^2) pairs/s paired vs 96 G/s with
 // the halves in two instructions; u64 192 G/s).
+// Fire-and-forget float64 add to global memory (RED, no return data; nvcc emitted a returning
+// ATOM for atomicAdd in the paired loop below: one 32-byte response per event through the xbar).
+__device__ __forceinline__ void red_f64(double *addr, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void red_u64(unsigned long long *addr, unsigned long long v) {
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
+}
 __device__ __forceinline__ void red_sw(double *sw, int g, double a, double b) {
-    atomicAdd(sw + 2 * (size_t)g, a);
-    atomicAdd(sw + 2 * (size_t)g + 1, b);
+    red_f64(sw + 2 * (size_t)g, a);
+    red_f64(sw + 2 * (size_t)g + 1, b);
 }
 
 // Warp-cooperative (a, b) adds into the global cells: every lane of `act` calls this; the lanes
@@ -478,7 +486,7 @@ __device__ __forceinline__ void red_sw_pairs(unsigned act, unsigned ib, double *
         const int src = !mine ? lane : ib == 0xffffffffu ? j : (int)__fns(ib, 0, j + 1);
         const int gg = __shfl_sync(act, g, src);
         const double va = __shfl_sync(act, a, src), vb = __shfl_sync(act, b, src);
-        if (mine) atomicAdd(sw + 2 * (size_t)gg + half, half ? vb : va);
+        if (mine) red_f64(sw + 2 * (size_t)gg + half, half ? vb : va);
     }
 }
 
@@ -816,7 +824,7 @@ struct PrivSink {
                     uint32_t v = 0;
                     for (int r = sub; ok && r < R; r += S) v += reinterpret_cast<const uint32_t *>(s + r * stride)[i];
                     for (int o = S / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    if (ok && sub == 0 && v) atomicAdd(p.count + i, (unsigned long long)v);
+                    if (ok && sub == 0 && v) red_u64(p.count + i, (unsigned long long)v);
                 }
             }
             return;
@@ -825,13 +833,13 @@ struct PrivSink {
             for (int i = threadIdx.x; i < 2 * G; i += blockDim.x) {
                 double v = reinterpret_cast<const double *>(s)[i];
                 for (int r = 1; r < R; ++r) v += reinterpret_cast<const double *>(s + r * stride)[i];
-                if (v != 0.0) atomicAdd(p.sw + i, v);
+                if (v != 0.0) red_f64(p.sw + i, v);
             }
         } else {
             for (int i = threadIdx.x; i < G; i += blockDim.x) {
                 uint32_t v = reinterpret_cast<const uint32_t *>(s)[i];
                 for (int r = 1; r < R; ++r) v += reinterpret_cast<const uint32_t *>(s + r * stride)[i];
-                if (v) atomicAdd(p.count + i, (unsigned long long)v);
+                if (v) red_u64(p.count + i, (unsigned long long)v);
             }
         }
     }
@@ -839,14 +847,18 @@ struct PrivSink {
 
 template <bool W>
 struct GlobalSink {
-    const FillP *pp;
+    // the global state's pointers, copied out of the kernel parameters (a pointer to the
+    // parameters would make nvcc copy them to local memory and emit generic atomics)
+    double *sw;
+    unsigned long long *count;
+    __device__ __forceinline__ void bind(const FillP &p) { sw = p.sw; count = p.count; }
     __device__ __forceinline__ void init(unsigned char *, int) {}
     __device__ __forceinline__ void add(int g, double w) {
         if (W) {
             const unsigned act = __activemask();
-            red_sw_pairs(act, act, pp->sw, g, w, w * w);
+            red_sw_pairs(act, act, sw, g, w, w * w);
         } else {
-            atomicAdd(pp->count + g, 1ull);
+            red_u64(count + g, 1ull);
         }
     }
     __device__ __forceinline__ void drain() {}
@@ -864,7 +876,9 @@ struct CacheSink {
     uint32_t *keys;
     unsigned char *vals;
     int S;
-    const FillP *pp;
+    double *sw;                          // the global state (see GlobalSink::bind)
+    unsigned long long *count;
+    __device__ __forceinline__ void bind(const FillP &p) { sw = p.sw; count = p.count; }
     static constexpr uint32_t kEmpty = 0xffffffffu;
     __device__ __forceinline__ void init(unsigned char *s, int slots) {
         S = slots;
@@ -930,7 +944,7 @@ struct CacheSink {
         }
         const int sl = lookup((uint32_t)g);
         if (sl >= 0) atomicAdd(reinterpret_cast<uint32_t *>(vals) + sl, c);
-        else atomicAdd(pp->count + g, (unsigned long long)c);
+        else red_u64(count + g, (unsigned long long)c);
     }
     __device__ __forceinline__ void add(int g, double w) {
         if (W && lw.add(g, w)) return;
@@ -976,7 +990,7 @@ struct CacheSink {
                 const uint32_t c = (uint32_t)__popc(peers);
                 const int sl = lookup((uint32_t)g);
                 if (sl >= 0) atomicAdd(reinterpret_cast<uint32_t *>(vals) + sl, c);
-                else atomicAdd(pp->count + g, (unsigned long long)c);
+                else red_u64(count + g, (unsigned long long)c);
             }
         }
     }
@@ -1009,13 +1023,13 @@ struct CacheSink {
                 else glob = true;
             }
         }
-        red_sw_pairs(act0, __ballot_sync(act0, glob), pp->sw, g, s1, s2);
+        red_sw_pairs(act0, __ballot_sync(act0, glob), sw, g, s1, s2);
     }
     // a weighted group sum into its shared-memory slot, or straight to the global cell
     __device__ __forceinline__ void put(int g, double s1, double s2) {
         const int sl = lookup((uint32_t)g);
         if (sl >= 0) add2_shared(reinterpret_cast<double2 *>(vals) + sl, s1, s2);
-        else red_sw(pp->sw, g, s1, s2);
+        else red_sw(sw, g, s1, s2);
     }
     __device__ __forceinline__ void drain() {
         if (!W && BH_LANE_CACHE_U && un) {
@@ -1035,7 +1049,7 @@ struct CacheSink {
         if (wsm) {                       // the box -> global, once per CTA
             const uint32_t *wc = reinterpret_cast<const uint32_t *>(__cvta_shared_to_generic(wsm));
             for (int i = threadIdx.x; i < wx * wy; i += blockDim.x)
-                if (wc[i]) atomicAdd(p.count + (wx0 + i % wx) + (size_t)wst * (wy0 + i / wx), (unsigned long long)wc[i]);
+                if (wc[i]) red_u64(p.count + (wx0 + i % wx) + (size_t)wst * (wy0 + i / wx), (unsigned long long)wc[i]);
         }
         for (int i = threadIdx.x; i < S; i += blockDim.x) {
             const uint32_t k = keys[i];
@@ -1045,7 +1059,7 @@ struct CacheSink {
                 red_sw(p.sw, (int)k, d.x, d.y);
             } else {
                 const uint32_t v = reinterpret_cast<const uint32_t *>(vals)[i];
-                if (v) atomicAdd(p.count + k, (unsigned long long)v);
+                if (v) red_u64(p.count + k, (unsigned long long)v);
             }
         }
     }
@@ -1102,8 +1116,7 @@ __global__ void __launch_bounds__((FillThreads<SINK, DIM, W>::v), SINK == SINK_G
     if (gated_off(p.gate, p.gate_run)) return;          // (uniform: the whole grid exits)
     using Sink_t = typename SinkOf<SINK, W>::T;
     Sink_t sink;
-    if constexpr (SINK == SINK_GLOBAL) sink.pp = &p;
-    if constexpr (SINK == SINK_CACHE) sink.pp = &p;
+    if constexpr (SINK == SINK_GLOBAL || SINK == SINK_CACHE) sink.bind(p);
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
     else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas, p.wc_off);
     else sink.init(smem, p.G);
@@ -1229,7 +1242,7 @@ __global__ void __launch_bounds__((ThreadsOf<SINK>::v), SINK == SINK_GLOBAL ? 2 
     extern __shared__ __align__(16) unsigned char smem[];
     using Sink_t = typename SinkOf<SINK, W>::T;
     Sink_t sink;
-    if constexpr (SINK == SINK_GLOBAL || SINK == SINK_CACHE) sink.pp = &p;
+    if constexpr (SINK == SINK_GLOBAL || SINK == SINK_CACHE) sink.bind(p);
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
     else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas, p.wc_off);
     else sink.init(smem, p.G);
@@ -1363,7 +1376,7 @@ __global__ void __launch_bounds__(ThreadsOf<SINK>::v, SINK == SINK_GLOBAL ? 2 : 
     extern __shared__ __align__(16) unsigned char smem[];
     using Sink_t = typename SinkOf<SINK, W>::T;
     Sink_t sink;
-    if constexpr (SINK == SINK_GLOBAL || SINK == SINK_CACHE) sink.pp = &p;
+    if constexpr (SINK == SINK_GLOBAL || SINK == SINK_CACHE) sink.bind(p);
     if constexpr (SINK == SINK_CACHE) sink.init(smem, p.cache_slots);
     else if constexpr (SINK == SINK_PRIV || SINK == SINK_PRIVA) sink.init(smem, p.G, p.replicas, p.wc_off);
     else sink.init(smem, p.G);
@@ -1671,11 +1684,11 @@ __global__ void __launch_bounds__(1024, 1) k_fill_multi(const __grid_constant__ 
         if (H.weighted) {
             const double *d = reinterpret_cast<const double *>(smem + H.smem_off);
             for (int i = threadIdx.x; i < 2 * H.G; i += T)
-                if (d[i] != 0.0) atomicAdd(H.sw + i, d[i]);
+                if (d[i] != 0.0) red_f64(H.sw + i, d[i]);
         } else {
             const uint32_t *c = reinterpret_cast<const uint32_t *>(smem + H.smem_off);
             for (int i = threadIdx.x; i < H.G; i += T)
-                if (c[i]) atomicAdd(H.count + i, (unsigned long long)c[i]);
+                if (c[i]) red_u64(H.count + i, (unsigned long long)c[i]);
         }
     }
     // stats: per-thread columns -> block partials (fixed order) -> last CTA, fixed order

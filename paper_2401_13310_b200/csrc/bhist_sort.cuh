@@ -729,11 +729,11 @@ __global__ void __launch_bounds__(kReduceThreads, kReduceCtas) k_part_reduce(Fil
             const double *d = reinterpret_cast<const double *>(smem);
             double *o = p.sw + 2 * (size_t)gb0;
             for (int i = threadIdx.x; i < 2 * nb; i += kReduceThreads)
-                if (d[i] != 0.0) atomicAdd(o + i, d[i]);
+                if (d[i] != 0.0) red_f64(o + i, d[i]);
         } else {
             const uint32_t *cc = reinterpret_cast<const uint32_t *>(smem);
             for (int i = threadIdx.x; i < nb; i += kReduceThreads)
-                if (cc[i]) atomicAdd(p.count + gb0 + i, (unsigned long long)cc[i]);
+                if (cc[i]) red_u64(p.count + gb0 + i, (unsigned long long)cc[i]);
         }
         __syncthreads();
     }

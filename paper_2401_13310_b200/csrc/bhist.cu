@@ -794,9 +794,36 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
                 for (int i = 1; i < A.nbins; ++i) crowded += cnt[cell[i]] >= 3;
                 compact = crowded <= 0.02 * std::max(1, A.nbins - 1);
             }
+            // log-domain compact cells (positive edges, e.g. log-spaced): cell = (bits(x) >> lg)
+            // - (bits(e0) >> lg), the finest lg whose cells fit the table; taken when the linear
+            // cells crowd too many edges and these do not
+            int lgc = 0, lcells = 0;
+            if (!compact && A.edges[0] > 0.0 && (A.nbins - 1) < 16384 && !getenv("BHIST_NO_LOG_GUIDE") &&
+                !getenv("BHIST_NO_COMPACT")) {
+                auto bits = [](double v) { long long b; memcpy(&b, &v, 8); return b; };
+                const long long b0 = bits(A.edges[0]), bn = bits(A.edges[A.nbins]);
+                const int maxc = (56 * 1024) / 4 - 1;
+                for (int lg = 8; lg < 62; ++lg) {
+                    const long long cells = (bn >> lg) - (b0 >> lg) + 1;
+                    if (cells > maxc) continue;
+                    std::vector<int> cnt((size_t)cells, 0), cell(A.nbins + 1, 0);
+                    for (int i = 1; i < A.nbins; ++i) {
+                        cell[i] = (int)((bits(A.edges[i]) >> lg) - (b0 >> lg));
+                        ++cnt[cell[i]];
+                    }
+                    int crowded = 0;
+                    for (int i = 1; i < A.nbins; ++i) crowded += cnt[cell[i]] >= 3;
+                    if (crowded <= 0.02 * std::max(1, A.nbins - 1)) { lgc = lg; lcells = (int)cells; }
+                    break;                   // the finest lg that fits decides
+                }
+            }
             if (compact) gc = gc3;
+            if (lgc) { compact = true; gc = lcells; }
             P.gcells = gc;
             P.gscale = (double)gc / (P.xmax - P.xmin);
+            P.lg = lgc;
+            P.kb = 0;
+            if (lgc) { long long b0; memcpy(&b0, &A.edges[0], 8); P.kb = b0 >> lgc; }
             if (!std::isfinite(P.gscale) || !(P.gscale > 0)) return cleanup(fail(BH_EINVAL, "axis %d: edge range too small", a));
             double *de = nullptr;
             uint32_t *dg2 = nullptr;

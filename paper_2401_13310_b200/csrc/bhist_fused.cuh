@@ -85,6 +85,8 @@ __device__ __forceinline__ AxisP ax_const(const AxisP &rt, AxC<N, XMIN, XMAX, D,
     a.g16 = G16;
     a.tab_img = rt.tab_img;
     a.tab_bytes = rt.tab_bytes;
+    a.lg = rt.lg;
+    a.kb = rt.kb;
     return a;
 }
 

@@ -72,6 +72,10 @@ struct AxisP {
     const uint4 *tab_img;    // variable: the shared-memory image [e32 | guide in mode g16] (mode 3: the
                              // compact table alone), built at create
     int32_t tab_bytes;       // its size (multiple of 16)
+    int32_t lg;              // variable: 0 linear guide cells; > 0 log-domain cells (edges > 0): cell =
+    long long kb;            // (bits(x) >> lg) - kb, kb = bits(e[0]) >> lg (positive doubles order as
+                             // their bit patterns, so the cell is monotone in x; log-spaced edges get
+                             // ~1 edge per cell where linear cells crowd them, e.g. C5's H3)
 };
 
 struct FillP {
@@ -134,6 +138,10 @@ __device__ __forceinline__ int find_bin_fixed(const AxisP &a, double x) {
 // monotone, gscale > 0, truncation and min are monotone).  The same function
 // builds the table, so the table is exact for it.
 __device__ __forceinline__ int guide_cell(const AxisP &a, double x) {
+    if (a.lg) {                          // log domain: x >= e[0] > 0, so the key is >= 0
+        const long long k = (__double_as_longlong(x) >> a.lg) - a.kb;
+        return k < a.gcells - 1 ? (int)k : a.gcells - 1;
+    }
     const double t = __dmul_rn(__dsub_rn(x, a.xmin), a.gscale);
     const int c = (int)t;               // cvt.rzi saturates; t >= 0
     return c < a.gcells - 1 ? c : a.gcells - 1;
@@ -203,6 +211,13 @@ __device__ __forceinline__ int find_bin_var_smem(const AxisP &a, double x, const
 // ~cnt/256 of the events) or a cell of >= 3 edges reads the float64 edges (global, L1/L2
 // resident).  One LDS.32 per event instead of the guide load plus the float32 edge search.
 __device__ __forceinline__ int compact_cell(const AxisP &a, double x, int &q) {
+    if (a.lg) {                          // log domain (lg >= 8): the next 8 bits are the position
+        const long long k = (__double_as_longlong(x) >> (a.lg - 8)) - (a.kb << 8);
+        int c = (int)(k >> 8);
+        q = (int)(k & 255);
+        if (k >= ((long long)a.gcells << 8)) { c = a.gcells - 1; q = 255; }
+        return c;
+    }
     const double t = __dmul_rn(__dsub_rn(x, a.xmin), a.gscale);
     const int qf = (int)__dmul_rn(t, 256.0);         // floor(256 t); t >= 0 and < ~gcells
     int c = qf >> 8;

@@ -41,6 +41,8 @@ def _axes_under_test():
         "uniform 16383": np.linspace(-1.0, 3.0, 16384),            # largest compact n
         "uniform 20000": np.linspace(0.0, 1.0, 20001),             # too many bins for compact
         "two bins": np.array([0.0, 0.25, 1.0]),
+        "log 1e-3..2": np.geomspace(1e-3, 2.0, 1001),               # log-domain compact cells
+        "log 1e-6..1e6 x 4000": np.geomspace(1e-6, 1e6, 4001),
     }
 
 
@@ -51,6 +53,12 @@ def _coords_for(edges, rng, m=200_000):
     sub = lo + (hi - lo) * (np.arange(0, 2 ** 15 * 256 + 1, 97) / (2 ** 15 * 256))
     xs = [rng.uniform(lo - 0.05 * (hi - lo), hi + 0.05 * (hi - lo), m), _near(edges), _near(sub, 2),
           np.array([np.nan, np.inf, -np.inf, -0.0, 0.0, 1e308, -1e308])]
+    if lo > 0:   # log-domain cells: IEEE bit-pattern cell and sub-cell (1/256) boundaries +-2 ulps
+        b0, bn = np.array([lo, hi]).view(np.int64)
+        for sh in (34, 42):
+            ks = np.arange(b0 >> sh, (bn >> sh) + 2, dtype=np.int64)
+            xs.append(_near((ks << sh).view(np.float64), 2))
+        xs.append(np.exp(rng.uniform(np.log(lo) - 0.1, np.log(hi) + 0.1, m // 2)))
     return np.concatenate(xs)
 
 

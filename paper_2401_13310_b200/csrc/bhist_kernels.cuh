@@ -668,6 +668,9 @@ constexpr int kHotTabSmem = kHotSlots * 8 + kHotW * 4;     // staged table + cel
 __host__ __device__ constexpr size_t hot_smem_bytes(int threads) { return kHotTabSmem + (size_t)kHotW * 16 * threads; }
 __host__ __device__ __forceinline__ int hot_slot(int g) { return (int)(((uint32_t)g * 2654435761u) >> 26); }
 
+#ifndef BH_HOT_PLAIN
+#define BH_HOT_PLAIN 0      // 1: C5 4.36 vs 4.33 ms (H7 1.31 vs 1.24): the adaptive sink stays
+#endif
 template <bool B, class T, class F> struct PickT { using type = T; };   // (NVRTC: no <type_traits>)
 template <class T, class F> struct PickT<false, T, F> { using type = F; };
 struct NoLaneWindow {
@@ -730,6 +733,10 @@ struct PrivSink {
     // lane-private window of hot cells (see HotTab); an empty member unless W && ADAPT (a
     // LaneWindow in the plain sink made nvcc keep the kernel parameters in local memory)
     typename PickT<W && ADAPT, LaneWindow, NoLaneWindow>::type lw;
+    __device__ __forceinline__ bool lw_active() const {
+        if constexpr (W && ADAPT) return lw.hn != 0;
+        else return false;
+    }
     static constexpr int kCell = W ? 16 : 4;
     static __device__ __forceinline__ size_t stride_of(int G) { return ((size_t)G * kCell + 15) & ~size_t(15); }
     __device__ __forceinline__ void init(unsigned char *s, int G, int R, int wc_off = -1) {
@@ -757,7 +764,9 @@ struct PrivSink {
 #ifdef BH_EXP_NOCAS   // experiment only (wrong results): plain read-modify-write instead of CAS
             { double2 v = base[g]; v.x += w; v.y += w * w; base[g] = v; return; }
 #endif
-            if (!ADAPT) {
+            // BH_HOT_PLAIN: with a lane window the remaining (colder) cells take the plain
+            // exchange add instead of the collision-adaptive machinery
+            if (!ADAPT || (BH_HOT_PLAIN && lw_active())) {
                 add2_shared(base + g, w, w * w);
                 return;
             }

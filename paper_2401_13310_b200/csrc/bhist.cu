@@ -426,10 +426,17 @@ bool win_plan(const bh_hist *h, int64_t n, FillPlan &pw, size_t &off, int &amax)
     return amax >= 1024;
 }
 
+// Smallest fill the AUTO probes look at: `dflt`, or BHIST_AUTO_MIN_EVENTS (sanitizer runs and
+// tests of the decisions on small inputs); never below two probe samples per event run.
+int64_t auto_min_events(int64_t dflt) {
+    const char *e = getenv("BHIST_AUTO_MIN_EVENTS");
+    return std::max<int64_t>(e ? atoll(e) : dflt, 2 * (int64_t)kProbeSamples);
+}
+
 const int32_t *auto_gate(bh_hist *h, int64_t n, const double *const *coords, bool weighted, cudaStream_t s) {
     if (h->strategy != BH_STRATEGY_AUTO || resolve_strategy(h, weighted) != BH_STRATEGY_CACHE) return nullptr;
     const int P = (int)sort_partitions(h, false);
-    if (P > kPartMaxP || n < 8LL * h->nsm * (1LL << sort_pb(false))) return nullptr;
+    if (P > kPartMaxP || n < auto_min_events(8LL * h->nsm * (1LL << sort_pb(false)))) return nullptr;
     if (getenv(weighted ? "BHIST_NO_AUTO_GLOBAL" : "BHIST_NO_AUTO_SORT")) return nullptr;
     if (!h->probe_dev) {
         if (cudaMalloc(reinterpret_cast<void **>(&h->probe_dev), 8 * sizeof(unsigned int)) != cudaSuccess) {
@@ -478,7 +485,7 @@ constexpr int kHotCacheSlots = 4096;       // CACHE's slots next to the lane win
 const HotTab *auto_hot(bh_hist *h, int64_t n, const double *const *coords, const FillPlan &pl,
                        const int32_t *gdec, cudaStream_t s) {
     const bool priva = pl.c.strategy == BH_STRATEGY_PRIV && pl.wc_off >= 0;
-    if (h->strategy != BH_STRATEGY_AUTO || !(priva || pl.c.strategy == BH_STRATEGY_CACHE) || n < kHotMinEvents ||
+    if (h->strategy != BH_STRATEGY_AUTO || !(priva || pl.c.strategy == BH_STRATEGY_CACHE) || n < auto_min_events(kHotMinEvents) ||
         getenv("BHIST_NO_HOT_WINDOW"))
         return nullptr;
     if (!h->hot_dev) {

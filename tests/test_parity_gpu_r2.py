@@ -583,3 +583,28 @@ def test_auto_window_unit_matches_oracle(case):
     a, b = outs
     assert np.array_equal(a["content"], b["content"]) and a["stats"].tobytes() == b["stats"].tobytes()
     compare(a, {k: 2 * v for k, v in ref.items()}, False, f"AUTO window {case}")
+
+
+# ------------------------------------------------------------------ every AUTO-gated kernel on small inputs
+@pytest.mark.parametrize("name,hidx", [("C3", 0), ("C3W", 0), ("C4", 0), ("C4W", 0), ("C5", 6), ("C5", 7),
+                                       ("C5", 5), ("C5", 1)])
+@pytest.mark.parametrize("n", [40_009, 100_003])
+def test_auto_probe_paths_small_inputs(name, hidx, n, monkeypatch):
+    """With BHIST_AUTO_MIN_EVENTS=1 the device probes and their gated kernels (SORT, GLOBAL
+    paired REDs, the unit WINDOW box, CACHE / PRIVA + lane window) run on small, ragged fills;
+    two fills plus a misaligned third equal the oracle (counts exact, sums within 1e-12)."""
+    monkeypatch.setenv("BHIST_AUTO_MIN_EVENTS", "1")
+    wl = bhgen.workload(name, n)
+    hist = wl.hists[hidx]
+    cols = [wl.column(c, 0, n) for c in hist.cols]
+    w = wl.column(wl.wcol, 0, n) if hist.weighted else None
+    h = pkg.Histogram(oracle.oracle_axes(hist))
+    tc = [_t(c) for c in cols]
+    tw = _t(w) if w is not None else None
+    h.fill(tc, tw)
+    h.fill(tc, tw)
+    h.fill([c[1:] for c in tc], tw[1:] if tw is not None else None)      # peeled / misaligned path
+    ref = oracle.OracleHist(oracle.oracle_axes(hist))
+    ref.fill(cols, w).fill(cols, w).fill([c[1:] for c in cols], w[1:] if w is not None else None)
+    compare(h.read(), ref.read(), hist.weighted, f"{name} H{hidx} n={n}")
+    h.close()

@@ -54,6 +54,27 @@ H = pkg.Histogram([(100, 0.0, 1.0)])
 H.fill([x], w)
 H.read()
 H.close()
+# AUTO's device probes and the kernels they gate, on small inputs (BHIST_AUTO_MIN_EVENTS):
+# GLOBAL paired REDs (C3W), CACHE + lane window (C4W), PRIVA + lane window (C5 H7), the unit
+# WINDOW box (C5 H6, and a 1-D 200k-bin Gaussian), SORT (C3)
+os.environ["BHIST_AUTO_MIN_EVENTS"] = "1"
+na = 40_009
+for name, hidx in (("C3W", 0), ("C4W", 0), ("C5", 7), ("C5", 6), ("C3", 0)):
+    wl = bhgen.workload(name, na)
+    h = wl.hists[hidx]
+    cols = [torch.from_numpy(wl.column(c, 0, na)).to(dev) for c in h.cols]
+    w = torch.from_numpy(wl.column(wl.wcol, 0, na)).to(dev) if h.weighted else None
+    H = pkg.Histogram(h.axes_spec())
+    H.fill(cols, w)
+    H.fill(cols, w)
+    H.read()
+    H.close()
+xg = torch.from_numpy(rng.normal(0.5, 0.15, na)).to(dev)
+H = pkg.Histogram([(200_000, 0.0, 1.0)])
+H.fill([xg])
+H.read()
+H.close()
+del os.environ["BHIST_AUTO_MIN_EVENTS"]
 # fused multi-histogram fill and the host path
 wl = bhgen.workload("C5", n)
 cols = [torch.from_numpy(wl.column(c, 0, n)).to(dev) for c in range(len(wl.columns))]

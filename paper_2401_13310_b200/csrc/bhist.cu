@@ -119,7 +119,7 @@ size_t sink_bytes(const bh_hist *h, int strategy, bool weighted, int slots = 0) 
 // Bytes of shared memory the variable-axis tables take (float32 edges + guide).
 size_t axis_table_bytes(const AxisP &a) {
     if (!a.var) return 0;
-    if (a.g16 == 3) return align16(4 * (size_t)(a.gcells + 1));
+    if (a.g16 >= 3) return align16(4 * (size_t)(a.gcells + 1));
     return align16(4 * (size_t)(a.n + 1)) + align16((a.g16 ? 2 : 4) * (size_t)(a.gcells + 1));
 }
 
@@ -846,7 +846,7 @@ bh_status bh_create(int32_t dim, const bh_axis *axes, int32_t device, bh_hist **
             P.e = de;
             P.guide = dg2;
             P.e32 = de32;
-            P.g16 = compact ? 3 : (A.nbins - 1) < 16384 ? 2 : ((A.nbins - 1) < 65536 ? 1 : 0);
+            P.g16 = compact ? (lgc ? 4 : 3) : (A.nbins - 1) < 16384 ? 2 : ((A.nbins - 1) < 65536 ? 1 : 0);
             k_build_guide<<<(gc + 1 + 255) / 256, 256>>>(P, dg2);
             k_edges_f32<<<(A.nbins + 1 + 255) / 256, 256>>>(de, A.nbins + 1, de32);
             unsigned char *img = nullptr;

@@ -68,7 +68,8 @@ struct AxisP {
     int32_t tab_off;         // variable + VSM: byte offset of [e32 | guide] in dynamic smem
     int32_t g16;             // variable + VSM: guide staged as uint32 (0), uint16 (1, n-1 < 65536) or
                              // packed uint16 (2, n-1 < 16384): guide[c] << 2 | min(guide[c+1]-guide[c], 3);
-                             // 3: compact table, no float32 edges (see find_bin_var_compact)
+                             // 3: compact table, no float32 edges (see find_bin_var_compact);
+                             // 4: the same with log-domain cells (lg > 0)
     const uint4 *tab_img;    // variable: the shared-memory image [e32 | guide in mode g16] (mode 3: the
                              // compact table alone), built at create
     int32_t tab_bytes;       // its size (multiple of 16)
@@ -210,8 +211,9 @@ __device__ __forceinline__ int find_bin_var_smem(const AxisP &a, double x, const
 // q(x) > q(e_i) implies x > e_i and q(x) < q(e_i) implies x < e_i; only an equal q (a tie,
 // ~cnt/256 of the events) or a cell of >= 3 edges reads the float64 edges (global, L1/L2
 // resident).  One LDS.32 per event instead of the guide load plus the float32 edge search.
-__device__ __forceinline__ int compact_cell(const AxisP &a, double x, int &q) {
-    if (a.lg) {                          // log domain (lg >= 8): the next 8 bits are the position
+template <bool LOG = false>              // LOG: log-domain cells (g16 == 4), a compile-time mode so
+__device__ __forceinline__ int compact_cell(const AxisP &a, double x, int &q) {   // C2's kernel carries no log path
+    if (LOG) {                           // log domain (lg >= 8): the next 8 bits are the position
         const long long k = (__double_as_longlong(x) >> (a.lg - 8)) - (a.kb << 8);
         int c = (int)(k >> 8);
         q = (int)(k & 255);
@@ -239,13 +241,13 @@ static __device__ __noinline__ int compact_slow(const double *e, double x, const
     return 1 + l;
 }
 
-template <bool CHECK_RANGE = true>
+template <bool CHECK_RANGE = true, bool LOG = false>
 __device__ __forceinline__ int find_bin_var_compact(const AxisP &a, double x, const unsigned char *tabc) {
     if (x < a.xmin) return 0;
     if (!(x < a.xmax)) return a.n + 1;
     const uint32_t *tab = reinterpret_cast<const uint32_t *>(tabc);
     int q;
-    const int c = compact_cell(a, x, q);
+    const int c = compact_cell<LOG>(a, x, q);
     const uint32_t v = tab[c];
     const int lo = (int)(v & 0x3fffu), cnt = (int)((v >> 14) & 3u);
     const int p1 = (int)((v >> 16) & 255u), p2 = (int)(v >> 24);
@@ -256,6 +258,7 @@ __device__ __forceinline__ int find_bin_var_compact(const AxisP &a, double x, co
 
 __device__ __forceinline__ int find_bin_var_smem_any(const AxisP &a, double x, const unsigned char *tab) {
     if (a.g16 == 3) return find_bin_var_compact(a, x, tab);
+    if (a.g16 == 4) return find_bin_var_compact<true, true>(a, x, tab);
     return a.g16 == 2 ? find_bin_var_smem<2>(a, x, tab)
                       : (a.g16 ? find_bin_var_smem<1>(a, x, tab) : find_bin_var_smem<0>(a, x, tab));
 }
@@ -1769,14 +1772,15 @@ __global__ void k_edges_f32(const double *e, int n, float *e32) {
 // mode a.g16]; the packed mode stores guide[c] << 2 | min(guide[c+1] - guide[c], 3).
 __global__ void k_table_image(AxisP a, const uint32_t *guide, unsigned char *img) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a.g16 == 3) {                    // compact: one word per cell, no float32 edges
+    if (a.g16 >= 3) {                    // compact: one word per cell, no float32 edges
         if (i <= a.gcells) {
             const uint32_t lo = guide[i];
             const uint32_t cnt = i < a.gcells ? guide[i + 1] - lo : 0u;
             uint32_t v = lo | (cnt < 3u ? cnt : 3u) << 14;
             int q;
-            if (cnt >= 1) { compact_cell(a, a.e[lo + 1], q); v |= (uint32_t)q << 16; }
-            if (cnt >= 2) { compact_cell(a, a.e[lo + 2], q); v |= (uint32_t)q << 24; }
+            auto qpos = [&](double e) { if (a.g16 == 4) compact_cell<true>(a, e, q); else compact_cell<false>(a, e, q); };
+            if (cnt >= 1) { qpos(a.e[lo + 1]); v |= (uint32_t)q << 16; }
+            if (cnt >= 2) { qpos(a.e[lo + 2]); v |= (uint32_t)q << 24; }
             reinterpret_cast<uint32_t *>(img)[i] = v;
         }
         return;

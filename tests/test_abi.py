@@ -41,6 +41,29 @@ def test_kernels_are_sm100a_sass():
     assert "sm_100a" in out
 
 
+def test_hot_kernels_use_no_local_memory():
+    """The bench headline kernel (C2: k_fill<1, weighted, PRIV, vector, compact>) and the
+    GLOBAL / unit-CACHE kernels keep the kernel parameters out of local memory: a reference or
+    pointer into FillP made nvcc copy it to local memory (STL at entry, generic returning
+    atomics, +9% instructions on C2)."""
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _build.SO], capture_output=True, text=True).stdout
+    funcs = {}
+    name = None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            name = m.group(1)
+            funcs[name] = []
+        elif name:
+            funcs[name].append(line)
+    for k in ("_ZN2bh6k_fillILi1ELb1ELi0ELb1ELi3EEEvNS_5FillPE",      # C2
+              "_ZN2bh6k_fillILi2ELb1ELi1ELb1ELi0EEEvNS_5FillPE",      # C3w GLOBAL
+              "_ZN2bh6k_fillILi2ELb0ELi2ELb1ELi0EEEvNS_5FillPE"):     # C5 H6 unit CACHE / WINDOW
+        body = "\n".join(funcs[k])
+        assert not re.search(r"\b(STL|LDL)\b", body), k
+        assert "ATOM.E.ADD" not in body, k                           # no generic returning atomics
+
+
 def test_no_cpu_fallback_without_gpu():
     import torch
     if torch.cuda.is_available():

@@ -547,7 +547,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
         FillP p = make_params(h, m, cs, ws);
         for (int a = 0; a < h->dim; ++a) p.ax[a] = pl.ax[a];
         p.gate = gate;                                        // CACHE, run iff the flag is 0
-        p.gate_run = 0;
+        p.gate_run = gate_bit(0);
         // vector path: every column must share the same 16-byte phase
         const uintptr_t ph = reinterpret_cast<uintptr_t>(cs[0]) & 15;
         c.vec = (ph % 8) == 0;
@@ -566,7 +566,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
             pq.cache_slots = kWinSlots;
             pq.win = h->probe_dev + 4;
             pq.win_off = (int32_t)win_off;
-            pq.gate_run = 2;
+            pq.gate_run = gate_bit(2);
             LaunchCfg cw = pwin.c;
             cw.smem = win_off + 4 * (size_t)win_amax;
             cw.vec = c.vec;
@@ -584,7 +584,7 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
             pq.hot = hot;
             pq.hot_off = (int32_t)align16(phot.c.smem);
             pq.gate = &hot->flag;
-            pq.gate_run = 2;
+            pq.gate_run = gate_bit(2);
             LaunchCfg ch = phot.c;
             ch.smem = pq.hot_off + hot_bytes;
             ch.vec = c.vec;
@@ -597,12 +597,14 @@ bh_status fill_device(bh_hist *h, int64_t n, const double *const *coords, const 
             if (e != cudaSuccess) return fail(BH_ECUDA, "fill launch: %s", cudaGetErrorString(e));
             ++h->launches;
             p.gate = &hot->flag;
-            p.gate_run = 0;
+            // the plain sink also runs for every word whose kernel this fill does not launch (the
+            // probe decided once, on an earlier fill that may have had other candidates)
+            p.gate_run = gate_bit(0) | (gate && w ? 0 : gate_bit(1));
         }
         if (gate && w) {                                      // weighted AUTO: the gated GLOBAL fill first
             FillP pq = p;
             for (int a = 0; a < h->dim; ++a) pq.ax[a] = pg.ax[a];
-            pq.gate_run = 1;
+            pq.gate_run = gate_bit(1);
             LaunchCfg &cg = pg.c;
             cg.vec = c.vec;
             cg.grid = grid_for(h, cg, m);

@@ -101,14 +101,18 @@ struct FillP {
     unsigned long long *entries; // running entries
     int64_t entries_add;         // added to *entries by the last CTA
     const int32_t *gate;         // AUTO's device-side strategy decision: the kernel runs only if
-    int32_t gate_run;            // gate == nullptr or *gate == gate_run (otherwise every CTA exits)
+    int32_t gate_run;            // bit mask: run iff gate == nullptr or bit *gate of gate_run is set
+                                 // (otherwise every CTA exits at once)
     const unsigned int *win;     // unit CACHE: the probe's dense box (x0, wx, y0, wy) of bins kept as
     int32_t win_off;             // shared-memory u32 counts at byte win_off (nullptr: none)
     int32_t hot_off;             // weighted PRIVA / CACHE: byte offset of the lane window in shared memory
     const struct HotTab *hot;    // the lane-private window of hot cells (nullptr: none)
 };
 
-__device__ __forceinline__ bool gated_off(const int32_t *gate, int32_t run) { return gate && __ldcg(gate) != run; }
+__device__ __forceinline__ bool gated_off(const int32_t *gate, int32_t mask) {
+    return gate && !((mask >> (__ldcg(gate) & 31)) & 1);
+}
+__host__ __device__ constexpr int32_t gate_bit(int v) { return 1 << v; }
 
 // ------------------------------------------------------------------ FindBin
 // Fixed axis: b = 1 + floor(n*(x-xmin)/(xmax-xmin)), evaluated as

@@ -94,7 +94,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // partial or whose columns are not 16-byte aligned are loaded by the threads instead.
 template <int DIM, bool W, int VM, int RC>
 __global__ void __launch_bounds__(kPartThreads, 1) k_part_scatter(FillP p, PartP q) {
-    if (gated_off(q.gate, 1)) return;
+    if (gated_off(q.gate, gate_bit(1))) return;
     constexpr int NCOL = DIM + (W ? 1 : 0);
     constexpr int kEv = part_ev(DIM, W);
     constexpr int kTile = kPartThreads * kEv;
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(1024, 1) k_hot_probe(FillP p, int samples, con
 // One warp: cp = exclusive prefix of cnt (records per partition); cnt is zeroed for
 // the next chunk.
 __global__ void k_part_plan(PartP q) {
-    if (gated_off(q.gate, 1)) return;
+    if (gated_off(q.gate, gate_bit(1))) return;
     const int lane = threadIdx.x;
     unsigned long long run = 0;
     for (int c0 = 0; c0 < q.P; c0 += 32) {
@@ -584,7 +584,7 @@ constexpr int kReduceBatch = 2048;                   // tiles whose segments are
 // still keeps all 32 warps busy), walking the segments in order.
 template <bool W, int RC>
 __global__ void __launch_bounds__(kReduceThreads, kReduceCtas) k_part_reduce(FillP p, PartP q) {
-    if (gated_off(q.gate, 1)) return;
+    if (gated_off(q.gate, gate_bit(1))) return;
     extern __shared__ __align__(16) unsigned char smem[];
     // layout: [bins (2^pb cells)] [o0 u32[batch]] [cp u32[batch+1]] [scan scratch u32[32]]
     const size_t binbytes = (size_t)(W ? 16 : 4) << q.pb;

@@ -608,3 +608,24 @@ def test_auto_probe_paths_small_inputs(name, hidx, n, monkeypatch):
     ref.fill(cols, w).fill(cols, w).fill([c[1:] for c in cols], w[1:] if w is not None else None)
     compare(h.read(), ref.read(), hist.weighted, f"{name} H{hidx} n={n}")
     h.close()
+
+
+@pytest.mark.slow
+def test_auto_decision_then_smaller_fills_with_fewer_candidates():
+    """The probes decide once (first large fill); a later, smaller fill that launches fewer
+    candidate kernels (C3w: GLOBAL needs >= 39M events, the hot-cell probe only 4M) still
+    runs exactly one sink: the plain kernel takes every word whose kernel is not launched."""
+    n1, n2 = 40_000_003, 5_000_011
+    wl = bhgen.workload("C3W", n1)
+    hist = wl.hists[0]
+    cols = [wl.column(c, 0, n1) for c in hist.cols]
+    w = wl.column(wl.wcol, 0, n1)
+    tc, tw = [_t(c) for c in cols], _t(w)
+    h = pkg.Histogram(oracle.oracle_axes(hist))
+    h.fill(tc, tw)                                   # probes: GLOBAL
+    assert h.strategy(True) == pkg.BH_STRATEGY_GLOBAL
+    h.fill([c[:n2] for c in tc], tw[:n2])            # no GLOBAL candidate: CACHE must run
+    ref = oracle.OracleHist(oracle.oracle_axes(hist))
+    ref.fill(cols, w).fill([c[:n2] for c in cols], w[:n2])
+    compare(h.read(), ref.read(), True, "C3w 40M then 5M")
+    h.close()

@@ -152,7 +152,7 @@ int threads_of(int strategy, bool weighted, int dim = 0) {     // dim: k_fill's 
     if (strategy == BH_STRATEGY_CACHE && weighted && dim == 3) return 768;
     return strategy == BH_STRATEGY_GLOBAL ? kThreadsGlobal : kThreadsSmem;
 }
-int resident_blocks(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? 2 : 1; }
+int resident_blocks(int strategy) { return strategy == BH_STRATEGY_GLOBAL ? kGlobalCtas : 1; }
 
 // Shared-memory plan of one fill: strategy, variable-axis tables (VSM), PRIV replicas.
 struct FillPlan {

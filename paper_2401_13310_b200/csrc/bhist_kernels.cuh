@@ -30,7 +30,11 @@ typedef unsigned long long uintptr_t;
 namespace bh {
 
 constexpr int kMaxDim = 3;
-constexpr int kThreadsGlobal = 512;   // GLOBAL sink: 2 CTAs/SM
+constexpr int kThreadsGlobal = 512;   // GLOBAL sink: kGlobalCtas CTAs/SM
+#ifndef BH_GLOBAL_CTAS
+#define BH_GLOBAL_CTAS 2
+#endif
+constexpr int kGlobalCtas = BH_GLOBAL_CTAS;   // k_fill's GLOBAL CTAs per SM (launch bounds + grid)
 #ifndef BH_SMEM_THREADS
 #define BH_SMEM_THREADS 1024
 #endif
@@ -1142,7 +1146,7 @@ struct Batch {            // U event pairs of every column, held in registers (x
 // leading events; the next batch is loaded before the current one is processed
 // (register double-buffering) so each thread keeps 2*U*ncol 16-byte loads in flight.
 template <int DIM, bool W, int SINK, bool VEC, int VM>
-__global__ void __launch_bounds__((FillThreads<SINK, DIM, W>::v), SINK == SINK_GLOBAL ? 2 : 1) k_fill(FillP p) {
+__global__ void __launch_bounds__((FillThreads<SINK, DIM, W>::v), SINK == SINK_GLOBAL ? kGlobalCtas : 1) k_fill(FillP p) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (gated_off(p.gate, p.gate_run)) return;          // (uniform: the whole grid exits)
     using Sink_t = typename SinkOf<SINK, W>::T;

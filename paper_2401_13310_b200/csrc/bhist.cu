@@ -426,6 +426,18 @@ bool win_plan(const bh_hist *h, int64_t n, FillPlan &pw, size_t &off, int &amax)
     return amax >= 1024;
 }
 
+// Identity of a fill's inputs for AUTO's decisions: the column pointers and the size.
+uint64_t input_key(const bh_hist *h, int64_t n, const double *const *coords) {
+    uint64_t k = 1469598103934665603ull ^ (uint64_t)n;
+    for (int a = 0; a < h->dim; ++a) k = (k ^ reinterpret_cast<uintptr_t>(coords[a])) * 1099511628211ull;
+    return k;
+}
+// After bh_reset (state 2) a decision stands for the same inputs, else it is made again.
+void rearm(int &state, uint64_t &stored, uint64_t key) {
+    if (state == 2) state = key == stored ? 1 : 0;
+    if (state == 0) stored = key;
+}
+
 // Smallest fill the AUTO probes look at: `dflt`, or BHIST_AUTO_MIN_EVENTS (sanitizer runs and
 // tests of the decisions on small inputs); never below two probe samples per event run.
 int64_t auto_min_events(int64_t dflt) {
@@ -444,6 +456,7 @@ const int32_t *auto_gate(bh_hist *h, int64_t n, const double *const *coords, boo
             return nullptr;                                  // no probe: stay on CACHE
         }
     }
+    rearm(h->probe_state, h->probe_key, input_key(h, n, coords));
     if (h->probe_state == 0) {
         FillP p = make_params(h, n, coords, nullptr);
         if (cudaMemsetAsync(h->probe_dev, 0, 8 * sizeof(unsigned int), s) != cudaSuccess) { cudaGetLastError(); return nullptr; }
@@ -494,6 +507,7 @@ const HotTab *auto_hot(bh_hist *h, int64_t n, const double *const *coords, const
             return nullptr;
         }
     }
+    rearm(h->hot_state, h->hot_key, input_key(h, n, coords));
     if (h->hot_state == 0) {
         FillP p = make_params(h, n, coords, nullptr);
         const unsigned int *gd = reinterpret_cast<const unsigned int *>(gdec);
@@ -924,8 +938,9 @@ bh_status bh_reset(bh_hist *h, bh_stream s) {
     CUDA_TRY(cudaGetLastError());
     ++h->launches;
     h->weighted_content = false;
-    h->probe_state = 0;                  // AUTO re-decides SORT vs CACHE on the next large fill
-    h->hot_state = 0;                    // and re-probes the hot-cell window
+    // AUTO re-decides on the next large fill unless it reads the same input buffers (state 2)
+    if (h->probe_state) h->probe_state = 2;
+    if (h->hot_state) h->hot_state = 2;
     return BH_OK;
 }
 
@@ -1741,7 +1756,7 @@ bh_status bh_get_strategy(const bh_hist *h, int32_t weighted, int32_t *strategy)
     *strategy = (weighted && h->strategy == BH_STRATEGY_EXACT) ? BH_STRATEGY_EXACT : resolve_strategy(h, weighted != 0);
     // AUTO's large fills after the probe decided (on the device) for SORT (unit weights) or
     // GLOBAL (weights)
-    if (h->strategy == BH_STRATEGY_AUTO && *strategy == BH_STRATEGY_CACHE && h->probe_state == 1 && h->probe_dev) {
+    if (h->strategy == BH_STRATEGY_AUTO && *strategy == BH_STRATEGY_CACHE && h->probe_state != 0 && h->probe_dev) {
         DeviceGuard dg(h->device);
         unsigned int flag = 0;
         if (cudaMemcpy(&flag, h->probe_dev + (weighted ? 3 : 2), sizeof flag, cudaMemcpyDeviceToHost) != cudaSuccess)

@@ -54,6 +54,9 @@ struct bh_hist {
     // 0 not probed since create/reset, 1 probed (hot_dev->flag on the device gates the kernels)
     bh::HotTab *hot_dev = nullptr;
     int hot_state = 0;
+    // state 2 (after bh_reset): the decision stands for a fill over the SAME input buffers and
+    // size (probe_key / hot_key), and is re-probed for any other
+    uint64_t probe_key = 0, hot_key = 0;
     unsigned int *probe_dev = nullptr;
     std::vector<void *> axis_mem;     // edges and guide tables
     // host->device double buffer

@@ -629,3 +629,34 @@ def test_auto_decision_then_smaller_fills_with_fewer_candidates():
     ref.fill(cols, w).fill([c[:n2] for c in cols], w[:n2])
     compare(h.read(), ref.read(), True, "C3w 40M then 5M")
     h.close()
+
+
+@pytest.mark.slow
+def test_auto_decision_after_reset_follows_the_inputs():
+    """bh_reset keeps AUTO's device decision for fills over the same input buffers (the bench's
+    repeated steps) and makes it again for other buffers: a histogram that chose SORT on
+    uniform data chooses CACHE after a reset and a fill of peaked data; counts stay exact."""
+    n = 40_000_000
+    g = torch.Generator(device=DEV).manual_seed(11)
+    u = [torch.rand(n, dtype=torch.float64, device=DEV, generator=g) for _ in range(2)]
+    pk = [0.505 + 0.002 * torch.tan(np.pi * (torch.rand(n, dtype=torch.float64, device=DEV, generator=g) - 0.5))
+          for _ in range(2)]
+    axes = [(1000, 0.0, 1.0), (1000, 0.0, 1.0)]
+    h = pkg.Histogram(axes)
+    ref = pkg.Histogram(axes, strategy=pkg.BH_STRATEGY_CACHE)
+    h.fill(u)
+    assert h.strategy(False) == pkg.BH_STRATEGY_SORT
+    h.reset()
+    h.fill(u)                                       # same buffers: decision kept
+    assert h.strategy(False) == pkg.BH_STRATEGY_SORT
+    ref.fill(u)
+    assert np.array_equal(h.read()["content"], ref.read()["content"])
+    h.reset()
+    ref.reset()
+    h.fill(pk)                                      # other buffers: decided again
+    ref.fill(pk)
+    assert h.strategy(False) == pkg.BH_STRATEGY_CACHE
+    a, b = h.read(), ref.read()
+    assert np.array_equal(a["content"], b["content"]) and a["entries"] == b["entries"] == n
+    h.close()
+    ref.close()

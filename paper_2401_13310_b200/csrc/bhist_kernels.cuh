@@ -679,6 +679,9 @@ constexpr int kHotTabSmem = kHotSlots * 8 + kHotW * 4;     // staged table + cel
 __host__ __device__ constexpr size_t hot_smem_bytes(int threads) { return kHotTabSmem + (size_t)kHotW * 16 * threads; }
 __host__ __device__ __forceinline__ int hot_slot(int g) { return (int)(((uint32_t)g * 2654435761u) >> 26); }
 
+#ifndef BH_HOT_COLLECTIVE
+#define BH_HOT_COLLECTIVE 1
+#endif
 #ifndef BH_HOT_PLAIN
 #define BH_HOT_PLAIN 0      // 1: C5 4.36 vs 4.33 ms (H7 1.31 vs 1.24): the adaptive sink stays
 #endif
@@ -769,6 +772,27 @@ struct PrivSink {
         lw.init(p.hot, smem + p.hot_off);
     }
     __device__ __forceinline__ void add(int g, double w) {
+#if BH_HOT_COLLECTIVE
+        if (W && ADAPT && lw_active()) {
+            // a window cell goes to this thread's private copy; the lane still takes part in the
+            // warp-collective adaptive add (with no item), so the warp stays converged and the
+            // per-warp hot-bin cache (full warps only) keeps absorbing the warm cells
+            const bool hit = lw.add(g, w);
+            double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
+            const unsigned act = __activemask();
+            const int lane = (int)(threadIdx.x & 31);
+            agg = __any_sync(act, agg);
+            if (agg) {
+                const unsigned peers = __match_any_sync(act, hit ? -1 - lane : g);
+                agg = __any_sync(act, !hit && __popc(peers) >= BH_AGG_STAY);
+                add_aggregated(base, hit ? -1 - lane : g, hit ? 0.0 : w, hit ? 0.0 : w * w, act, peers, !hit);
+            } else {
+                const int lost = hit ? 0 : add2_shared_count(base + g, w, w * w);
+                agg = __popc(__ballot_sync(act, lost > 0)) >= BH_AGG_ENTER;
+            }
+            return;
+        }
+#endif
         if (W && ADAPT && lw.add(g, w)) return;     // a window cell: this thread's private copy
         if (W) {
             double2 *base = reinterpret_cast<double2 *>(__cvta_shared_to_generic(sm));
@@ -802,7 +826,7 @@ struct PrivSink {
     // warp's hot-bin cache -> plain add; miss with a group of >= 2 -> claim the entry (one
     // claimant per entry, the old occupant flushed into the replica); else CAS.
     __device__ __forceinline__ void add_aggregated(double2 *base, int g, double w, double w2, unsigned act,
-                                                   unsigned peers) {
+                                                   unsigned peers, bool item = true) {
         const int lane = (int)(threadIdx.x & 31);
         const int rounds = __reduce_max_sync(act, (unsigned)__popc(peers));
         double s1 = 0.0, s2 = 0.0;
@@ -812,7 +836,7 @@ struct PrivSink {
             const double v1 = __shfl_sync(act, w, src), v2 = __shfl_sync(act, w2, src);
             if (m) { s1 += v1; s2 += v2; m &= m - 1; }
         }
-        const bool leader = lane == __ffs(peers) - 1;
+        const bool leader = item && lane == __ffs(peers) - 1;
         const bool done = hot.absorb(act, leader, __popc(peers), g, s1, s2,
                                      [&](int t, double a1, double a2) { add2_shared(base + t, a1, a2); });
         if (leader && !done) add2_shared(base + g, s1, s2);

@@ -315,11 +315,14 @@ def test_pack_multi_layout_and_roundtrip():
     for h in hs:
         h.reset()
     pkg.bh_unpack_multi(handles, unit, buf.data_ptr(), torch.cuda.current_stream().cuda_stream)
-    for h, r in zip(hs, before):
+    for h, r, u in zip(hs, before, unit):
         a = h.read()
         for k in ("content", "sumw2", "stats"):
             assert np.array_equal(a[k], r[k]), k
         assert a["entries"] == r["entries"]
+        if u:   # a reduced unit-weight state still reads as TH1I counts (reading R18)
+            i32 = h.read(content_type=pkg.BH_CONTENT_I32)
+            assert np.array_equal(i32["content"], r["content"].astype(np.int64))
     with pytest.raises(pkg.BHistError):       # histogram 1 is weighted: no unit packing
         hs[1].fill([cols[1]], w)
         pkg.bh_pack_multi(handles, [True] * len(hs), buf.data_ptr(), torch.cuda.current_stream().cuda_stream)

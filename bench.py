@@ -535,6 +535,22 @@ def run_gpu(args):
             cpu_par = {"value": sample / tp, "unit": UNIT, "cores": threads, "kind": "oracle",
                        "sample": f"the same events sharded over {threads} forked processes (all host cores)"}
 
+    # same-run read ceiling: a plain torch reduction over this step's input columns (measurement
+    # only, outside the timed region), the bandwidth a read-only stream of these bytes reaches here
+    read_gbs = None
+    if rank == 0:
+        torch.cuda.synchronize()
+        tr = []
+        for _ in range(3):
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r0.record()
+            for t in devc:
+                t.sum()
+            r1.record()
+            torch.cuda.synchronize()
+            tr.append(r0.elapsed_time(r1))
+        read_gbs = sum(t.numel() * 8 for t in devc) / (min(tr) * 1e-3) / 1e9
+
     if rank == 0:
         peak, peak_src = hbm_peak()
         bpe = wl.bytes_per_event
@@ -561,7 +577,9 @@ def run_gpu(args):
                          else ("k_part_scatter + k_part_reduce (sort)"
                                                                   if strat == "sort" else f"k_fill ({strat})"),
                          "launch_ms": fill_avg,
-                         "algorithmic_bytes_per_launch": bpe * N, "peak_source": peak_src},
+                         "algorithmic_bytes_per_launch": bpe * N, "peak_source": peak_src,
+                         "read_ceiling_gbs": read_gbs, "frac_of_read_ceiling": achieved / read_gbs if read_gbs else None,
+                         "read_ceiling_source": "torch .sum() over the step's device columns, same run, best of 3"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps, "pcie_gbs": h2d * world * e2e_steps / e2e_s / 1e9 / world,
                     "pcie_peak_gbs": pcie_peak,

@@ -510,6 +510,22 @@ def run_gpu(args):
     pcie_peak = 3 * 8 * nb / (e0.elapsed_time(e1) * 1e-3) / 1e9
     del dst
 
+    # same-run read ceiling: a plain torch reduction over this step's input columns (measurement
+    # only, outside the timed region), the bandwidth a read-only stream of these bytes reaches here
+    read_gbs = None
+    if rank == 0:
+        torch.cuda.synchronize()
+        tr = []
+        for _ in range(3):
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r0.record()
+            for t in devc:
+                t.sum()
+            r1.record()
+            torch.cuda.synchronize()
+            tr.append(r0.elapsed_time(r1))
+        read_gbs = sum(t.numel() * 8 for t in devc) / (min(tr) * 1e-3) / 1e9
+
     # ---- secondary rows (rank 0, N=1): e.g. the 1D fixed-bin target of the north star (C1S)
     secondary = {}
     if rank == 0 and world == 1 and args.secondary:
@@ -534,22 +550,6 @@ def run_gpu(args):
             tp = time_oracle_parallel(wl, sample, threads)
             cpu_par = {"value": sample / tp, "unit": UNIT, "cores": threads, "kind": "oracle",
                        "sample": f"the same events sharded over {threads} forked processes (all host cores)"}
-
-    # same-run read ceiling: a plain torch reduction over this step's input columns (measurement
-    # only, outside the timed region), the bandwidth a read-only stream of these bytes reaches here
-    read_gbs = None
-    if rank == 0:
-        torch.cuda.synchronize()
-        tr = []
-        for _ in range(3):
-            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            r0.record()
-            for t in devc:
-                t.sum()
-            r1.record()
-            torch.cuda.synchronize()
-            tr.append(r0.elapsed_time(r1))
-        read_gbs = sum(t.numel() * 8 for t in devc) / (min(tr) * 1e-3) / 1e9
 
     if rank == 0:
         peak, peak_src = hbm_peak()
